@@ -1,0 +1,173 @@
+/*
+ * rkr.h -- C ABI of the B200-native rk-Rotor chain solver (librkr.so).
+ *
+ * This is the drop-in boundary for the hot path named by BASELINE.json's
+ * north_star: the rk-Rotor chain dynamic program of
+ * /root/reference/proj/include/remat/chain_dp.hpp.  The reference has no FFI
+ * layer of its own (its "operator API" is the header-only C++ API in
+ * namespace remat), so every entry point below cites the C++ interface it
+ * replaces; include/remat_b200/chain_dp.hpp re-exposes that exact C++ API on
+ * top of these calls.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no exceptions cross the ABI.  Every call
+ *    returns an rkr_status; rkr_last_error() gives a thread-local message.
+ *  - Host buffers are caller-owned.  rkr_table owns its device memory.
+ *  - The DP runs on the GPU only.  There is no CPU fallback: on a host
+ *    without a usable sm_100 device every compute call returns RKR_ERR_CUDA.
+ *  - A table handle is immutable after creation; distinct handles may be
+ *    used from distinct threads.
+ */
+#ifndef RKR_H
+#define RKR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RKR_ABI_VERSION 1
+
+/* Mirrors remat::kInfTime (chain_dp.hpp:23). */
+#define RKR_INF_TIME ((int64_t)(INT64_MAX / 4))
+
+typedef enum {
+    RKR_OK = 0,
+    RKR_ERR_INVALID = 1,     /* remat::ValidationError (chain_dp.hpp:33,58,84,94,203) */
+    RKR_ERR_INFEASIBLE = 2,  /* remat::InfeasibleBudget (chain_dp.hpp:214,245,261,285) */
+    RKR_ERR_CUDA = 3,        /* device missing / launch or copy failure */
+    RKR_ERR_OOM = 4,         /* device allocation failed */
+    RKR_ERR_CAPACITY = 5,    /* caller's output buffer too small (size reported) */
+    RKR_ERR_ARGUMENT = 6     /* null pointer / index out of range */
+} rkr_status;
+
+/* DpArg::Kind (chain_dp.hpp:44-47). */
+typedef enum { RKR_ARG_NONE = 0, RKR_ARG_OPTION = 1, RKR_ARG_CUT = 2 } rkr_arg_kind;
+
+/* ScheduleOp::Kind (types.hpp:346-362).  COMPUTE is the loss op of block
+ * L-1; FORGET drops block j's input activation. */
+typedef enum {
+    RKR_OP_COMPUTE = 0,
+    RKR_OP_FORGET = 1,
+    RKR_OP_BLOCK_FWD = 2,
+    RKR_OP_BLOCK_BWD = 3
+} rkr_op_kind;
+
+typedef struct {
+    int32_t kind;   /* rkr_op_kind */
+    int32_t block;
+    int32_t option; /* option id for BLOCK_FWD/BLOCK_BWD, -1 otherwise */
+} rkr_op;
+
+/* remat::OptionMenu (chain_dp.hpp:16-21) flattened: options of block i are
+ * entries [option_offsets[i], option_offsets[i+1]) in menu order; the fields
+ * are remat::BlockOption's (types.hpp:330-344); has_bwd[o] says whether the
+ * optional time_bwd is present.  act_sizes holds a_0..a_L in bytes. */
+typedef struct {
+    int32_t n_blocks;
+    const int32_t* option_offsets; /* [n_blocks + 1] */
+    const int32_t* option_id;
+    const int64_t* time_fwd;
+    const int64_t* time_bwd;
+    const uint8_t* has_bwd;
+    const int64_t* save_mem;
+    const int64_t* peak_fwd;
+    const int64_t* peak_fwd_pre;
+    const int64_t* peak_bwd;
+    const int64_t* act_sizes;      /* [n_blocks + 1] */
+} rkr_menu;
+
+typedef enum {
+    RKR_WIDTH_AUTO = 0, /* 32-bit costs when the host overflow proof holds, else 64 */
+    RKR_WIDTH_64 = 64   /* force the general int64 kernels */
+} rkr_width;
+
+/* Execution settings; pass NULL for defaults (device 0, the library's own
+ * stream, auto width). */
+typedef struct {
+    int32_t device;
+    void* stream;       /* cudaStream_t, or NULL for a stream owned by the handle */
+    int32_t width;      /* rkr_width */
+    int32_t reserved[5];
+} rkr_exec;
+
+typedef struct rkr_table rkr_table;
+
+const char* rkr_last_error(void);
+int32_t rkr_abi_version(void);
+/* 1 when an sm_100 device is visible and the kernels can run here. */
+int32_t rkr_device_ok(int32_t device);
+
+/* remat::quantize (chain_dp.hpp:32-39) and remat::to_units (:41). */
+rkr_status rkr_quantize(int64_t budget_bytes, int32_t units, int64_t* unit,
+                        int64_t* budget_units);
+int64_t rkr_to_units(int64_t bytes, int64_t unit);
+
+/* remat::DpTable::DpTable(menu, unit, m_max) (chain_dp.hpp:56-101): validates
+ * the menu, does the per-block unit precompute on the host, copies it to the
+ * device and fills every cell (s <= t, 0 <= m <= m_max) with the wavefront
+ * kernels.  Returns when the fill has been enqueued on the handle's stream. */
+rkr_status rkr_table_create(const rkr_menu* menu, int64_t unit, int32_t m_max,
+                            const rkr_exec* exec, rkr_table** out);
+void rkr_table_destroy(rkr_table* table);
+
+/* DpTable::length/unit/m_max/act_units (chain_dp.hpp:113-116). */
+int32_t rkr_table_length(const rkr_table* table);
+int64_t rkr_table_unit(const rkr_table* table);
+int32_t rkr_table_m_max(const rkr_table* table);
+int64_t rkr_table_act_units(const rkr_table* table, int32_t i);
+/* 32 or 64: the cost width the fill ran in (bookkeeping only; every value
+ * leaving the library is int64 and bit-exact). */
+int32_t rkr_table_width(const rkr_table* table);
+/* DpTable::max_candidates_per_cell / worst_cell_allowance (:118-120),
+ * computed in closed form from the menu (the device fill visits exactly the
+ * reference's candidate sequence). */
+rkr_status rkr_table_work_bound(const rkr_table* table, int64_t* max_candidates_per_cell,
+                                int64_t* worst_cell_allowance);
+
+/* DpTable::opt / arg (chain_dp.hpp:103-112): m < 0 -> RKR_INF_TIME / NONE,
+ * m > m_max clamps to m_max.  Requires 0 <= s <= t < L. */
+rkr_status rkr_table_opt(const rkr_table* table, int32_t s, int32_t t, int32_t m, int64_t* out);
+rkr_status rkr_table_arg(const rkr_table* table, int32_t s, int32_t t, int32_t m,
+                         int32_t* kind, int32_t* value);
+
+/* Bulk copy of one row (s, t), m = 0..m_max, as the reference stores it:
+ * opt int64, arg kind and value.  Any output pointer may be NULL. */
+rkr_status rkr_table_row(const rkr_table* table, int32_t s, int32_t t, int64_t* opt,
+                         int8_t* kind, int32_t* value);
+/* Bulk copy of the whole table, rows in s-major upper-triangular order
+ * (row(s,t) = s*L - s*(s-1)/2 + (t-s)), each m_max+1 long. */
+rkr_status rkr_table_download(const rkr_table* table, int64_t* opt, int8_t* kind,
+                              int32_t* value);
+
+/* remat::build_schedule_rec(table, menu, chain, s, t, m, out)
+ * (chain_dp.hpp:211-246), run on the device; only the ops return.  On
+ * RKR_ERR_CAPACITY *n_ops holds the required count.  On RKR_ERR_INFEASIBLE
+ * *n_ops holds the ops emitted before the infeasible cell (as the
+ * reference's out-vector would). */
+rkr_status rkr_backtrack(const rkr_table* table, int32_t s, int32_t t, int32_t m, rkr_op* ops,
+                         int64_t cap, int64_t* n_ops);
+
+/* First m with opt(s, t, m) < inf, or -1 (the scan in solve_chain's
+ * infeasible branch, chain_dp.hpp:280-284), computed on the device. */
+rkr_status rkr_first_feasible(const rkr_table* table, int32_t s, int32_t t, int32_t* m_out);
+
+/* remat::solve_chain(chain, menu, budget_bytes, units) (chain_dp.hpp:255-296)
+ * in one call: quantize, fill, top cell, device backtrack; on infeasibility
+ * the wide-table min-feasible search, returned in *min_feasible (bytes, or -1)
+ * with RKR_ERR_INFEASIBLE. */
+rkr_status rkr_solve_chain(const rkr_menu* menu, int64_t budget_bytes, int32_t units,
+                           const rkr_exec* exec, rkr_op* ops, int64_t cap, int64_t* n_ops,
+                           int64_t* opt_time, int64_t* unit, int32_t* m_top,
+                           int64_t* min_feasible);
+
+/* Wait for all work queued on the table's stream. */
+rkr_status rkr_table_sync(const rkr_table* table);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RKR_H */

@@ -1,0 +1,668 @@
+// rkr_capi.cu -- host half of librkr.so: the C ABI of include/rkr.h.
+//
+// Host work here is exactly the reference's host-side bookkeeping (menu
+// validation and the per-block unit precompute of the DpTable constructor,
+// chain_dp.hpp:56-95; quantize/to_units :32-41; solve_chain's control flow
+// :255-296).  Every table cell is computed on the device (rkr_kernels.cu);
+// there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rkr.h"
+#include "rkr_internal.h"
+
+using namespace rkr;
+
+namespace {
+
+thread_local std::string g_err;
+
+rkr_status fail(rkr_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+rkr_status cuda_fail(cudaError_t e, const char* where) {
+    cudaGetLastError();  // clear sticky-free errors
+    return fail(e == cudaErrorMemoryAllocation ? RKR_ERR_OOM : RKR_ERR_CUDA, "%s: %s", where,
+                cudaGetErrorString(e));
+}
+
+#define CK(call)                                          \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+int64_t to_units(int64_t b, int64_t unit) { return (b + unit - 1) / unit; }  // chain_dp.hpp:41
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Host image of the DpTable constructor's precompute (chain_dp.hpp:56-95).
+struct HostMenu {
+    int32_t L = 0;
+    std::vector<int32_t> blk_off;  // saved options per block, CSR
+    std::vector<int64_t> fwd_req, fwd_req_pre, bwd_req, pack_chg, tftb, chg_bt;
+    std::vector<int32_t> ids;
+    std::vector<int64_t> act_u, fwd0_own, fwd0_full, tf0;
+    int32_t max_opts = 0;
+    bool bounded32 = false;  // the 32-bit overflow proof holds
+};
+
+rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
+    if (!m) return fail(RKR_ERR_ARGUMENT, "null menu");
+    const int32_t L = m->n_blocks;
+    if (L <= 0) return fail(RKR_ERR_INVALID, "empty option menu");      // chain_dp.hpp:58
+    if (!m->option_offsets || !m->option_id || !m->time_fwd || !m->time_bwd || !m->has_bwd ||
+        !m->save_mem || !m->peak_fwd || !m->peak_fwd_pre || !m->peak_bwd || !m->act_sizes)
+        return fail(RKR_ERR_ARGUMENT, "null menu array");
+    if (unit < 1) return fail(RKR_ERR_INVALID, "unit must be >= 1");
+    if (L > 0x7fff) return fail(RKR_ERR_INVALID, "chains longer than 32767 blocks are not supported");
+    for (int32_t i = 0; i < L; ++i)
+        if (m->option_offsets[i + 1] < m->option_offsets[i])
+            return fail(RKR_ERR_ARGUMENT, "option_offsets not monotone at block %d", i);
+    h.L = L;
+    h.act_u.resize(L + 1);
+    for (int32_t i = 0; i <= L; ++i) h.act_u[i] = to_units(m->act_sizes[i], unit);  // :59-60
+    h.blk_off.assign(L + 1, 0);
+    h.fwd0_own.assign(L, 0);
+    h.fwd0_full.assign(L, 0);
+    h.tf0.assign(L, 0);
+    bool nonneg = true;
+    long double F = 0, Bk = 0;
+    for (int32_t i = 0; i < L; ++i) {                                         // :72-95
+        const int64_t a_i = m->act_sizes[i];
+        bool saw_zero = false;
+        h.blk_off[i] = (int32_t)h.ids.size();
+        int64_t fmax = 0, bmax = 0;
+        for (int32_t o = m->option_offsets[i]; o < m->option_offsets[i + 1]; ++o) {
+            if (m->time_fwd[o] < 0) nonneg = false;
+            fmax = std::max(fmax, m->time_fwd[o]);
+            if (m->option_id[o] == 0) {                                       // :76-81
+                h.fwd0_own[i] = to_units(m->peak_fwd[o] - a_i, unit);
+                h.fwd0_full[i] = to_units(m->peak_fwd[o], unit);
+                h.tf0[i] = m->time_fwd[o];
+                saw_zero = true;
+                continue;
+            }
+            if (!m->has_bwd[o])                                               // :83-85
+                return fail(RKR_ERR_INVALID, "saved option without a backward in block %d", i);
+            if (m->time_bwd[o] < 0) nonneg = false;
+            bmax = std::max(bmax, m->time_bwd[o]);
+            h.ids.push_back(m->option_id[o]);                                 // :86-92
+            h.fwd_req.push_back(to_units(m->peak_fwd[o] - a_i, unit));
+            h.fwd_req_pre.push_back(to_units(m->peak_fwd_pre[o] - a_i, unit));
+            h.bwd_req.push_back(to_units(m->peak_bwd[o] - a_i, unit));
+            h.pack_chg.push_back(to_units(m->save_mem[o] - a_i, unit));
+            h.tftb.push_back(m->time_fwd[o] + m->time_bwd[o]);
+            // build_schedule_rec looks the option up by id (first match,
+            // chain_dp.hpp:200-205, :228)
+            int64_t chg = 0;
+            for (int32_t p = m->option_offsets[i]; p < m->option_offsets[i + 1]; ++p)
+                if (m->option_id[p] == m->option_id[o]) {
+                    chg = to_units(m->save_mem[p] - a_i, unit);
+                    break;
+                }
+            h.chg_bt.push_back(chg);
+        }
+        if (!saw_zero) return fail(RKR_ERR_INVALID, "block %d lacks option 0", i);  // :94
+        const int32_t n = (int32_t)h.ids.size() - h.blk_off[i];
+        if (n > 0x7ffe) return fail(RKR_ERR_INVALID, "block %d has more than 32766 options", i);
+        h.max_opts = std::max(h.max_opts, n);
+        F += (long double)fmax;
+        Bk += (long double)bmax;
+    }
+    h.blk_off[L] = (int32_t)h.ids.size();
+    // Shifts index earlier budget columns; a negative one would read past
+    // m_max, which is undefined behaviour in the reference (vector overrun).
+    for (size_t q = 0; q < h.pack_chg.size(); ++q)
+        if (h.pack_chg[q] < 0)
+            return fail(RKR_ERR_INVALID,
+                        "saved option with save_mem below its input size (negative pack shift)");
+    for (int32_t c = 1; c < L; ++c)
+        if (h.act_u[c] < 0) return fail(RKR_ERR_INVALID, "negative activation size a_%d", c);
+    // Overflow proof for 32-bit costs: every finite candidate total is at most
+    // L * sum_j max time_fwd_j + sum_j max time_bwd_j when times are >= 0
+    // (induction over span).  Require it below INF32 = 2^30.
+    h.bounded32 = nonneg && ((long double)L * F + Bk) < (long double)kInf32;
+    return RKR_OK;
+}
+
+}  // namespace
+
+struct rkr_table {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int64_t unit = 1;
+    int width = 64;
+    HostMenu hm;
+    Geometry g{};
+    DevMenu dm{};
+    void* dmenu = nullptr;
+    void* opt = nullptr;
+    uint16_t* arg = nullptr;
+    int4* stack = nullptr;
+    int64_t* dout = nullptr;      // device scratch: backtrack result / first-feasible
+    int64_t* hout = nullptr;      // pinned mirror
+    int32_t* dops = nullptr;
+    int64_t dops_cap = 0;
+
+    LaunchCtx ctx() const {
+        LaunchCtx c;
+        c.g = g;
+        c.dm = dm;
+        c.opt = opt;
+        c.arg = arg;
+        c.width = width;
+        c.max_opts = hm.max_opts;
+        c.stream = stream;
+        return c;
+    }
+};
+
+namespace {
+
+void free_table(rkr_table* t) {
+    if (!t) return;
+    DeviceGuard dg(t->device);
+    if (t->stream) cudaStreamSynchronize(t->stream);
+    cudaFree(t->dmenu);
+    cudaFree(t->opt);
+    cudaFree(t->arg);
+    cudaFree(t->stack);
+    cudaFree(t->dout);
+    cudaFree(t->dops);
+    if (t->hout) cudaFreeHost(t->hout);
+    if (t->own_stream && t->stream) cudaStreamDestroy(t->stream);
+    delete t;
+}
+
+rkr_status check_cell(const rkr_table* t, int32_t s, int32_t tt) {
+    if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
+    if (s < 0 || tt < s || tt >= t->g.L)
+        return fail(RKR_ERR_ARGUMENT, "cell (%d, %d) outside 0 <= s <= t < %d", s, tt, t->g.L);
+    return RKR_OK;
+}
+
+// Upload the precompute as one blob and point DevMenu into it.
+rkr_status upload_menu(rkr_table* t) {
+    const HostMenu& h = t->hm;
+    const size_t nq = std::max<size_t>(h.ids.size(), 1);
+    const size_t L = h.L;
+    std::vector<size_t> off;
+    size_t bytes = 0;
+    auto take = [&](size_t n) {
+        off.push_back(bytes);
+        bytes += round_up((int64_t)n, 16);
+    };
+    take((L + 1) * 4);                       // 0 blk_off
+    for (int i = 0; i < 6; ++i) take(nq * 8);  // 1..6 fwd_req..chg_bt
+    take(nq * 4);                            // 7 ids
+    take((L + 1) * 8);                       // 8 act_u
+    for (int i = 0; i < 3; ++i) take(L * 8);   // 9..11 fwd0_own, fwd0_full, tf0
+    std::vector<unsigned char> blob(bytes, 0);
+    auto put = [&](int idx, const void* src, size_t n) {
+        if (n) std::memcpy(blob.data() + off[idx], src, n);
+    };
+    put(0, h.blk_off.data(), (L + 1) * 4);
+    put(1, h.fwd_req.data(), h.fwd_req.size() * 8);
+    put(2, h.fwd_req_pre.data(), h.fwd_req_pre.size() * 8);
+    put(3, h.bwd_req.data(), h.bwd_req.size() * 8);
+    put(4, h.pack_chg.data(), h.pack_chg.size() * 8);
+    put(5, h.tftb.data(), h.tftb.size() * 8);
+    put(6, h.chg_bt.data(), h.chg_bt.size() * 8);
+    put(7, h.ids.data(), h.ids.size() * 4);
+    put(8, h.act_u.data(), (L + 1) * 8);
+    put(9, h.fwd0_own.data(), L * 8);
+    put(10, h.fwd0_full.data(), L * 8);
+    put(11, h.tf0.data(), L * 8);
+    CK(cudaMalloc(&t->dmenu, bytes));
+    CK(cudaMemcpyAsync(t->dmenu, blob.data(), bytes, cudaMemcpyHostToDevice, t->stream));
+    unsigned char* b = static_cast<unsigned char*>(t->dmenu);
+    t->dm.blk_off = reinterpret_cast<const int32_t*>(b + off[0]);
+    t->dm.fwd_req = reinterpret_cast<const int64_t*>(b + off[1]);
+    t->dm.fwd_req_pre = reinterpret_cast<const int64_t*>(b + off[2]);
+    t->dm.bwd_req = reinterpret_cast<const int64_t*>(b + off[3]);
+    t->dm.pack_chg = reinterpret_cast<const int64_t*>(b + off[4]);
+    t->dm.tftb = reinterpret_cast<const int64_t*>(b + off[5]);
+    t->dm.chg_bt = reinterpret_cast<const int64_t*>(b + off[6]);
+    t->dm.ids = reinterpret_cast<const int32_t*>(b + off[7]);
+    t->dm.act_u = reinterpret_cast<const int64_t*>(b + off[8]);
+    t->dm.fwd0_own = reinterpret_cast<const int64_t*>(b + off[9]);
+    t->dm.fwd0_full = reinterpret_cast<const int64_t*>(b + off[10]);
+    t->dm.tf0 = reinterpret_cast<const int64_t*>(b + off[11]);
+    // blob must outlive the async copy
+    CK(cudaStreamSynchronize(t->stream));
+    return RKR_OK;
+}
+
+rkr_status create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max, const rkr_exec* exec,
+                       rkr_table** out) {
+    if (!out) return fail(RKR_ERR_ARGUMENT, "null output handle");
+    *out = nullptr;
+    if (m_max < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
+    rkr_table* t = new rkr_table();
+    rkr_status st = build_host_menu(menu, unit, t->hm);
+    if (st != RKR_OK) {
+        delete t;
+        return st;
+    }
+    t->unit = unit;
+    t->device = exec ? exec->device : 0;
+    const int want = exec ? exec->width : RKR_WIDTH_AUTO;
+    t->width = (want != RKR_WIDTH_64 && t->hm.bounded32) ? 32 : 64;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= t->device) {
+        cudaGetLastError();
+        delete t;
+        return fail(RKR_ERR_CUDA, "no CUDA device %d visible (librkr has no CPU fallback)",
+                    exec ? exec->device : 0);
+    }
+    DeviceGuard dg(t->device);
+    if (exec && exec->stream) {
+        t->stream = static_cast<cudaStream_t>(exec->stream);
+    } else {
+        cudaError_t e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete t;
+            return cuda_fail(e, "cudaStreamCreate");
+        }
+        t->own_stream = true;
+    }
+    // geometry
+    const HostMenu& h = t->hm;
+    int64_t maxshift = 0;
+    for (int64_t p : h.pack_chg) maxshift = std::max(maxshift, p);
+    for (int32_t c = 1; c < h.L; ++c) maxshift = std::max(maxshift, h.act_u[c]);
+    t->g.L = h.L;
+    t->g.M = m_max;
+    t->g.pad = (int32_t)std::min<int64_t>(maxshift, (int64_t)m_max + 1);
+    t->g.pad = (int32_t)round_up(t->g.pad, 8);
+    t->g.sr = round_up((int64_t)t->g.pad + m_max + 1, 32);
+    t->g.sa = round_up((int64_t)m_max + 1, 64);
+    t->g.rows = (int64_t)h.L * (h.L + 1) / 2;
+    const size_t vbytes = t->width == 32 ? 4 : 8;
+#define CKT(call)                                         \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) {                          \
+            rkr_status s_ = cuda_fail(e_, #call);         \
+            free_table(t);                                \
+            return s_;                                    \
+        }                                                 \
+    } while (0)
+    CKT(cudaMalloc(&t->opt, (size_t)t->g.rows * t->g.sr * vbytes));
+    CKT(cudaMalloc(reinterpret_cast<void**>(&t->arg), (size_t)t->g.rows * t->g.sa * 2));
+    CKT(cudaMalloc(reinterpret_cast<void**>(&t->stack), sizeof(int4) * (2 * (size_t)h.L + 16)));
+    CKT(cudaMalloc(reinterpret_cast<void**>(&t->dout), 8 * sizeof(int64_t)));
+    CKT(cudaMallocHost(reinterpret_cast<void**>(&t->hout), 8 * sizeof(int64_t)));
+    st = upload_menu(t);
+    if (st != RKR_OK) {
+        free_table(t);
+        return st;
+    }
+    LaunchCtx c = t->ctx();
+    if (launch_init_pads(c) || launch_fill_all(c)) {
+        rkr_status s = cuda_fail(cudaGetLastError(), "fill launch");
+        free_table(t);
+        return s;
+    }
+    *out = t;
+    return RKR_OK;
+}
+
+template <typename V>
+rkr_status read_cell(const rkr_table* t, int32_t s, int32_t tt, int32_t m, int64_t* val,
+                     uint16_t* code) {
+    const int64_t rid = row_id(t->g.L, s, tt);
+    V v{};
+    const V* o = static_cast<const V*>(t->opt);
+    CK(cudaMemcpyAsync(&v, o + rid * t->g.sr + t->g.pad + m, sizeof(V), cudaMemcpyDeviceToHost,
+                       t->stream));
+    uint16_t c = 0;
+    CK(cudaMemcpyAsync(&c, t->arg + rid * t->g.sa + m, 2, cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    if (t->width == 32)
+        *val = (uint64_t)v >= kInf32 ? kInf64 : (int64_t)v;
+    else
+        *val = (int64_t)v;
+    *code = c;
+    return RKR_OK;
+}
+
+rkr_status cell(const rkr_table* t, int32_t s, int32_t tt, int32_t m, int64_t* val,
+                uint16_t* code) {
+    return t->width == 32 ? read_cell<uint32_t>(t, s, tt, m, val, code)
+                          : read_cell<int64_t>(t, s, tt, m, val, code);
+}
+
+void decode(const rkr_table* t, int32_t s, int64_t val, uint16_t code, int32_t* kind,
+            int32_t* value) {
+    if (val >= kInf64 || code == 0) {  // chain_dp.hpp:177
+        *kind = RKR_ARG_NONE;
+        *value = -1;
+    } else if (code & kCutBit) {
+        *kind = RKR_ARG_CUT;
+        *value = code & 0x7fff;
+    } else {
+        *kind = RKR_ARG_OPTION;
+        *value = t->hm.ids[t->hm.blk_off[s] + code - 1];
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rkr_last_error(void) { return g_err.c_str(); }
+int32_t rkr_abi_version(void) { return RKR_ABI_VERSION; }
+
+int32_t rkr_device_ok(int32_t device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return 0;
+    return p.major == 10 ? 1 : 0;
+}
+
+rkr_status rkr_quantize(int64_t budget_bytes, int32_t units, int64_t* unit,
+                        int64_t* budget_units) {
+    if (!unit || !budget_units) return fail(RKR_ERR_ARGUMENT, "null output");
+    if (units < 1) return fail(RKR_ERR_INVALID, "quantization needs at least one unit");  // :33
+    int64_t u = (budget_bytes + units - 1) / units;                                       // :35
+    if (u < 1) u = 1;
+    *unit = u;
+    *budget_units = budget_bytes / u;
+    return RKR_OK;
+}
+
+int64_t rkr_to_units(int64_t bytes, int64_t unit) { return to_units(bytes, unit); }
+
+rkr_status rkr_table_create(const rkr_menu* menu, int64_t unit, int32_t m_max,
+                            const rkr_exec* exec, rkr_table** out) {
+    return create_impl(menu, unit, m_max, exec, out);
+}
+
+void rkr_table_destroy(rkr_table* table) { free_table(table); }
+
+int32_t rkr_table_length(const rkr_table* t) { return t ? t->g.L : 0; }
+int64_t rkr_table_unit(const rkr_table* t) { return t ? t->unit : 0; }
+int32_t rkr_table_m_max(const rkr_table* t) { return t ? t->g.M : -1; }
+int32_t rkr_table_width(const rkr_table* t) { return t ? t->width : 0; }
+int64_t rkr_table_act_units(const rkr_table* t, int32_t i) {
+    return (t && i >= 0 && i <= t->g.L) ? t->hm.act_u[i] : 0;
+}
+
+rkr_status rkr_table_work_bound(const rkr_table* t, int64_t* max_cands, int64_t* worst_allow) {
+    if (!t || !max_cands || !worst_allow) return fail(RKR_ERR_ARGUMENT, "null argument");
+    // Candidates per cell are non-decreasing in m (every test is "x <= m"),
+    // so the maximum sits at m = m_max (counting as chain_dp.hpp:140,161).
+    const HostMenu& h = t->hm;
+    const int L = h.L;
+    const int64_t M = t->g.M;
+    // For a fixed t (fixed seed), the cut loop of cell (s, t) counts
+    // min(t, j + 1) - s candidates, j = first block > s whose bare forward
+    // does not fit (the `break`, counted before it fires); nxt[] gives j for
+    // every s in one backward scan, so the whole bound is O(L^2).
+    int64_t best = 0, worst = 0;  // both start at 0 as in chain_dp.hpp:119-120
+    std::vector<int> nxt(L + 1);
+    for (int tt = 0; tt < L; ++tt) {
+        const int64_t seed = tt < L - 1 ? 2 * h.act_u[tt + 1] : 0;
+        nxt[L - 1] = L;  // none
+        for (int s = L - 2; s >= 0; --s)
+            nxt[s] = (h.fwd0_full[s + 1] + seed > M) ? s + 1 : nxt[s + 1];
+        for (int s = 0; s <= tt; ++s) {
+            const int64_t nopt = h.blk_off[s + 1] - h.blk_off[s];
+            int64_t cands = nopt;
+            if (h.fwd0_own[s] + seed <= M) cands += std::min<int64_t>(tt, (int64_t)nxt[s] + 1) - s;
+            best = std::max(best, cands);
+            worst = std::max(worst, cands - ((tt - s) + nopt + 1));
+        }
+    }
+    *max_cands = best;
+    *worst_allow = worst;
+    return RKR_OK;
+}
+
+rkr_status rkr_table_opt(const rkr_table* t, int32_t s, int32_t tt, int32_t m, int64_t* out) {
+    rkr_status st = check_cell(t, s, tt);
+    if (st) return st;
+    if (!out) return fail(RKR_ERR_ARGUMENT, "null output");
+    if (m < 0) {  // chain_dp.hpp:104
+        *out = RKR_INF_TIME;
+        return RKR_OK;
+    }
+    if (m > t->g.M) m = t->g.M;  // :105
+    DeviceGuard dg(t->device);
+    uint16_t code;
+    return cell(t, s, tt, m, out, &code);
+}
+
+rkr_status rkr_table_arg(const rkr_table* t, int32_t s, int32_t tt, int32_t m, int32_t* kind,
+                         int32_t* value) {
+    rkr_status st = check_cell(t, s, tt);
+    if (st) return st;
+    if (!kind || !value) return fail(RKR_ERR_ARGUMENT, "null output");
+    if (m < 0) {  // chain_dp.hpp:109
+        *kind = RKR_ARG_NONE;
+        *value = -1;
+        return RKR_OK;
+    }
+    if (m > t->g.M) m = t->g.M;
+    DeviceGuard dg(t->device);
+    int64_t v;
+    uint16_t code;
+    st = cell(t, s, tt, m, &v, &code);
+    if (st) return st;
+    decode(t, s, v, code, kind, value);
+    return RKR_OK;
+}
+
+static rkr_status export_rows_host(const rkr_table* t, int64_t r0, int64_t r1, int64_t* opt,
+                                   int8_t* kind, int32_t* value) {
+    // Device-side conversion in chunks of rows, then D2H.
+    const int64_t W = t->g.M + 1;
+    const int64_t per_row = W * (8 + 1 + 4);
+    int64_t chunk = std::max<int64_t>(1, (int64_t)(256ll << 20) / per_row);
+    chunk = std::min<int64_t>(chunk, 65535);
+    chunk = std::min<int64_t>(chunk, r1 - r0);
+    void* buf = nullptr;
+    CK(cudaMalloc(&buf, (size_t)(chunk * per_row)));
+    int64_t* dopt = static_cast<int64_t*>(buf);
+    int32_t* dval = reinterpret_cast<int32_t*>(dopt + chunk * W);
+    int8_t* dkind = reinterpret_cast<int8_t*>(dval + chunk * W);
+    LaunchCtx c = t->ctx();
+    rkr_status st = RKR_OK;
+    for (int64_t r = r0; r < r1 && st == RKR_OK; r += chunk) {
+        const int64_t n = std::min(chunk, r1 - r);
+        if (launch_export(c, r, r + n, opt ? dopt : nullptr, kind ? dkind : nullptr,
+                          value ? dval : nullptr)) {
+            st = cuda_fail(cudaGetLastError(), "export launch");
+            break;
+        }
+        const int64_t o = (r - r0) * W;
+        cudaError_t e = cudaSuccess;
+        if (opt && e == cudaSuccess)
+            e = cudaMemcpyAsync(opt + o, dopt, n * W * 8, cudaMemcpyDeviceToHost, t->stream);
+        if (value && e == cudaSuccess)
+            e = cudaMemcpyAsync(value + o, dval, n * W * 4, cudaMemcpyDeviceToHost, t->stream);
+        if (kind && e == cudaSuccess)
+            e = cudaMemcpyAsync(kind + o, dkind, n * W, cudaMemcpyDeviceToHost, t->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(t->stream);
+        if (e != cudaSuccess) st = cuda_fail(e, "export copy");
+    }
+    cudaStreamSynchronize(t->stream);
+    cudaFree(buf);
+    return st;
+}
+
+rkr_status rkr_table_row(const rkr_table* t, int32_t s, int32_t tt, int64_t* opt, int8_t* kind,
+                         int32_t* value) {
+    rkr_status st = check_cell(t, s, tt);
+    if (st) return st;
+    DeviceGuard dg(t->device);
+    const int64_t r = (int64_t)s * t->g.L - (int64_t)s * (s - 1) / 2 + (tt - s);
+    return export_rows_host(t, r, r + 1, opt, kind, value);
+}
+
+rkr_status rkr_table_download(const rkr_table* t, int64_t* opt, int8_t* kind, int32_t* value) {
+    if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
+    DeviceGuard dg(t->device);
+    return export_rows_host(t, 0, t->g.rows, opt, kind, value);
+}
+
+rkr_status rkr_backtrack(const rkr_table* tc, int32_t s, int32_t tt, int32_t m, rkr_op* ops,
+                         int64_t cap, int64_t* n_ops) {
+    rkr_table* t = const_cast<rkr_table*>(tc);  // scratch buffers only
+    rkr_status st = check_cell(t, s, tt);
+    if (st) return st;
+    if (!n_ops || (cap > 0 && !ops)) return fail(RKR_ERR_ARGUMENT, "null output");
+    DeviceGuard dg(t->device);
+    *n_ops = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if (t->dops_cap < 1024) {
+            CK(cudaMalloc(reinterpret_cast<void**>(&t->dops), 1024 * 12));
+            t->dops_cap = 1024;
+        }
+        LaunchCtx c = t->ctx();
+        if (launch_backtrack(c, s, tt, m, t->dops, t->dops_cap,
+                             reinterpret_cast<int32_t*>(t->stack), t->dout))
+            return cuda_fail(cudaGetLastError(), "backtrack launch");
+        CK(cudaMemcpyAsync(t->hout, t->dout, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                           t->stream));
+        CK(cudaStreamSynchronize(t->stream));
+        const int64_t n = t->hout[0];
+        if (n > t->dops_cap) {  // grow the device buffer and walk again
+            cudaFree(t->dops);
+            t->dops = nullptr;
+            t->dops_cap = 0;
+            CK(cudaMalloc(reinterpret_cast<void**>(&t->dops), (size_t)n * 12));
+            t->dops_cap = n;
+            continue;
+        }
+        const int64_t status = t->hout[1];
+        const int64_t ncopy = std::min(n, cap);
+        if (ncopy > 0)
+            CK(cudaMemcpy(ops, t->dops, (size_t)ncopy * 12, cudaMemcpyDeviceToHost));
+        *n_ops = n;
+        if (status == 2)
+            return fail(RKR_ERR_INFEASIBLE, "no feasible schedule for blocks %lld..%lld",
+                        (long long)t->hout[2], (long long)t->hout[3]);
+        if (n > cap) return fail(RKR_ERR_CAPACITY, "schedule needs %lld ops", (long long)n);
+        return RKR_OK;
+    }
+    return fail(RKR_ERR_CUDA, "backtrack did not converge");
+}
+
+rkr_status rkr_first_feasible(const rkr_table* t, int32_t s, int32_t tt, int32_t* m_out) {
+    rkr_status st = check_cell(t, s, tt);
+    if (st) return st;
+    if (!m_out) return fail(RKR_ERR_ARGUMENT, "null output");
+    DeviceGuard dg(t->device);
+    int32_t* dm = reinterpret_cast<int32_t*>(t->dout);
+    const int32_t big = 0x7fffffff;
+    CK(cudaMemcpyAsync(dm, &big, 4, cudaMemcpyHostToDevice, t->stream));
+    if (launch_first_feasible(t->ctx(), s, tt, dm))
+        return cuda_fail(cudaGetLastError(), "first_feasible launch");
+    int32_t* hm = reinterpret_cast<int32_t*>(t->hout);
+    CK(cudaMemcpyAsync(hm, dm, 4, cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    *m_out = hm[0] == big ? -1 : hm[0];
+    return RKR_OK;
+}
+
+rkr_status rkr_table_sync(const rkr_table* t) {
+    if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
+    DeviceGuard dg(t->device);
+    CK(cudaStreamSynchronize(t->stream));
+    return RKR_OK;
+}
+
+rkr_status rkr_solve_chain(const rkr_menu* menu, int64_t budget_bytes, int32_t units,
+                           const rkr_exec* exec, rkr_op* ops, int64_t cap, int64_t* n_ops,
+                           int64_t* opt_time, int64_t* unit_out, int32_t* m_top_out,
+                           int64_t* min_feasible) {
+    if (!menu || !n_ops || !opt_time || !unit_out || !m_top_out || !min_feasible)
+        return fail(RKR_ERR_ARGUMENT, "null argument");
+    *n_ops = 0;
+    *min_feasible = -1;
+    int64_t unit, bu;
+    rkr_status st = rkr_quantize(budget_bytes, units, &unit, &bu);        // :257
+    if (st) return st;
+    if (menu->n_blocks <= 0 || !menu->act_sizes)
+        return fail(RKR_ERR_INVALID, "empty option menu");
+    const int64_t a0_u = to_units(menu->act_sizes[0], unit);              // :258
+    const int64_t m_top = bu - a0_u;                                       // :259
+    if (m_top < 0) return fail(RKR_ERR_INFEASIBLE, "budget cannot hold the chain input");
+    if (m_top > 0x7ffffffe) return fail(RKR_ERR_INVALID, "budget slots exceed int range");
+    rkr_table* t = nullptr;
+    st = rkr_table_create(menu, unit, (int32_t)m_top, exec, &t);           // :262
+    if (st) return st;
+    const int L = t->g.L;
+    int64_t best;
+    st = rkr_table_opt(t, 0, L - 1, (int32_t)m_top, &best);                // :264
+    if (st) {
+        rkr_table_destroy(t);
+        return st;
+    }
+    if (best >= RKR_INF_TIME) {                                            // :265-288
+        int64_t capu = 0;
+        for (int i = 0; i < L; ++i) {
+            int64_t worst = 0;
+            for (int o = menu->option_offsets[i]; o < menu->option_offsets[i + 1]; ++o)
+                worst = std::max({worst, to_units(menu->peak_fwd[o], unit),
+                                  to_units(menu->peak_bwd[o], unit),
+                                  to_units(menu->save_mem[o], unit)});
+            capu += worst;
+        }
+        for (int i = 0; i <= L; ++i) capu += 2 * to_units(menu->act_sizes[i], unit);
+        rkr_table_destroy(t);
+        if (capu > 0x7ffffffe) return fail(RKR_ERR_INVALID, "feasibility cap exceeds int range");
+        rkr_table* wide = nullptr;
+        st = rkr_table_create(menu, unit, (int32_t)capu, exec, &wide);
+        if (st) return st;
+        int32_t m = -1;
+        st = rkr_first_feasible(wide, 0, L - 1, &m);
+        rkr_table_destroy(wide);
+        if (st) return st;
+        if (m >= 0) *min_feasible = (m + a0_u) * unit;
+        return fail(RKR_ERR_INFEASIBLE, "budget of %lld bytes is infeasible for this chain",
+                    (long long)budget_bytes);
+    }
+    *opt_time = best;
+    *unit_out = unit;
+    *m_top_out = (int32_t)m_top;
+    st = rkr_backtrack(t, 0, L - 1, (int32_t)m_top, ops, cap, n_ops);     // :293
+    rkr_table_destroy(t);
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,416 @@
+// rkr_kernels.cu -- sm_100a kernels of the rk-Rotor chain DP.
+//
+//   K1 fill_diag      one launch per anti-diagonal k = t - s; CTA = (s, tile of
+//                     NT*R budget slots); lanes over consecutive m; the
+//                     candidate loop (options in menu order, then cuts
+//                     ascending) with a strict '<' reproduces the reference
+//                     argmin exactly (chain_dp.hpp:125-183).
+//   K2 backtrack      build_schedule_rec (chain_dp.hpp:211-246) as an explicit
+//                     stack walk on one thread; only the ops go back to the host.
+//   K3 first_feasible the min-feasible scan of solve_chain (chain_dp.hpp:280-284).
+//   export_rows       converts packed rows (uint32/int64 cost + uint16 code) to
+//                     the reference's (int64 Micros, DpArg) layout.
+//
+// Integer min-plus only: no tensor cores (there is no contraction to feed).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rkr_internal.h"
+
+namespace rkr {
+
+namespace {
+
+template <typename V>
+struct Cost;
+template <>
+struct Cost<uint32_t> {
+    static constexpr uint32_t inf = kInf32;
+    static constexpr bool checked = false;  // bounded by the host overflow proof
+};
+template <>
+struct Cost<int64_t> {
+    static constexpr int64_t inf = kInf64;
+    static constexpr bool checked = true;   // arbitrary int64: explicit inf tests
+};
+
+__device__ __forceinline__ int32_t clamp_thr(int64_t x, int32_t M) {
+    return x < -1 ? -1 : (x > (int64_t)M + 1 ? M + 1 : (int32_t)x);
+}
+
+// Shared-memory image of one cell's candidates (uniform across the CTA).
+template <typename V>
+struct CellSmem {
+    int64_t* lbase;  // [k] left row (s, c-1) base, element index of m = 0
+    int64_t* rbase;  // [k] right row (c, t) base, pre-shifted by -act_u[c]
+    V* inc;          // [k] time_fwd0[c-1]: sweep increment
+    V* otot;         // [nopt] time_fwd + time_bwd
+    int32_t* gate;   // [k] fwd0_full[c-1] + seed (clamped), -1 when c-1 == s
+    int32_t* thr;    // [nopt] validity threshold of option oi (clamped)
+    int32_t* pc;     // [nopt] pack_chg (clamped to pad)
+};
+
+template <typename V>
+__host__ __device__ inline size_t cell_smem_bytes(int k, int nopt) {
+    return (size_t)k * (8 + 8 + sizeof(V) + 4) + (size_t)nopt * (sizeof(V) + 4 + 4);
+}
+
+template <typename V>
+__device__ inline CellSmem<V> carve(unsigned char* p, int k, int nopt) {
+    CellSmem<V> c;
+    c.lbase = reinterpret_cast<int64_t*>(p);
+    c.rbase = c.lbase + k;
+    c.inc = reinterpret_cast<V*>(c.rbase + k);
+    c.otot = c.inc + k;
+    c.gate = reinterpret_cast<int32_t*>(c.otot + nopt);
+    c.thr = c.gate + k;
+    c.pc = c.thr + nopt;
+    return c;
+}
+
+// K1: fill every cell (s, s+k, m) of diagonal k.
+template <typename V, int NT, int R>
+__global__ void __launch_bounds__(NT) fill_diag(Geometry g, DevMenu dm, V* __restrict__ opt,
+                                                uint16_t* __restrict__ arg, int k) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr V INF = Cost<V>::inf;
+    const int L = g.L, M = g.M;
+    const int s = blockIdx.y;
+    const int t = s + k;
+    const bool seeded = t < L - 1;                                    // chain_dp.hpp:126
+    const int64_t seed = seeded ? 2 * dm.act_u[t + 1] : 0;            // chain_dp.hpp:127
+    const int o0 = dm.blk_off[s];
+    const int nopt = dm.blk_off[s + 1] - o0;
+    CellSmem<V> cs = carve<V>(smem_raw, k, nopt);
+
+    // ---- prologue: stage this cell's candidate parameters -------------------
+    for (int i = threadIdx.x; i < k; i += NT) {
+        const int c = s + 1 + i;
+        cs.lbase[i] = row_id(L, s, c - 1) * g.sr + g.pad;
+        const int64_t a = dm.act_u[c];
+        const int sh = a > g.pad ? g.pad : (int)a;
+        cs.rbase[i] = row_id(L, c, t) * g.sr + g.pad - sh;
+        cs.inc[i] = (V)dm.tf0[c - 1];
+        cs.gate[i] = (c - 1 > s) ? clamp_thr(dm.fwd0_full[c - 1] + seed, M) : -1;
+    }
+    for (int i = threadIdx.x; i < nopt; i += NT) {
+        const int q = o0 + i;
+        // chain_dp.hpp:141-147: fwd need, bwd need and (s < t) pack fit
+        int64_t need = (k == 0 && seeded) ? dm.fwd_req_pre[q] + dm.act_u[t + 1]
+                                          : dm.fwd_req[q] + seed;
+        int64_t th = need > dm.bwd_req[q] ? need : dm.bwd_req[q];
+        if (k > 0 && dm.pack_chg[q] > th) th = dm.pack_chg[q];
+        cs.thr[i] = clamp_thr(th, M);
+        const int64_t p = dm.pack_chg[q];
+        cs.pc[i] = p > g.pad ? g.pad : (int)p;
+        cs.otot[i] = (V)dm.tftb[q];
+    }
+    const int32_t gate0 = clamp_thr(dm.fwd0_own[s] + seed, M);       // chain_dp.hpp:159
+    __syncthreads();
+
+    // ---- lanes over consecutive budget slots ---------------------------------
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mb = blockIdx.x * (NT * R) + warp * (32 * R) + lane;
+    int mj[R];
+    bool inr[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int m = mb + 32 * j;
+        inr[j] = m <= M;
+        mj[j] = inr[j] ? m : M;
+    }
+    V best[R];
+    uint16_t code[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        best[j] = INF;
+        code[j] = 0;
+    }
+
+    // ---- Case 1: saved options in menu order (chain_dp.hpp:139-156) ---------
+    if (k == 0) {
+        for (int i = 0; i < nopt; ++i) {
+            const V tot = cs.otot[i];
+            const int th = cs.thr[i];
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+                if (mj[j] >= th && tot < best[j]) {
+                    best[j] = tot;
+                    code[j] = (uint16_t)(i + 1);
+                }
+        }
+    } else {
+        const V* __restrict__ nxt = opt + row_id(L, s + 1, t) * g.sr + g.pad;
+        for (int i = 0; i < nopt; ++i) {
+            const V tt = cs.otot[i];
+            const int th = cs.thr[i];
+            const int p = cs.pc[i];
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const V sub = __ldcg(nxt + (mj[j] - p));  // pad slots hold INF
+                bool ok = mj[j] >= th;
+                if constexpr (Cost<V>::checked) ok = ok && sub < INF;
+                const V tot = tt + sub;
+                if (ok && tot < best[j]) {
+                    best[j] = tot;
+                    code[j] = (uint16_t)(i + 1);
+                }
+            }
+        }
+
+        // ---- Case 2: cuts ascending with the option-0 sweep (chain_dp.hpp:158-174)
+        bool alive[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) alive[j] = mj[j] >= gate0;
+        V sweep = 0;
+        for (int i = 0; i < k; ++i) {
+            sweep += cs.inc[i];
+            const int gt = cs.gate[i];
+            bool any = false;
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                alive[j] = alive[j] && mj[j] >= gt;  // the reference's `break`
+                any |= alive[j];
+            }
+            if (!any) break;
+            const V* __restrict__ lrow = opt + cs.lbase[i];
+            const V* __restrict__ rrow = opt + cs.rbase[i];
+            const uint16_t cc = (uint16_t)(kCutBit | (s + 1 + i));
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                if (!alive[j]) continue;
+                const V r = __ldcg(rrow + mj[j]);  // m - act_u[c] < 0 lands in the pad
+                const V l = __ldcg(lrow + mj[j]);
+                const V tot = sweep + r + l;
+                bool ok = tot < best[j];
+                if constexpr (Cost<V>::checked) ok = ok && r < INF && l < INF;
+                if (ok) {
+                    best[j] = tot;
+                    code[j] = cc;
+                }
+            }
+        }
+    }
+
+    // ---- store (chain_dp.hpp:176-177) ---------------------------------------
+    const int64_t rid = row_id(L, s, t);
+    V* __restrict__ orow = opt + rid * g.sr + g.pad;
+    uint16_t* __restrict__ arow = arg + rid * g.sa;
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+        if (inr[j]) {
+            orow[mj[j]] = best[j];
+            arow[mj[j]] = code[j];
+        }
+}
+
+template <typename V>
+__global__ void init_pads(Geometry g, V* opt) {
+    const int64_t n = g.rows * (int64_t)g.pad;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / g.pad, p = i - r * g.pad;
+        opt[r * g.sr + p] = Cost<V>::inf;
+    }
+}
+
+// K2: build_schedule_rec on one thread.  Stack entries are int4
+// {type, s, t, m}: type 0 = cell to expand, type 1 = pending BlockBwd(s, t=option).
+template <typename V>
+__global__ void backtrack(Geometry g, DevMenu dm, const V* __restrict__ opt,
+                          const uint16_t* __restrict__ arg, int s0, int t0, int m0,
+                          int32_t* __restrict__ ops, int64_t cap, int4* __restrict__ stack,
+                          int64_t* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int L = g.L, M = g.M;
+    int64_t n = 0;
+    int sp = 0;
+    int64_t status = 0, bad_s = -1, bad_t = -1;
+    auto emit = [&](int kd, int b, int x) {
+        if (n < cap) {
+            ops[3 * n] = kd;
+            ops[3 * n + 1] = b;
+            ops[3 * n + 2] = x;
+        }
+        ++n;
+    };
+    stack[sp++] = make_int4(0, s0, t0, m0);
+    while (sp > 0) {
+        const int4 e = stack[--sp];
+        if (e.x == 1) {  // deferred BlockBwd of an option turn (chain_dp.hpp:230)
+            emit(3, e.y, e.z);
+            continue;
+        }
+        const int s = e.y, t = e.z, m = e.w;
+        // table.opt(s,t,m) >= kInfTime -> InfeasibleBudget (chain_dp.hpp:213-215)
+        const int64_t rid = row_id(L, s, t);
+        bool inf = m < 0;
+        int mm = m > M ? M : m;
+        uint16_t code = 0;
+        if (!inf) {
+            inf = opt[rid * g.sr + g.pad + mm] >= Cost<V>::inf;
+            code = arg[rid * g.sa + mm];
+        }
+        if (inf || code == 0) {  // code 0 on a finite cell = "cell without a decision"
+            status = 2;
+            bad_s = s;
+            bad_t = t;
+            break;
+        }
+        if (!(code & kCutBit)) {  // Option (chain_dp.hpp:217-232)
+            const int q = dm.blk_off[s] + code - 1;
+            const int val = dm.ids[q];
+            emit(2, s, val);
+            if (s == t) {
+                if (t == L - 1) emit(0, t, -1);
+                emit(3, s, val);
+            } else {
+                stack[sp++] = make_int4(1, s, val, 0);
+                stack[sp++] = make_int4(0, s + 1, t, m - (int)dm.chg_bt[q]);
+            }
+        } else {  // Cut (chain_dp.hpp:233-244)
+            const int c = code & 0x7fff;
+            emit(2, s, 0);
+            for (int j = s + 1; j < c; ++j) {
+                emit(2, j, 0);
+                emit(1, j, -1);
+            }
+            stack[sp++] = make_int4(0, s, c - 1, m);                  // left, after
+            stack[sp++] = make_int4(0, c, t, m - (int)dm.act_u[c]);   // right, first
+        }
+    }
+    out[0] = n;
+    out[1] = status;
+    out[2] = bad_s;
+    out[3] = bad_t;
+}
+
+// K3: first m with opt(s,t,m) < inf.
+template <typename V>
+__global__ void first_feasible(Geometry g, const V* __restrict__ opt, int s, int t, int* m_out) {
+    const int64_t base = row_id(g.L, s, t) * g.sr + g.pad;
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m <= g.M; m += gridDim.x * blockDim.x)
+        if (opt[base + m] < Cost<V>::inf) {
+            atomicMin(m_out, m);
+            return;
+        }
+}
+
+// Packed rows -> reference layout for rows [r0, r1) of the s-major order.
+template <typename V>
+__global__ void export_rows(Geometry g, DevMenu dm, const V* __restrict__ opt,
+                            const uint16_t* __restrict__ arg, int64_t r0, int64_t* __restrict__ o,
+                            int8_t* __restrict__ kd, int32_t* __restrict__ val) {
+    const int L = g.L;
+    const int64_t r = r0 + blockIdx.y;
+    int s = 0;
+    int64_t first = 0;
+    while (first + (L - s) <= r) {
+        first += L - s;
+        ++s;
+    }
+    const int t = s + (int)(r - first);
+    const int64_t rid = row_id(L, s, t);
+    const int64_t W = g.M + 1;
+    const int64_t ob = (int64_t)blockIdx.y * W;
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m <= g.M; m += gridDim.x * blockDim.x) {
+        const V v = opt[rid * g.sr + g.pad + m];
+        const uint16_t c = arg[rid * g.sa + m];
+        if (o) o[ob + m] = v >= Cost<V>::inf ? kInf64 : (int64_t)v;
+        int8_t k = 0;
+        int32_t x = -1;
+        if (v < Cost<V>::inf && c != 0) {
+            if (c & kCutBit) {
+                k = 2;
+                x = c & 0x7fff;
+            } else {
+                k = 1;
+                x = dm.ids[dm.blk_off[s] + c - 1];
+            }
+        }
+        if (kd) kd[ob + m] = k;
+        if (val) val[ob + m] = x;
+    }
+}
+
+template <typename V>
+int fill_all_t(const LaunchCtx& c) {
+    constexpr int NT = 128, R = 2;
+    cudaStream_t st = static_cast<cudaStream_t>(c.stream);
+    V* opt = static_cast<V*>(c.opt);
+    const int tiles = (c.g.M + 1 + NT * R - 1) / (NT * R);
+    const size_t max_smem = cell_smem_bytes<V>(c.g.L, c.max_opts);
+    if (max_smem > 48 * 1024)
+        cudaFuncSetAttribute(fill_diag<V, NT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)max_smem);
+    for (int k = 0; k < c.g.L; ++k) {
+        dim3 grid(tiles, c.g.L - k);
+        fill_diag<V, NT, R><<<grid, NT, cell_smem_bytes<V>(k, c.max_opts), st>>>(
+            c.g, c.dm, opt, c.arg, k);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+}  // namespace
+
+int launch_init_pads(const LaunchCtx& c) {
+    if (c.g.pad == 0) return 0;
+    cudaStream_t st = static_cast<cudaStream_t>(c.stream);
+    const int64_t n = c.g.rows * (int64_t)c.g.pad;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (c.width == 32)
+        init_pads<uint32_t><<<blocks, 256, 0, st>>>(c.g, static_cast<uint32_t*>(c.opt));
+    else
+        init_pads<int64_t><<<blocks, 256, 0, st>>>(c.g, static_cast<int64_t*>(c.opt));
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int launch_fill_all(const LaunchCtx& c) {
+    return c.width == 32 ? fill_all_t<uint32_t>(c) : fill_all_t<int64_t>(c);
+}
+
+int launch_backtrack(const LaunchCtx& c, int32_t s, int32_t t, int32_t m, int32_t* dev_ops,
+                     int64_t cap, int32_t* dev_stack, int64_t* dev_out) {
+    cudaStream_t st = static_cast<cudaStream_t>(c.stream);
+    int4* stk = reinterpret_cast<int4*>(dev_stack);
+    if (c.width == 32)
+        backtrack<uint32_t><<<1, 32, 0, st>>>(c.g, c.dm, static_cast<const uint32_t*>(c.opt),
+                                              c.arg, s, t, m, dev_ops, cap, stk, dev_out);
+    else
+        backtrack<int64_t><<<1, 32, 0, st>>>(c.g, c.dm, static_cast<const int64_t*>(c.opt),
+                                             c.arg, s, t, m, dev_ops, cap, stk, dev_out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int launch_first_feasible(const LaunchCtx& c, int32_t s, int32_t t, int32_t* dev_m) {
+    cudaStream_t st = static_cast<cudaStream_t>(c.stream);
+    int blocks = (c.g.M + 1 + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (c.width == 32)
+        first_feasible<uint32_t><<<blocks, 256, 0, st>>>(
+            c.g, static_cast<const uint32_t*>(c.opt), s, t, dev_m);
+    else
+        first_feasible<int64_t><<<blocks, 256, 0, st>>>(
+            c.g, static_cast<const int64_t*>(c.opt), s, t, dev_m);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int launch_export(const LaunchCtx& c, int64_t r0, int64_t r1, int64_t* o, int8_t* kd,
+                  int32_t* val) {
+    cudaStream_t st = static_cast<cudaStream_t>(c.stream);
+    if (r1 <= r0) return 0;
+    int bx = (c.g.M + 1 + 255) / 256;
+    if (bx > 64) bx = 64;
+    dim3 grid(bx, (unsigned)(r1 - r0));
+    if (c.width == 32)
+        export_rows<uint32_t><<<grid, 256, 0, st>>>(
+            c.g, c.dm, static_cast<const uint32_t*>(c.opt), c.arg, r0, o, kd, val);
+    else
+        export_rows<int64_t><<<grid, 256, 0, st>>>(
+            c.g, c.dm, static_cast<const int64_t*>(c.opt), c.arg, r0, o, kd, val);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+}  // namespace rkr

@@ -1,0 +1,350 @@
+"""Python host mirror of the reference solver API, over librkr's C ABI.
+
+Names, argument meaning and error behaviour follow namespace ``remat`` in
+/root/reference/proj/include/remat/chain_dp.hpp:
+
+    quantize / to_units            chain_dp.hpp:25-41
+    DpArg                          chain_dp.hpp:44-47
+    DpTable(menu, unit, m_max)     chain_dp.hpp:54-196   (filled on the GPU)
+    build_schedule_rec(...)        chain_dp.hpp:211-246  (walked on the GPU)
+    ChainSolution / solve_chain    chain_dp.hpp:248-296
+    ValidationError / InfeasibleBudget   errors.hpp:14-16, :51-55
+
+The C++ drop-in with the identical signatures is include/remat_b200/chain_dp.hpp;
+this module is the same surface for Python callers, tests and bench.py.
+All DP work runs in librkr.so on an sm_100 device.  There is no CPU
+fallback: if the library or the device is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from .menu import Menu, RkrMenu
+
+K_INF_TIME = (2**63 - 1) // 4  # remat::kInfTime, chain_dp.hpp:23
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librkr.so")
+
+RKR_OK, RKR_ERR_INVALID, RKR_ERR_INFEASIBLE, RKR_ERR_CUDA, RKR_ERR_OOM, RKR_ERR_CAPACITY, \
+    RKR_ERR_ARGUMENT = range(7)
+
+
+class ValidationError(RuntimeError):
+    """remat::ValidationError (errors.hpp:14-16)."""
+
+
+class InfeasibleBudget(RuntimeError):
+    """remat::InfeasibleBudget (errors.hpp:51-55)."""
+
+    def __init__(self, what: str, min_feasible_budget: int = -1):
+        super().__init__(what)
+        self.min_feasible_budget = min_feasible_budget
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure, missing device or missing librkr.so (no CPU fallback)."""
+
+
+class RkrOp(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("block", ctypes.c_int32), ("option", ctypes.c_int32)]
+
+
+class RkrExec(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("stream", ctypes.c_void_p), ("width", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load librkr.so (in-tree build).  Raises DeviceError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(f"librkr.so not built at {LIB_PATH}: run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    i32, i64, p = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
+    P = ctypes.POINTER
+    L.rkr_last_error.restype = ctypes.c_char_p
+    L.rkr_abi_version.restype = i32
+    L.rkr_device_ok.argtypes = [i32]
+    L.rkr_device_ok.restype = i32
+    L.rkr_quantize.argtypes = [i64, i32, P(i64), P(i64)]
+    L.rkr_to_units.argtypes = [i64, i64]
+    L.rkr_to_units.restype = i64
+    L.rkr_table_create.argtypes = [P(RkrMenu), i64, i32, P(RkrExec), P(p)]
+    L.rkr_table_destroy.argtypes = [p]
+    L.rkr_table_destroy.restype = None
+    for name, rt in (("rkr_table_length", i32), ("rkr_table_unit", i64), ("rkr_table_m_max", i32),
+                     ("rkr_table_width", i32)):
+        getattr(L, name).argtypes = [p]
+        getattr(L, name).restype = rt
+    L.rkr_table_act_units.argtypes = [p, i32]
+    L.rkr_table_act_units.restype = i64
+    L.rkr_table_work_bound.argtypes = [p, P(i64), P(i64)]
+    L.rkr_table_opt.argtypes = [p, i32, i32, i32, P(i64)]
+    L.rkr_table_arg.argtypes = [p, i32, i32, i32, P(i32), P(i32)]
+    L.rkr_table_row.argtypes = [p, i32, i32, p, p, p]
+    L.rkr_table_download.argtypes = [p, p, p, p]
+    L.rkr_backtrack.argtypes = [p, i32, i32, i32, P(RkrOp), i64, P(i64)]
+    L.rkr_first_feasible.argtypes = [p, i32, i32, P(i32)]
+    L.rkr_solve_chain.argtypes = [P(RkrMenu), i64, i32, P(RkrExec), P(RkrOp), i64, P(i64), P(i64),
+                                  P(i64), P(i32), P(i64)]
+    L.rkr_table_sync.argtypes = [p]
+    _lib = L
+    return L
+
+
+def _check(st: int, min_feasible: int = -1) -> None:
+    if st == RKR_OK:
+        return
+    msg = lib().rkr_last_error().decode()
+    if st == RKR_ERR_INVALID:
+        raise ValidationError(msg)
+    if st == RKR_ERR_INFEASIBLE:
+        raise InfeasibleBudget(msg, min_feasible)
+    if st == RKR_ERR_ARGUMENT:
+        raise IndexError(msg)
+    raise DeviceError(f"librkr status {st}: {msg}")
+
+
+def _exec(device: int, width: str, stream: Optional[int] = None) -> RkrExec:
+    e = RkrExec()
+    e.device = device
+    e.stream = stream
+    e.width = 64 if width == "64" else 0
+    return e
+
+
+@dataclass
+class Quantization:
+    unit: int = 1
+    budget_units: int = 0
+
+
+def quantize(budget_bytes: int, units: int) -> Quantization:
+    u, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().rkr_quantize(budget_bytes, units, ctypes.byref(u), ctypes.byref(b)))
+    return Quantization(u.value, b.value)
+
+
+def to_units(nbytes: int, unit: int) -> int:
+    return lib().rkr_to_units(nbytes, unit)
+
+
+@dataclass(frozen=True)
+class DpArg:
+    """remat::DpArg: kind None=0 / Option=1 / Cut=2, value = option id or cut index."""
+
+    kind: int = 0
+    value: int = -1
+
+    NONE, OPTION, CUT = 0, 1, 2
+
+
+# ScheduleOp kinds (types.hpp:346-362)
+OP_COMPUTE, OP_FORGET, OP_BLOCK_FWD, OP_BLOCK_BWD = 0, 1, 2, 3
+
+
+@dataclass(frozen=True)
+class ScheduleOp:
+    kind: int
+    block: int
+    target: str = ""
+    option: int = -1
+
+
+@dataclass
+class Chain:
+    """The id-bearing part of remat::Chain that build_schedule_rec reads:
+    per block, the input dnode id and the loss cnode id."""
+
+    input_ids: List[str]
+    loss_ids: List[str]
+
+    @staticmethod
+    def skeleton(L: int) -> "Chain":
+        return Chain([f"b{i}_in" for i in range(L)], [f"b{i}_loss" for i in range(L)])
+
+    def length(self) -> int:
+        return len(self.input_ids)
+
+
+class DpTable:
+    """remat::DpTable (chain_dp.hpp:54-196); cells live in device memory."""
+
+    def __init__(self, menu: Menu, unit: int, m_max: int, device: int = 0, width: str = "auto",
+                 stream: Optional[int] = None):
+        self._lib = lib()
+        self._h = ctypes.c_void_p()
+        self._menu_struct = menu.struct()
+        ex = _exec(device, width, stream)
+        _check(self._lib.rkr_table_create(ctypes.byref(self._menu_struct), unit, m_max,
+                                          ctypes.byref(ex), ctypes.byref(self._h)))
+        self.menu = menu
+        self._host: Optional[Tuple[np.ndarray, np.ndarray, np.ndarray]] = None
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.rkr_table_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # accessors (chain_dp.hpp:103-116)
+    def length(self) -> int:
+        return self._lib.rkr_table_length(self._h)
+
+    def unit(self) -> int:
+        return self._lib.rkr_table_unit(self._h)
+
+    def m_max(self) -> int:
+        return self._lib.rkr_table_m_max(self._h)
+
+    def act_units(self, i: int) -> int:
+        return self._lib.rkr_table_act_units(self._h, i)
+
+    def width(self) -> int:
+        return self._lib.rkr_table_width(self._h)
+
+    def sync(self) -> None:
+        _check(self._lib.rkr_table_sync(self._h))
+
+    @property
+    def max_candidates_per_cell(self) -> int:
+        return self._work_bound()[0]
+
+    @property
+    def worst_cell_allowance(self) -> int:
+        return self._work_bound()[1]
+
+    def _work_bound(self) -> Tuple[int, int]:
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(self._lib.rkr_table_work_bound(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def opt(self, s: int, t: int, m: int) -> int:
+        if self._host is not None:
+            return self._host_opt(s, t, m)
+        v = ctypes.c_int64()
+        _check(self._lib.rkr_table_opt(self._h, s, t, m, ctypes.byref(v)))
+        return v.value
+
+    def arg(self, s: int, t: int, m: int) -> DpArg:
+        k, v = ctypes.c_int32(), ctypes.c_int32()
+        _check(self._lib.rkr_table_arg(self._h, s, t, m, ctypes.byref(k), ctypes.byref(v)))
+        return DpArg(k.value, v.value)
+
+    def row(self, s: int, t: int) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        W = self.m_max() + 1
+        o = np.empty(W, np.int64)
+        k = np.empty(W, np.int8)
+        v = np.empty(W, np.int32)
+        _check(self._lib.rkr_table_row(self._h, s, t, o.ctypes.data, k.ctypes.data, v.ctypes.data))
+        return o, k, v
+
+    def download(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """Whole table, rows in s-major triangular order, reference types."""
+        L, W = self.length(), self.m_max() + 1
+        rows = L * (L + 1) // 2
+        o = np.empty((rows, W), np.int64)
+        k = np.empty((rows, W), np.int8)
+        v = np.empty((rows, W), np.int32)
+        _check(self._lib.rkr_table_download(self._h, o.ctypes.data, k.ctypes.data, v.ctypes.data))
+        self._host = (o, k, v)
+        return o, k, v
+
+    def _host_opt(self, s, t, m):
+        if m < 0:
+            return K_INF_TIME
+        m = min(m, self.m_max())
+        L = self.length()
+        return int(self._host[0][s * L - s * (s - 1) // 2 + (t - s), m])
+
+    def backtrack(self, s: int, t: int, m: int) -> List[Tuple[int, int, int]]:
+        """Raw device backtrack: (kind, block, option) triples."""
+        cap = 4096
+        while True:
+            buf = (RkrOp * cap)()
+            n = ctypes.c_int64()
+            st = self._lib.rkr_backtrack(self._h, s, t, m, buf, cap, ctypes.byref(n))
+            if st == RKR_ERR_CAPACITY:
+                cap = n.value
+                continue
+            _check(st)
+            return [(buf[i].kind, buf[i].block, buf[i].option) for i in range(n.value)]
+
+    def first_feasible(self, s: int, t: int) -> int:
+        m = ctypes.c_int32()
+        _check(self._lib.rkr_first_feasible(self._h, s, t, ctypes.byref(m)))
+        return m.value
+
+
+def _named(ops, chain: Chain) -> List[ScheduleOp]:
+    out = []
+    for k, b, o in ops:
+        if k == OP_COMPUTE:
+            out.append(ScheduleOp(k, b, chain.loss_ids[b], -1))
+        elif k == OP_FORGET:
+            out.append(ScheduleOp(k, b, chain.input_ids[b], -1))
+        else:
+            out.append(ScheduleOp(k, b, "", o))
+    return out
+
+
+def build_schedule_rec(table: DpTable, menu: Menu, chain: Chain, s: int, t: int, m: int,
+                       out: Optional[list] = None) -> List[ScheduleOp]:
+    """remat::build_schedule_rec (chain_dp.hpp:211-246), walked on the device."""
+    ops = _named(table.backtrack(s, t, m), chain)
+    if out is not None:
+        out.extend(ops)
+    return ops
+
+
+@dataclass
+class ChainSolution:
+    schedule: List[ScheduleOp] = field(default_factory=list)
+    opt_time: int = 0
+    unit: int = 1
+    m_top: int = 0
+    raw_ops: List[Tuple[int, int, int]] = field(default_factory=list)
+
+
+def solve_chain(chain: Chain, menu: Menu, budget_bytes: int, units: int, device: int = 0,
+                width: str = "auto") -> ChainSolution:
+    """remat::solve_chain (chain_dp.hpp:255-296) in one C-ABI call."""
+    L = lib()
+    ms = menu.struct()
+    ex = _exec(device, width)
+    cap = max(4096, 4 * menu.L * menu.L)
+    while True:
+        buf = (RkrOp * cap)()
+        n, ot, un, mf = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        mt = ctypes.c_int32()
+        st = L.rkr_solve_chain(ctypes.byref(ms), budget_bytes, units, ctypes.byref(ex), buf, cap,
+                               ctypes.byref(n), ctypes.byref(ot), ctypes.byref(un), ctypes.byref(mt),
+                               ctypes.byref(mf))
+        if st == RKR_ERR_CAPACITY:
+            cap = n.value
+            continue
+        _check(st, mf.value)
+        raw = [(buf[i].kind, buf[i].block, buf[i].option) for i in range(n.value)]
+        return ChainSolution(_named(raw, chain), ot.value, un.value, mt.value, raw)

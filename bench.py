@@ -1,0 +1,363 @@
+"""bench.py -- rk-Rotor chain DP throughput (DP cell-updates/s) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config 2]
+
+One step = one full rk-Rotor solve of one chain: every cell (s <= t, m) of
+the DP table filled on the GPU (the wavefront kernels) plus the device
+backtrack of the top cell into a schedule (BASELINE.json metric: "DP
+cell-updates/sec and solve wall-time").  Workload at N=1: BASELINE.json
+configs[1] (ResNet-101-like chain, L=33, B=16, M=4096), synthetic menus from
+the deterministic generator of SURVEY.md 8(d).  Under torchrun each rank
+solves its own independent chain of the same shape (budget sweeps / model
+instances shard with no communication: "scaling": "weak"); the only
+collectives are the timing barrier and the max-over-ranks reduction.
+
+The JSON line carries: value (device-timed, inputs resident), e2e (the same
+metric through the public C-ABI call with host menu arrays, H2D + fill +
+backtrack + D2H of the schedule inside the timed region), roofline of the
+dominant kernel (fill_diag) against the measured HBM copy bandwidth, the
+reference CPU solver timed on this host (cpu_baseline), clocks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2307_01236_b200.menu import CONFIGS, synthetic_menu  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0
+
+
+def cells_of(L, M):
+    return L * (L + 1) // 2 * (M + 1)
+
+
+def alg_bytes(L, M):
+    """bytes(s,t,m) = 16(t-s) + 24, summed exactly."""
+    return sum((L - k) * (16 * k + 24) for k in range(L)) * (M + 1)
+
+
+def candidates_of(L, B, M):
+    return sum((L - k) * (B + k) for k in range(L)) * (M + 1)
+
+
+def rank_menu(cfg_idx, rank):
+    c = CONFIGS[cfg_idx]
+    return synthetic_menu(c["L"], c["B"], c["M"], seed=42 + cfg_idx + 1000 * rank)
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfg_idx):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"config{cfg_idx}", {}).get("dram_bytes_per_fill")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _one(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=5).stdout.strip()
+            if out:
+                self.rows.append([x.strip() for x in out.split(",")])
+        except Exception:
+            pass
+
+    def _loop(self):
+        while not self._stop.is_set():
+            self._one()
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+        if not self.rows:
+            self._one()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reference_arm(args, world, rank):
+    """The reference's own CPU implementation (oracle/_ref: remat::DpTable from
+    the unmodified headers) on this host's cores; rank 0 only."""
+    if rank != 0:
+        return
+    from oracle.pyoracle import HAVE_REF, Orc, Ref
+
+    c = CONFIGS[args.config]
+    L, B, M = c["L"], c["B"], c["M"]
+    menu = rank_menu(args.config, 0)
+    threads = os.cpu_count() or 1
+    if HAVE_REF:
+        ref, kind = Ref(), "reference"
+    else:  # the C restatement, same algorithm
+        ref, kind = None, "port"
+    cells = cells_of(L, M)
+
+    def step():
+        if ref is not None:
+            secs, top = ref.table_bench(menu, 1, M, threads)
+        else:
+            import concurrent.futures as cf
+            t0 = time.perf_counter()
+            with cf.ThreadPoolExecutor(threads) as ex:
+                list(ex.map(lambda _: Orc().fill(menu, 1, M), range(threads)))
+            secs = time.perf_counter() - t0
+        return secs
+
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    total = sum(times)
+    value = threads * cells * args.steps / total
+    line = {
+        "impl": "reference",
+        "metric": "DP cell-updates/sec (rk-Rotor chain DP, full table fill)",
+        "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (SURVEY.md 8(d) splitmix64 generator)",
+        "config": {"workload": f"config{args.config}: {c['name']} chain, L={L}, B={B}, M={M}; "
+                               f"reference remat::DpTable fill, {threads} concurrent solves/step",
+                   "L": L, "B": B, "M": M},
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": threads, "kind": kind,
+                         "sample": f"each step = {threads} concurrent full config-{args.config} "
+                                   f"table fills (one per host thread; the reference solver "
+                                   f"itself is single-threaded, pipeline.hpp:58)"},
+        "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(cfg_idx, menu, L, M):
+    """Reference CPU solver on this host, 1 thread (as it ships), bounded sample."""
+    from oracle.pyoracle import HAVE_REF, Orc, Ref
+
+    reps = 3
+    if HAVE_REF:
+        ref = Ref()
+        secs = [ref.table_bench(menu, 1, M, 1)[0] for _ in range(reps)]
+        kind = "reference"
+    else:
+        orc = Orc()
+        secs = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            orc.fill(menu, 1, M)
+            secs.append(time.perf_counter() - t0)
+        kind = "port"
+    s = statistics.median(secs)
+    return {"value": cells_of(L, M) / s, "unit": "cells/s", "cores": 1, "kind": kind,
+            "sample": f"full config-{cfg_idx} table fill (L={L}, M={M}), median of {reps}, "
+                      f"1 thread (the reference solver is single-threaded)",
+            "seconds_per_solve": s}
+
+
+def b200_arm(args, world, rank, local):
+    import torch
+
+    from paper_2307_01236_b200 import rotor
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if not rotor.lib().rkr_device_ok(local):
+        raise SystemExit("bench: no sm_100 device")
+    c = CONFIGS[args.config]
+    L, B, M = c["L"], c["B"], c["M"]
+    menu = rank_menu(args.config, rank)
+    stream = torch.cuda.Stream(device=local)
+    table = rotor.DpTable(menu, 1, M, device=local, stream=stream.cuda_stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident solves -----------------------------------------------
+    def one_step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        table.refill()
+        if ev is not None:
+            ev[1].record(stream)
+        table.backtrack_async(0, L - 1, M)
+        if ev is not None:
+            ev[2].record(stream)
+
+    sampler = ClockSampler(local)
+    with sampler:
+        for _ in range(args.warmup):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            one_step()
+        ops_ref = table.backtrack_fetch()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # L2 flush between timed steps (outside the events)
+            one_step(evs[i])
+        torch.cuda.synchronize()
+        barrier()
+    fill_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
+    ops = table.backtrack_fetch()
+    assert ops == ops_ref
+    top = table.opt(0, L - 1, M)
+    tot_s = max_over_ranks(sum(step_ms) / 1e3)
+    fill_mean_s = statistics.mean(fill_ms) / 1e3
+
+    # ---- end to end through the public API (host menu arrays) -------------------
+    h2d = table.h2d_bytes()
+    e2e_times = []
+    n_ops = 0
+    for i in range(args.warmup + args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        with rotor.DpTable(menu, 1, M, device=local, stream=stream.cuda_stream) as t2:
+            topv = t2.opt(0, L - 1, M)          # D2H of the solve value
+            sched = t2.backtrack(0, L - 1, M)   # device walk + D2H of the schedule
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_times.append(dt)
+        n_ops = len(sched)
+        assert topv == top and sched == ops
+    e2e_s = max_over_ranks(sum(e2e_times))
+    d2h = 8 + 2 + 32 + 12 * n_ops
+
+    cells = cells_of(L, M)
+    if rank != 0:
+        return
+    peak, peak_src = measured_peak()
+    ab = alg_bytes(L, M)
+    achieved = ab / fill_mean_s / 1e9
+    traffic = ncu_traffic(args.config)
+    line = {
+        "metric": "DP cell-updates/sec (rk-Rotor chain DP, full table fill + backtrack)",
+        "value": world * cells * args.steps / tot_s,
+        "unit": "cells/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int64" if table.width() == 64 else "int64 (stored as u32, overflow-proven)",
+        "data": "synthetic (SURVEY.md 8(d) splitmix64 generator; one independent chain per rank)",
+        "config": {
+            "workload": f"config{args.config}: {c['name']} chain, L={L} blocks, B={B} options/block, "
+                        f"M={M} budget slots; full DP fill + device backtrack per step",
+            "L": L, "B": B, "M": M, "cells_per_solve": cells,
+            "candidates_per_solve": candidates_of(L, B, M),
+            "l2": "flushed between timed steps (256 MiB write, outside the events)",
+            "parallelism": f"instances x{world} (no data-path collective)",
+            "solve_ms": 1e3 * tot_s / args.steps,
+            "top_opt": top,
+        },
+        "e2e": {"value": world * cells * args.steps / e2e_s, "unit": "cells/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": 1e3 * e2e_s / args.steps,
+                "path": "rkr_table_create(host menu) + rkr_table_opt + rkr_backtrack + destroy"},
+        "gpu_launches": args.steps * (L + 2),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "fill_diag (all L diagonal launches of one fill)",
+                     "alg_bytes_per_fill": ab, "fill_ms": 1e3 * fill_mean_s,
+                     "peak_source": peak_src},
+        "clocks": sampler.summary(),
+    }
+    if world == 1:
+        line["cpu_baseline"] = cpu_baseline_sample(args.config, menu, L, M)
+    print(json.dumps(line), flush=True)
+    table.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+    else:
+        b200_arm(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -150,6 +150,11 @@ rkr_status rkr_table_download(const rkr_table* table, int64_t* opt, int8_t* kind
 rkr_status rkr_backtrack(const rkr_table* table, int32_t s, int32_t t, int32_t m, rkr_op* ops,
                          int64_t cap, int64_t* n_ops);
 
+/* The same walk split in two: _async enqueues it on the table's stream (no
+ * host sync), _fetch waits and copies the ops (same statuses as above). */
+rkr_status rkr_backtrack_async(rkr_table* table, int32_t s, int32_t t, int32_t m);
+rkr_status rkr_backtrack_fetch(rkr_table* table, rkr_op* ops, int64_t cap, int64_t* n_ops);
+
 /* First m with opt(s, t, m) < inf, or -1 (the scan in solve_chain's
  * infeasible branch, chain_dp.hpp:280-284), computed on the device. */
 rkr_status rkr_first_feasible(const rkr_table* table, int32_t s, int32_t t, int32_t* m_out);
@@ -165,6 +170,16 @@ rkr_status rkr_solve_chain(const rkr_menu* menu, int64_t budget_bytes, int32_t u
 
 /* Wait for all work queued on the table's stream. */
 rkr_status rkr_table_sync(const rkr_table* table);
+
+/* Re-run the whole fill from the device-resident menu (no host work, async):
+ * the device-only step bench.py times. */
+rkr_status rkr_table_refill(rkr_table* table);
+/* The cudaStream_t every kernel of this table is launched on. */
+void* rkr_table_stream(const rkr_table* table);
+/* Bytes copied host->device by rkr_table_create (the staged menu precompute). */
+int64_t rkr_table_h2d_bytes(const rkr_table* table);
+/* Device bytes the table holds (menu, scratch, opt and arg rows). */
+int64_t rkr_table_device_bytes(const rkr_table* table);
 
 #ifdef __cplusplus
 }

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -154,23 +155,92 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
 
 }  // namespace
 
+namespace {
+
+// Per-device state shared by all tables: a non-blocking stream for handles
+// created without one, and the default memory pool kept warm (release
+// threshold = max) so per-table cudaMallocAsync is a pool hit after warm-up.
+struct DeviceCtx {
+    std::once_flag once;
+    cudaStream_t stream = nullptr;
+    cudaError_t err = cudaSuccess;
+};
+DeviceCtx g_dev[64];
+
+cudaError_t device_ctx(int dev, cudaStream_t* st) {
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    DeviceCtx& c = g_dev[dev];
+    std::call_once(c.once, [&] {
+        c.err = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
+        if (c.err != cudaSuccess) return;
+        cudaMemPool_t pool;
+        c.err = cudaDeviceGetDefaultMemPool(&pool, dev);
+        if (c.err != cudaSuccess) return;
+        uint64_t thr = UINT64_MAX;
+        c.err = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    });
+    *st = c.stream;
+    return c.err;
+}
+
+// Thread-local pinned staging for the menu upload and small readbacks; an
+// event guards reuse while an earlier async copy may still read it.
+struct Staging {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    cudaEvent_t done = nullptr;
+    ~Staging() {
+        if (done) cudaEventDestroy(done);
+        if (ptr) cudaFreeHost(ptr);
+    }
+    cudaError_t get(size_t n, void** out) {
+        cudaError_t e = cudaSuccess;
+        if (done) {
+            e = cudaEventSynchronize(done);
+            if (e != cudaSuccess) return e;
+        } else {
+            e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        if (n > cap) {
+            if (ptr) cudaFreeHost(ptr);
+            ptr = nullptr;
+            size_t c = std::max<size_t>(n, 1 << 16);
+            e = cudaMallocHost(&ptr, c);
+            if (e != cudaSuccess) {
+                cap = 0;
+                return e;
+            }
+            cap = c;
+        }
+        *out = ptr;
+        return cudaSuccess;
+    }
+};
+thread_local Staging t_stage;
+
+}  // namespace
+
 struct rkr_table {
     int device = 0;
     cudaStream_t stream = nullptr;
-    bool own_stream = false;
     int64_t unit = 1;
     int width = 64;
     HostMenu hm;
     Geometry g{};
     DevMenu dm{};
-    void* dmenu = nullptr;
+    void* block = nullptr;        // one pooled allocation: menu | scratch | opt | arg
+    size_t block_bytes = 0;
+    size_t menu_bytes = 0;        // H2D bytes per create
     void* opt = nullptr;
     uint16_t* arg = nullptr;
     int4* stack = nullptr;
     int64_t* dout = nullptr;      // device scratch: backtrack result / first-feasible
-    int64_t* hout = nullptr;      // pinned mirror
-    int32_t* dops = nullptr;
+    int64_t hout[8] = {};
+    int32_t* dops = nullptr;      // device op buffer (separate, grows on demand)
     int64_t dops_cap = 0;
+    bool bt_pending = false;
+    int32_t bt_s = 0, bt_t = 0, bt_m = 0;
 
     LaunchCtx ctx() const {
         LaunchCtx c;
@@ -190,15 +260,8 @@ namespace {
 void free_table(rkr_table* t) {
     if (!t) return;
     DeviceGuard dg(t->device);
-    if (t->stream) cudaStreamSynchronize(t->stream);
-    cudaFree(t->dmenu);
-    cudaFree(t->opt);
-    cudaFree(t->arg);
-    cudaFree(t->stack);
-    cudaFree(t->dout);
-    cudaFree(t->dops);
-    if (t->hout) cudaFreeHost(t->hout);
-    if (t->own_stream && t->stream) cudaStreamDestroy(t->stream);
+    if (t->block) cudaFreeAsync(t->block, t->stream);
+    if (t->dops) cudaFreeAsync(t->dops, t->stream);
     delete t;
 }
 
@@ -209,8 +272,9 @@ rkr_status check_cell(const rkr_table* t, int32_t s, int32_t tt) {
     return RKR_OK;
 }
 
-// Upload the precompute as one blob and point DevMenu into it.
-rkr_status upload_menu(rkr_table* t) {
+// Lay out one device block (menu blob, scratch, opt rows, arg rows), stage
+// the menu precompute in pinned memory and upload it asynchronously.
+rkr_status alloc_and_upload(rkr_table* t) {
     const HostMenu& h = t->hm;
     const size_t nq = std::max<size_t>(h.ids.size(), 1);
     const size_t L = h.L;
@@ -218,16 +282,28 @@ rkr_status upload_menu(rkr_table* t) {
     size_t bytes = 0;
     auto take = [&](size_t n) {
         off.push_back(bytes);
-        bytes += round_up((int64_t)n, 16);
+        bytes += round_up((int64_t)n, 256);
     };
-    take((L + 1) * 4);                       // 0 blk_off
+    take((L + 1) * 4);                         // 0 blk_off
     for (int i = 0; i < 6; ++i) take(nq * 8);  // 1..6 fwd_req..chg_bt
-    take(nq * 4);                            // 7 ids
-    take((L + 1) * 8);                       // 8 act_u
+    take(nq * 4);                              // 7 ids
+    take((L + 1) * 8);                         // 8 act_u
     for (int i = 0; i < 3; ++i) take(L * 8);   // 9..11 fwd0_own, fwd0_full, tf0
-    std::vector<unsigned char> blob(bytes, 0);
+    const size_t menu_bytes = bytes;
+    take(sizeof(int4) * (2 * L + 16));         // 12 backtrack stack
+    take(8 * sizeof(int64_t));                 // 13 dout
+    const size_t vbytes = t->width == 32 ? 4 : 8;
+    take((size_t)t->g.rows * t->g.sr * vbytes);  // 14 opt
+    take((size_t)t->g.rows * t->g.sa * 2);       // 15 arg
+    t->menu_bytes = menu_bytes;
+    t->block_bytes = bytes;
+
+    void* stage = nullptr;
+    CK(t_stage.get(menu_bytes, &stage));
+    unsigned char* blob = static_cast<unsigned char*>(stage);
+    std::memset(blob, 0, menu_bytes);
     auto put = [&](int idx, const void* src, size_t n) {
-        if (n) std::memcpy(blob.data() + off[idx], src, n);
+        if (n) std::memcpy(blob + off[idx], src, n);
     };
     put(0, h.blk_off.data(), (L + 1) * 4);
     put(1, h.fwd_req.data(), h.fwd_req.size() * 8);
@@ -241,9 +317,10 @@ rkr_status upload_menu(rkr_table* t) {
     put(9, h.fwd0_own.data(), L * 8);
     put(10, h.fwd0_full.data(), L * 8);
     put(11, h.tf0.data(), L * 8);
-    CK(cudaMalloc(&t->dmenu, bytes));
-    CK(cudaMemcpyAsync(t->dmenu, blob.data(), bytes, cudaMemcpyHostToDevice, t->stream));
-    unsigned char* b = static_cast<unsigned char*>(t->dmenu);
+    CK(cudaMallocAsync(&t->block, bytes, t->stream));
+    CK(cudaMemcpyAsync(t->block, blob, menu_bytes, cudaMemcpyHostToDevice, t->stream));
+    CK(cudaEventRecord(t_stage.done, t->stream));
+    unsigned char* b = static_cast<unsigned char*>(t->block);
     t->dm.blk_off = reinterpret_cast<const int32_t*>(b + off[0]);
     t->dm.fwd_req = reinterpret_cast<const int64_t*>(b + off[1]);
     t->dm.fwd_req_pre = reinterpret_cast<const int64_t*>(b + off[2]);
@@ -256,8 +333,16 @@ rkr_status upload_menu(rkr_table* t) {
     t->dm.fwd0_own = reinterpret_cast<const int64_t*>(b + off[9]);
     t->dm.fwd0_full = reinterpret_cast<const int64_t*>(b + off[10]);
     t->dm.tf0 = reinterpret_cast<const int64_t*>(b + off[11]);
-    // blob must outlive the async copy
-    CK(cudaStreamSynchronize(t->stream));
+    t->stack = reinterpret_cast<int4*>(b + off[12]);
+    t->dout = reinterpret_cast<int64_t*>(b + off[13]);
+    t->opt = b + off[14];
+    t->arg = reinterpret_cast<uint16_t*>(b + off[15]);
+    return RKR_OK;
+}
+
+rkr_status enqueue_fill(rkr_table* t) {
+    LaunchCtx c = t->ctx();
+    if (launch_init_pads(c) || launch_fill_all(c)) return cuda_fail(cudaGetLastError(), "fill launch");
     return RKR_OK;
 }
 
@@ -277,23 +362,20 @@ rkr_status create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max, const 
     const int want = exec ? exec->width : RKR_WIDTH_AUTO;
     t->width = (want != RKR_WIDTH_64 && t->hm.bounded32) ? 32 : 64;
     int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= t->device) {
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= t->device || t->device < 0) {
         cudaGetLastError();
         delete t;
         return fail(RKR_ERR_CUDA, "no CUDA device %d visible (librkr has no CPU fallback)",
                     exec ? exec->device : 0);
     }
     DeviceGuard dg(t->device);
-    if (exec && exec->stream) {
-        t->stream = static_cast<cudaStream_t>(exec->stream);
-    } else {
-        cudaError_t e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking);
-        if (e != cudaSuccess) {
-            delete t;
-            return cuda_fail(e, "cudaStreamCreate");
-        }
-        t->own_stream = true;
+    cudaStream_t shared = nullptr;
+    cudaError_t e = device_ctx(t->device, &shared);
+    if (e != cudaSuccess) {
+        delete t;
+        return cuda_fail(e, "device context");
     }
+    t->stream = (exec && exec->stream) ? static_cast<cudaStream_t>(exec->stream) : shared;
     // geometry
     const HostMenu& h = t->hm;
     int64_t maxshift = 0;
@@ -306,31 +388,11 @@ rkr_status create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max, const 
     t->g.sr = round_up((int64_t)t->g.pad + m_max + 1, 32);
     t->g.sa = round_up((int64_t)m_max + 1, 64);
     t->g.rows = (int64_t)h.L * (h.L + 1) / 2;
-    const size_t vbytes = t->width == 32 ? 4 : 8;
-#define CKT(call)                                         \
-    do {                                                  \
-        cudaError_t e_ = (call);                          \
-        if (e_ != cudaSuccess) {                          \
-            rkr_status s_ = cuda_fail(e_, #call);         \
-            free_table(t);                                \
-            return s_;                                    \
-        }                                                 \
-    } while (0)
-    CKT(cudaMalloc(&t->opt, (size_t)t->g.rows * t->g.sr * vbytes));
-    CKT(cudaMalloc(reinterpret_cast<void**>(&t->arg), (size_t)t->g.rows * t->g.sa * 2));
-    CKT(cudaMalloc(reinterpret_cast<void**>(&t->stack), sizeof(int4) * (2 * (size_t)h.L + 16)));
-    CKT(cudaMalloc(reinterpret_cast<void**>(&t->dout), 8 * sizeof(int64_t)));
-    CKT(cudaMallocHost(reinterpret_cast<void**>(&t->hout), 8 * sizeof(int64_t)));
-    st = upload_menu(t);
+    st = alloc_and_upload(t);
+    if (st == RKR_OK) st = enqueue_fill(t);
     if (st != RKR_OK) {
         free_table(t);
         return st;
-    }
-    LaunchCtx c = t->ctx();
-    if (launch_init_pads(c) || launch_fill_all(c)) {
-        rkr_status s = cuda_fail(cudaGetLastError(), "fill launch");
-        free_table(t);
-        return s;
     }
     *out = t;
     return RKR_OK;
@@ -539,48 +601,81 @@ rkr_status rkr_table_download(const rkr_table* t, int64_t* opt, int8_t* kind, in
     return export_rows_host(t, 0, t->g.rows, opt, kind, value);
 }
 
-rkr_status rkr_backtrack(const rkr_table* tc, int32_t s, int32_t tt, int32_t m, rkr_op* ops,
-                         int64_t cap, int64_t* n_ops) {
-    rkr_table* t = const_cast<rkr_table*>(tc);  // scratch buffers only
+rkr_status rkr_backtrack_async(rkr_table* t, int32_t s, int32_t tt, int32_t m) {
     rkr_status st = check_cell(t, s, tt);
     if (st) return st;
+    DeviceGuard dg(t->device);
+    if (t->dops_cap == 0) {
+        const int64_t cap = std::max<int64_t>(4096, 8 * (int64_t)t->g.L + 64);
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->dops), (size_t)cap * 12, t->stream));
+        t->dops_cap = cap;
+    }
+    if (launch_backtrack(t->ctx(), s, tt, m, t->dops, t->dops_cap,
+                         reinterpret_cast<int32_t*>(t->stack), t->dout))
+        return cuda_fail(cudaGetLastError(), "backtrack launch");
+    t->bt_s = s;
+    t->bt_t = tt;
+    t->bt_m = m;
+    t->bt_pending = true;
+    return RKR_OK;
+}
+
+rkr_status rkr_backtrack_fetch(rkr_table* t, rkr_op* ops, int64_t cap, int64_t* n_ops) {
+    if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
     if (!n_ops || (cap > 0 && !ops)) return fail(RKR_ERR_ARGUMENT, "null output");
+    if (!t->bt_pending) return fail(RKR_ERR_ARGUMENT, "no backtrack enqueued on this table");
     DeviceGuard dg(t->device);
     *n_ops = 0;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        if (t->dops_cap < 1024) {
-            CK(cudaMalloc(reinterpret_cast<void**>(&t->dops), 1024 * 12));
-            t->dops_cap = 1024;
-        }
-        LaunchCtx c = t->ctx();
-        if (launch_backtrack(c, s, tt, m, t->dops, t->dops_cap,
+    CK(cudaMemcpyAsync(t->hout, t->dout, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    int64_t n = t->hout[0];
+    if (n > t->dops_cap) {  // grow the device op buffer and walk again (rare)
+        CK(cudaFreeAsync(t->dops, t->stream));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->dops), (size_t)n * 12, t->stream));
+        t->dops_cap = n;
+        if (launch_backtrack(t->ctx(), t->bt_s, t->bt_t, t->bt_m, t->dops, t->dops_cap,
                              reinterpret_cast<int32_t*>(t->stack), t->dout))
             return cuda_fail(cudaGetLastError(), "backtrack launch");
         CK(cudaMemcpyAsync(t->hout, t->dout, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost,
                            t->stream));
         CK(cudaStreamSynchronize(t->stream));
-        const int64_t n = t->hout[0];
-        if (n > t->dops_cap) {  // grow the device buffer and walk again
-            cudaFree(t->dops);
-            t->dops = nullptr;
-            t->dops_cap = 0;
-            CK(cudaMalloc(reinterpret_cast<void**>(&t->dops), (size_t)n * 12));
-            t->dops_cap = n;
-            continue;
-        }
-        const int64_t status = t->hout[1];
-        const int64_t ncopy = std::min(n, cap);
-        if (ncopy > 0)
-            CK(cudaMemcpy(ops, t->dops, (size_t)ncopy * 12, cudaMemcpyDeviceToHost));
-        *n_ops = n;
-        if (status == 2)
-            return fail(RKR_ERR_INFEASIBLE, "no feasible schedule for blocks %lld..%lld",
-                        (long long)t->hout[2], (long long)t->hout[3]);
-        if (n > cap) return fail(RKR_ERR_CAPACITY, "schedule needs %lld ops", (long long)n);
-        return RKR_OK;
+        n = t->hout[0];
     }
-    return fail(RKR_ERR_CUDA, "backtrack did not converge");
+    t->bt_pending = false;
+    const int64_t status = t->hout[1];
+    const int64_t ncopy = std::min(n, cap);
+    if (ncopy > 0) {
+        CK(cudaMemcpyAsync(ops, t->dops, (size_t)ncopy * 12, cudaMemcpyDeviceToHost, t->stream));
+        CK(cudaStreamSynchronize(t->stream));
+    }
+    *n_ops = n;
+    if (status == 2)
+        return fail(RKR_ERR_INFEASIBLE, "no feasible schedule for blocks %lld..%lld",
+                    (long long)t->hout[2], (long long)t->hout[3]);
+    if (n > cap) return fail(RKR_ERR_CAPACITY, "schedule needs %lld ops", (long long)n);
+    return RKR_OK;
 }
+
+rkr_status rkr_backtrack(const rkr_table* tc, int32_t s, int32_t tt, int32_t m, rkr_op* ops,
+                         int64_t cap, int64_t* n_ops) {
+    rkr_table* t = const_cast<rkr_table*>(tc);  // scratch buffers only
+    if (!n_ops || (cap > 0 && !ops)) return fail(RKR_ERR_ARGUMENT, "null output");
+    rkr_status st = rkr_backtrack_async(t, s, tt, m);
+    if (st) return st;
+    return rkr_backtrack_fetch(t, ops, cap, n_ops);
+}
+
+rkr_status rkr_table_refill(rkr_table* t) {
+    if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
+    DeviceGuard dg(t->device);
+    return enqueue_fill(t);
+}
+
+void* rkr_table_stream(const rkr_table* t) { return t ? (void*)t->stream : nullptr; }
+
+int64_t rkr_table_h2d_bytes(const rkr_table* t) { return t ? (int64_t)t->menu_bytes : 0; }
+
+int64_t rkr_table_device_bytes(const rkr_table* t) { return t ? (int64_t)t->block_bytes : 0; }
 
 rkr_status rkr_first_feasible(const rkr_table* t, int32_t s, int32_t tt, int32_t* m_out) {
     rkr_status st = check_cell(t, s, tt);
@@ -592,10 +687,10 @@ rkr_status rkr_first_feasible(const rkr_table* t, int32_t s, int32_t tt, int32_t
     CK(cudaMemcpyAsync(dm, &big, 4, cudaMemcpyHostToDevice, t->stream));
     if (launch_first_feasible(t->ctx(), s, tt, dm))
         return cuda_fail(cudaGetLastError(), "first_feasible launch");
-    int32_t* hm = reinterpret_cast<int32_t*>(t->hout);
-    CK(cudaMemcpyAsync(hm, dm, 4, cudaMemcpyDeviceToHost, t->stream));
+    int32_t hm = big;
+    CK(cudaMemcpyAsync(&hm, dm, 4, cudaMemcpyDeviceToHost, t->stream));
     CK(cudaStreamSynchronize(t->stream));
-    *m_out = hm[0] == big ? -1 : hm[0];
+    *m_out = hm == big ? -1 : hm;
     return RKR_OK;
 }
 

@@ -99,6 +99,15 @@ def lib() -> ctypes.CDLL:
     L.rkr_solve_chain.argtypes = [P(RkrMenu), i64, i32, P(RkrExec), P(RkrOp), i64, P(i64), P(i64),
                                   P(i64), P(i32), P(i64)]
     L.rkr_table_sync.argtypes = [p]
+    L.rkr_table_refill.argtypes = [p]
+    L.rkr_table_stream.argtypes = [p]
+    L.rkr_table_stream.restype = p
+    L.rkr_table_h2d_bytes.argtypes = [p]
+    L.rkr_table_h2d_bytes.restype = i64
+    L.rkr_table_device_bytes.argtypes = [p]
+    L.rkr_table_device_bytes.restype = i64
+    L.rkr_backtrack_async.argtypes = [p, i32, i32, i32]
+    L.rkr_backtrack_fetch.argtypes = [p, P(RkrOp), i64, P(i64)]
     _lib = L
     return L
 
@@ -227,6 +236,29 @@ class DpTable:
 
     def sync(self) -> None:
         _check(self._lib.rkr_table_sync(self._h))
+
+    # device-resident re-solve hooks (bench.py)
+    def refill(self) -> None:
+        """Enqueue the whole fill again from the device-resident menu (async)."""
+        _check(self._lib.rkr_table_refill(self._h))
+
+    def stream(self) -> int:
+        return self._lib.rkr_table_stream(self._h) or 0
+
+    def h2d_bytes(self) -> int:
+        return self._lib.rkr_table_h2d_bytes(self._h)
+
+    def device_bytes(self) -> int:
+        return self._lib.rkr_table_device_bytes(self._h)
+
+    def backtrack_async(self, s: int, t: int, m: int) -> None:
+        _check(self._lib.rkr_backtrack_async(self._h, s, t, m))
+
+    def backtrack_fetch(self, cap: int = 1 << 16) -> List[Tuple[int, int, int]]:
+        buf = (RkrOp * cap)()
+        n = ctypes.c_int64()
+        _check(self._lib.rkr_backtrack_fetch(self._h, buf, cap, ctypes.byref(n)))
+        return [(buf[i].kind, buf[i].block, buf[i].option) for i in range(n.value)]
 
     @property
     def max_candidates_per_cell(self) -> int:

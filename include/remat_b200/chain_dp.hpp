@@ -119,6 +119,7 @@ struct ExecConfig {
     int device = 0;
     void* stream = nullptr;
     bool force_int64 = false;
+    int kernel = RKR_KERNEL_PERSISTENT;  // or RKR_KERNEL_DIAGONAL
 };
 
 // chain_dp.hpp:54-196.  Construction fills every cell on the GPU.
@@ -130,6 +131,7 @@ public:
         ex.device = cfg.device;
         ex.stream = cfg.stream;
         ex.width = cfg.force_int64 ? RKR_WIDTH_64 : RKR_WIDTH_AUTO;
+        ex.kernel = cfg.kernel;
         rkr_table* h = nullptr;
         detail::check(rkr_table_create(&flat.view, unit, m_max, &ex, &h));
         h_.reset(h);
@@ -248,6 +250,7 @@ inline ChainSolution solve_chain(const Chain& chain, const OptionMenu& menu, Byt
     ex.device = cfg.device;
     ex.stream = cfg.stream;
     ex.width = cfg.force_int64 ? RKR_WIDTH_64 : RKR_WIDTH_AUTO;
+    ex.kernel = cfg.kernel;
     std::vector<rkr_op> raw(4096);
     int64_t n = 0, opt_time = 0, unit = 1, min_feasible = -1;
     int32_t m_top = 0;

@@ -84,13 +84,19 @@ typedef enum {
     RKR_WIDTH_64 = 64   /* force the general int64 kernels */
 } rkr_width;
 
-/* Execution settings; pass NULL for defaults (device 0, the library's own
- * stream, auto width). */
+typedef enum {
+    RKR_KERNEL_PERSISTENT = 0, /* one persistent, dataflow-scheduled launch per fill (default) */
+    RKR_KERNEL_DIAGONAL = 1    /* one launch per anti-diagonal (the simple wavefront) */
+} rkr_kernel;
+
+/* Execution settings; pass NULL for defaults (device 0, the library's shared
+ * per-device stream, auto width, persistent kernel). */
 typedef struct {
     int32_t device;
-    void* stream;       /* cudaStream_t, or NULL for a stream owned by the handle */
+    void* stream;       /* cudaStream_t, or NULL for the library's per-device stream */
     int32_t width;      /* rkr_width */
-    int32_t reserved[5];
+    int32_t kernel;     /* rkr_kernel */
+    int32_t reserved[4];
 } rkr_exec;
 
 typedef struct rkr_table rkr_table;

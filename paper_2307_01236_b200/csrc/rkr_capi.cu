@@ -240,6 +240,9 @@ struct rkr_table {
     int32_t* dops = nullptr;      // device op buffer (separate, grows on demand)
     int64_t dops_cap = 0;
     bool bt_pending = false;
+    int kernel = 0;
+    void* sched = nullptr;
+    size_t sched_bytes = 0;
     int32_t bt_s = 0, bt_t = 0, bt_m = 0;
 
     LaunchCtx ctx() const {
@@ -251,6 +254,9 @@ struct rkr_table {
         c.width = width;
         c.max_opts = hm.max_opts;
         c.stream = stream;
+        c.kernel = kernel;
+        c.sched = sched;
+        c.sched_bytes = sched_bytes;
         return c;
     }
 };
@@ -293,8 +299,9 @@ rkr_status alloc_and_upload(rkr_table* t) {
     take(sizeof(int4) * (2 * L + 16));         // 12 backtrack stack
     take(8 * sizeof(int64_t));                 // 13 dout
     const size_t vbytes = t->width == 32 ? 4 : 8;
-    take((size_t)t->g.rows * t->g.sr * vbytes);  // 14 opt
+    take(((size_t)t->g.rows * t->g.sr + kOptSlack) * vbytes);  // 14 opt
     take((size_t)t->g.rows * t->g.sa * 2);       // 15 arg
+    take(persistent_sched_bytes(t->g));          // 16 K1p scheduler state
     t->menu_bytes = menu_bytes;
     t->block_bytes = bytes;
 
@@ -337,6 +344,8 @@ rkr_status alloc_and_upload(rkr_table* t) {
     t->dout = reinterpret_cast<int64_t*>(b + off[13]);
     t->opt = b + off[14];
     t->arg = reinterpret_cast<uint16_t*>(b + off[15]);
+    t->sched = b + off[16];
+    t->sched_bytes = persistent_sched_bytes(t->g);
     return RKR_OK;
 }
 
@@ -360,6 +369,7 @@ rkr_status create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max, const 
     t->unit = unit;
     t->device = exec ? exec->device : 0;
     const int want = exec ? exec->width : RKR_WIDTH_AUTO;
+    t->kernel = exec ? exec->kernel : RKR_KERNEL_PERSISTENT;
     t->width = (want != RKR_WIDTH_64 && t->hm.bounded32) ? 32 : 64;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= t->device || t->device < 0) {

@@ -65,7 +65,15 @@ struct LaunchCtx {
     int32_t width;      // 32 or 64
     int32_t max_opts;   // max saved options per block
     void* stream;       // cudaStream_t
+    int32_t kernel;     // 0 = persistent dataflow fill (K1p), 1 = one launch per diagonal (K1)
+    void* sched;        // K1p scheduler state: counter + per-(diagonal, tile) done flags
+    size_t sched_bytes;
 };
+
+// K1p (rkr_persist.cu)
+size_t persistent_sched_bytes(const Geometry& g);
+int launch_fill_persistent(const LaunchCtx& c);
+constexpr int64_t kOptSlack = 4096;  // elements past the last row (tile over-reads)
 
 int launch_init_pads(const LaunchCtx& c);
 int launch_fill_all(const LaunchCtx& c);

@@ -368,6 +368,7 @@ int launch_init_pads(const LaunchCtx& c) {
 }
 
 int launch_fill_all(const LaunchCtx& c) {
+    if (c.kernel == 0) return launch_fill_persistent(c);
     return c.width == 32 ? fill_all_t<uint32_t>(c) : fill_all_t<int64_t>(c);
 }
 

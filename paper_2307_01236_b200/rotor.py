@@ -57,7 +57,7 @@ class RkrOp(ctypes.Structure):
 
 class RkrExec(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("stream", ctypes.c_void_p), ("width", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
 
 
 _lib = None
@@ -125,11 +125,16 @@ def _check(st: int, min_feasible: int = -1) -> None:
     raise DeviceError(f"librkr status {st}: {msg}")
 
 
-def _exec(device: int, width: str, stream: Optional[int] = None) -> RkrExec:
+KERNELS = {"persistent": 0, "diagonal": 1}
+
+
+def _exec(device: int, width: str, stream: Optional[int] = None,
+          kernel: str = "persistent") -> RkrExec:
     e = RkrExec()
     e.device = device
     e.stream = stream
     e.width = 64 if width == "64" else 0
+    e.kernel = KERNELS[kernel]
     return e
 
 
@@ -191,11 +196,11 @@ class DpTable:
     """remat::DpTable (chain_dp.hpp:54-196); cells live in device memory."""
 
     def __init__(self, menu: Menu, unit: int, m_max: int, device: int = 0, width: str = "auto",
-                 stream: Optional[int] = None):
+                 stream: Optional[int] = None, kernel: str = "persistent"):
         self._lib = lib()
         self._h = ctypes.c_void_p()
         self._menu_struct = menu.struct()
-        ex = _exec(device, width, stream)
+        ex = _exec(device, width, stream, kernel)
         _check(self._lib.rkr_table_create(ctypes.byref(self._menu_struct), unit, m_max,
                                           ctypes.byref(ex), ctypes.byref(self._h)))
         self.menu = menu

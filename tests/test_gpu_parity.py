@@ -14,6 +14,7 @@ pytestmark = pytest.mark.gpu
 
 INF = rotor.K_INF_TIME
 WIDTHS = ["auto", "64"]
+KERNELS = ["persistent", "diagonal"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -21,8 +22,8 @@ def _device():
     assert rotor.lib().rkr_device_ok(0) == 1, "no sm_100 device visible"
 
 
-def dev_tables(menu, unit, M, width="auto"):
-    with rotor.DpTable(menu, unit, M, width=width) as t:
+def dev_tables(menu, unit, M, width="auto", kernel="persistent"):
+    with rotor.DpTable(menu, unit, M, width=width, kernel=kernel) as t:
         o, k, v = t.download()
         return o, k, v, t.width()
 
@@ -100,11 +101,12 @@ def test_solve_chain_kats(kat):
 @pytest.mark.parametrize("suite", ["monotone", "ample", "symmetry", "enumeration", "work_bound",
                                    "relaxed"])
 @pytest.mark.parametrize("width", WIDTHS)
-def test_random_suites_whole_tables(random_suites, suite, width):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_random_suites_whole_tables(random_suites, suite, width, kernel):
     S = random_suites[suite]
     for e in S["menus"]:
         menu = Menu.from_json(e["menu"])
-        o, k, v, _ = dev_tables(menu, 1, S["M"], width)
+        o, k, v, _ = dev_tables(menu, 1, S["M"], width, kernel)
         if "opt" in e:
             assert o.tolist() == e["opt"]
             assert k.tolist() == e["kind"]
@@ -155,10 +157,11 @@ def test_class_permutation_symmetry(random_suites):
 # Synthetic chains against golden digests and the oracle
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("width", WIDTHS)
-def test_synthetic_golden_tables(synthetic, width):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_synthetic_golden_tables(synthetic, width, kernel):
     for e in synthetic["tables"]:
         menu = synthetic_menu(e["L"], e["B"], e["M"], e["seed"], tie_stress=e["tie_stress"])
-        o, k, v, _ = dev_tables(menu, 1, e["M"], width)
+        o, k, v, _ = dev_tables(menu, 1, e["M"], width, kernel)
         assert table_digest(o, k, v) == e["digest"], (e["L"], e["M"])
         L = e["L"]
         r = tri_row(L, 0, L - 1)
@@ -187,13 +190,14 @@ def test_config1_solves_with_replay(synthetic, orc):
     (2, 40, 60, 15, True), (1, 4, 30, 16, False),
 ])
 @pytest.mark.parametrize("width", WIDTHS)
-def test_fresh_synthetic_vs_oracle(orc, L, B, M, seed, tie, width):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_fresh_synthetic_vs_oracle(orc, L, B, M, seed, tie, width, kernel):
     menu = synthetic_menu(L, B, M, seed, tie_stress=tie)
     st, *ref = orc.fill(menu, 1, M)
     assert st == 0
-    o, k, v, _ = dev_tables(menu, 1, M, width)
+    o, k, v, _ = dev_tables(menu, 1, M, width, kernel)
     assert_same((o, k, v), ref[:3])
-    with rotor.DpTable(menu, 1, M, width=width) as t:
+    with rotor.DpTable(menu, 1, M, width=width, kernel=kernel) as t:
         assert t.max_candidates_per_cell == ref[3]
         ff = t.first_feasible(0, L - 1)
         top = ref[0][tri_row(L, 0, L - 1)]
@@ -210,13 +214,33 @@ def test_fresh_synthetic_vs_oracle(orc, L, B, M, seed, tie, width):
                         t.backtrack(s, tt, m)
 
 
-def test_config3_reduced_twin_vs_oracle(orc):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config3_reduced_twin_vs_oracle(orc, kernel):
     """GPT-2-XL-like chain (L=96, B=32) at M=1024: whole table bit-exact."""
     menu = synthetic_menu(96, 32, 1024, 45)
     st, *ref = orc.fill(menu, 1, 1024)
-    o, k, v, w = dev_tables(menu, 1, 1024)
+    o, k, v, w = dev_tables(menu, 1, 1024, "auto", kernel)
     assert w == 32
     assert_same((o, k, v), ref[:3])
+
+
+@pytest.mark.parametrize("M", [9000, 20000])
+def test_wide_budget_twin_vs_oracle(orc, M):
+    """Several column groups, halo tiles and R=2 tiles (persistent kernel), both widths."""
+    menu = synthetic_menu(24, 6, M, 46, tie_stress=True)
+    st, *ref = orc.fill(menu, 1, M)
+    for width in WIDTHS:
+        assert_same(dev_tables(menu, 1, M, width)[:3], ref[:3])
+
+
+def test_persistent_matches_diagonal_full_config3():
+    """Full config 3: the persistent dataflow fill and the per-diagonal fill
+    produce identical tables (sampled rows + digest of the top rows)."""
+    L, M = 96, 16384
+    menu = synthetic_menu(L, 32, M, 45)
+    with rotor.DpTable(menu, 1, M) as a, rotor.DpTable(menu, 1, M, kernel="diagonal") as b:
+        for (s, tt) in ((0, L - 1), (1, L - 1), (0, L - 2), (5, 60), (40, 41), (17, 17)):
+            assert_same(a.row(s, tt), b.row(s, tt))
 
 
 def test_config2_full_both_widths(synthetic):
@@ -296,8 +320,8 @@ def test_edge_menus_vs_oracle(orc, idx, M, unit):
     menu = _edge_menus()[idx]
     st, *ref = orc.fill(menu, unit, M)
     assert st == 0
-    for width in WIDTHS:
-        o, k, v, w = dev_tables(menu, unit, M, width)
+    for width, kernel in ((w_, k_) for w_ in WIDTHS for k_ in KERNELS):
+        o, k, v, w = dev_tables(menu, unit, M, width, kernel)
         if idx in (2, 3):
             assert w == 64
         assert_same((o, k, v), ref[:3])

@@ -337,7 +337,7 @@ def b200_arm(args, world, rank, local):
                      "peak_source": peak_src},
         "clocks": sampler.summary(),
     }
-    if world == 1:
+    if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(args.config, menu, L, M)
     print(json.dumps(line), flush=True)
     table.close()
@@ -350,6 +350,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
+    ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU leg (tuning runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     world, rank, local = dist_setup()

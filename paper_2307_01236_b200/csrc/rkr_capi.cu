@@ -241,8 +241,11 @@ struct rkr_table {
     int64_t dops_cap = 0;
     bool bt_pending = false;
     int kernel = 0;
-    void* sched = nullptr;
-    size_t sched_bytes = 0;
+    PersistPlan plan;
+    PlanDev pdev{};
+    ProgDev prog{};
+    size_t state_bytes = 0;
+    unsigned long long* trace = nullptr;
     int32_t bt_s = 0, bt_t = 0, bt_m = 0;
 
     LaunchCtx ctx() const {
@@ -255,8 +258,9 @@ struct rkr_table {
         c.max_opts = hm.max_opts;
         c.stream = stream;
         c.kernel = kernel;
-        c.sched = sched;
-        c.sched_bytes = sched_bytes;
+        c.plan = pdev;
+        c.prog = prog;
+        c.state_bytes = state_bytes;
         return c;
     }
 };
@@ -266,6 +270,7 @@ namespace {
 void free_table(rkr_table* t) {
     if (!t) return;
     DeviceGuard dg(t->device);
+    if (t->trace) cudaFreeAsync(t->trace, t->stream);
     if (t->block) cudaFreeAsync(t->block, t->stream);
     if (t->dops) cudaFreeAsync(t->dops, t->stream);
     delete t;
@@ -295,13 +300,27 @@ rkr_status alloc_and_upload(rkr_table* t) {
     take(nq * 4);                              // 7 ids
     take((L + 1) * 8);                         // 8 act_u
     for (int i = 0; i < 3; ++i) take(L * 8);   // 9..11 fwd0_own, fwd0_full, tf0
+    const size_t np = t->plan.start.size();
+    take(np * 8);                              // 12 plan start
+    take(np * 4);                              // 13 plan g
+    take(np * 4);                              // 14 plan k
     const size_t menu_bytes = bytes;
-    take(sizeof(int4) * (2 * L + 16));         // 12 backtrack stack
-    take(8 * sizeof(int64_t));                 // 13 dout
+    take(sizeof(int4) * (2 * L + 16));         // 15 backtrack stack
+    take(8 * sizeof(int64_t));                 // 16 dout
     const size_t vbytes = t->width == 32 ? 4 : 8;
-    take(((size_t)t->g.rows * t->g.sr + kOptSlack) * vbytes);  // 14 opt
-    take((size_t)t->g.rows * t->g.sa * 2);       // 15 arg
-    take(persistent_sched_bytes(t->g));          // 16 K1p scheduler state
+    take(((size_t)t->g.rows * t->g.sr + kOptSlack) * vbytes);  // 17 opt
+    take((size_t)t->g.rows * t->g.sa * 2);       // 18 arg
+    t->state_bytes = persistent_state_bytes(t->g, t->plan);
+    take(t->state_bytes);                        // 19 K1p counter + done flags
+    const bool progs = t->kernel == RKR_KERNEL_PERSISTENT;
+    const size_t nc = progs ? (size_t)program_cut_entries(t->g) : 0;
+    const size_t ocap = std::max<int32_t>(h.max_opts, 1);
+    take(nc * 16);                               // 20 program ptr
+    take(nc * vbytes);                           // 21 program sweep
+    take(nc * 4);                                // 22 program gate
+    take(progs ? (size_t)t->g.rows * ocap * 4 : 0);  // 23 program thr
+    take(progs ? nq * 4 : 0);                    // 24 program pc
+    take(progs ? nq * vbytes : 0);               // 25 program otot
     t->menu_bytes = menu_bytes;
     t->block_bytes = bytes;
 
@@ -324,6 +343,9 @@ rkr_status alloc_and_upload(rkr_table* t) {
     put(9, h.fwd0_own.data(), L * 8);
     put(10, h.fwd0_full.data(), L * 8);
     put(11, h.tf0.data(), L * 8);
+    put(12, t->plan.start.data(), np * 8);
+    put(13, t->plan.g.data(), np * 4);
+    put(14, t->plan.k.data(), np * 4);
     CK(cudaMallocAsync(&t->block, bytes, t->stream));
     CK(cudaMemcpyAsync(t->block, blob, menu_bytes, cudaMemcpyHostToDevice, t->stream));
     CK(cudaEventRecord(t_stage.done, t->stream));
@@ -340,16 +362,36 @@ rkr_status alloc_and_upload(rkr_table* t) {
     t->dm.fwd0_own = reinterpret_cast<const int64_t*>(b + off[9]);
     t->dm.fwd0_full = reinterpret_cast<const int64_t*>(b + off[10]);
     t->dm.tf0 = reinterpret_cast<const int64_t*>(b + off[11]);
-    t->stack = reinterpret_cast<int4*>(b + off[12]);
-    t->dout = reinterpret_cast<int64_t*>(b + off[13]);
-    t->opt = b + off[14];
-    t->arg = reinterpret_cast<uint16_t*>(b + off[15]);
-    t->sched = b + off[16];
-    t->sched_bytes = persistent_sched_bytes(t->g);
+    t->stack = reinterpret_cast<int4*>(b + off[15]);
+    t->dout = reinterpret_cast<int64_t*>(b + off[16]);
+    t->opt = b + off[17];
+    t->arg = reinterpret_cast<uint16_t*>(b + off[18]);
+    PlanDev& pd = t->pdev;
+    pd.R = t->plan.R;
+    pd.TM = t->plan.TM;
+    pd.J = t->plan.J;
+    pd.dj = t->plan.dj;
+    pd.seg_cap = t->plan.seg_cap;
+    pd.n_plan = (int32_t)np;
+    pd.total = t->plan.total;
+    pd.start = reinterpret_cast<const int64_t*>(b + off[12]);
+    pd.g = reinterpret_cast<const int32_t*>(b + off[13]);
+    pd.k = reinterpret_cast<const int32_t*>(b + off[14]);
+    pd.counter = reinterpret_cast<unsigned long long*>(b + off[19]);
+    pd.done = reinterpret_cast<int32_t*>(b + off[19] + 8);
+    pd.trace = nullptr;
+    t->prog.ptr = b + off[20];
+    t->prog.sweep = b + off[21];
+    t->prog.gate = reinterpret_cast<int32_t*>(b + off[22]);
+    t->prog.thr = reinterpret_cast<int32_t*>(b + off[23]);
+    t->prog.pc = reinterpret_cast<int32_t*>(b + off[24]);
+    t->prog.otot = b + off[25];
+    t->prog.nq = (int64_t)h.ids.size();
     return RKR_OK;
 }
 
 rkr_status enqueue_fill(rkr_table* t) {
+    t->pdev.trace = t->trace;
     LaunchCtx c = t->ctx();
     if (launch_init_pads(c) || launch_fill_all(c)) return cuda_fail(cudaGetLastError(), "fill launch");
     return RKR_OK;
@@ -398,7 +440,10 @@ rkr_status create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max, const 
     t->g.sr = round_up((int64_t)t->g.pad + m_max + 1, 32);
     t->g.sa = round_up((int64_t)m_max + 1, 64);
     t->g.rows = (int64_t)h.L * (h.L + 1) / 2;
+    if (t->kernel == RKR_KERNEL_PERSISTENT) persistent_plan(t->g, t->width, t->plan);
     st = alloc_and_upload(t);
+    if (st == RKR_OK && t->kernel == RKR_KERNEL_PERSISTENT && launch_prep_programs(t->ctx()))
+        st = cuda_fail(cudaGetLastError(), "program launch");
     if (st == RKR_OK) st = enqueue_fill(t);
     if (st != RKR_OK) {
         free_table(t);
@@ -679,6 +724,42 @@ rkr_status rkr_table_refill(rkr_table* t) {
     if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
     DeviceGuard dg(t->device);
     return enqueue_fill(t);
+}
+
+rkr_status rkr_debug_trace(rkr_table* t, int32_t enable) {
+    if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
+    DeviceGuard dg(t->device);
+    if (enable && !t->trace && t->kernel == RKR_KERNEL_PERSISTENT) {
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->trace), (size_t)t->plan.total * 32,
+                           t->stream));
+        CK(cudaMemsetAsync(t->trace, 0, (size_t)t->plan.total * 32, t->stream));
+    } else if (!enable && t->trace) {
+        CK(cudaFreeAsync(t->trace, t->stream));
+        t->trace = nullptr;
+    }
+    return RKR_OK;
+}
+
+int64_t rkr_debug_trace_items(const rkr_table* t) {
+    return (t && t->trace) ? t->plan.total : 0;
+}
+
+rkr_status rkr_debug_trace_read(const rkr_table* t, uint64_t* out, int32_t* item_k,
+                                int32_t* item_j) {
+    if (!t || !t->trace) return fail(RKR_ERR_ARGUMENT, "tracing not enabled");
+    DeviceGuard dg(t->device);
+    CK(cudaStreamSynchronize(t->stream));
+    CK(cudaMemcpy(out, t->trace, (size_t)t->plan.total * 32, cudaMemcpyDeviceToHost));
+    // item -> (k, j) from the host copy of the plan
+    const PersistPlan& p = t->plan;
+    for (size_t e = 0; e < p.start.size(); ++e) {
+        const int64_t n = t->g.L - p.k[e];
+        for (int64_t i = 0; i < n; ++i) {
+            if (item_k) item_k[p.start[e] + i] = p.k[e];
+            if (item_j) item_j[p.start[e] + i] = p.g[e];
+        }
+    }
+    return RKR_OK;
 }
 
 void* rkr_table_stream(const rkr_table* t) { return t ? (void*)t->stream : nullptr; }

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 namespace rkr {
 
@@ -56,6 +57,41 @@ __host__ __device__ inline int64_t row_id(int32_t L, int32_t s, int32_t t) {
     return diag_off(L, t - s) + s;
 }
 
+// K1p schedule (rkr_persist.cu).  Work items are (column group g, diagonal k,
+// tile j in the group, s).  Groups are GW = 1 tile wide; their diagonal
+// sweeps are interleaved with a lag of `lambda` diagonals (item order key
+// tau = lambda * g + k), so about L / lambda groups are in flight: enough
+// items to fill the GPU, few enough that their rows stay in L2.
+struct PersistPlan {
+    int32_t R = 1, TM = 256, J = 1, dj = 0, seg_cap = 0, lambda = 1;
+    int64_t total = 0;
+    std::vector<int64_t> start;  // first item index of each (g, k) plan entry, in key order
+    std::vector<int32_t> g, k;   // the entry's group and diagonal
+};
+struct PlanDev {
+    int32_t R, TM, J, dj, seg_cap, n_plan;
+    int64_t total;
+    const int64_t* start;
+    const int32_t* g;
+    const int32_t* k;
+    int32_t* done;                   // [L * J] rows completed per (diagonal, tile)
+    unsigned long long* counter;     // next item
+    unsigned long long* trace;       // optional: 4 globaltimer stamps per item (nullptr = off)
+};
+// Per-table cell programs (K1p), filled by launch_prep_programs.
+struct ProgDev {
+    void* ptr;        // longlong2 [cut entries]
+    void* sweep;      // V [cut entries]
+    int32_t* gate;    // [cut entries]
+    int32_t* thr;     // [rows * max_opts]
+    int32_t* pc;      // [saved options]
+    void* otot;       // V [saved options]
+    int64_t nq;
+};
+int64_t program_cut_entries(const Geometry& g);
+void persistent_plan(const Geometry& g, int width, PersistPlan& p);
+size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p);  // counter + flags
+
 // Launch entry points (rkr_kernels.cu).
 struct LaunchCtx {
     Geometry g;
@@ -66,13 +102,13 @@ struct LaunchCtx {
     int32_t max_opts;   // max saved options per block
     void* stream;       // cudaStream_t
     int32_t kernel;     // 0 = persistent dataflow fill (K1p), 1 = one launch per diagonal (K1)
-    void* sched;        // K1p scheduler state: counter + per-(diagonal, tile) done flags
-    size_t sched_bytes;
+    PlanDev plan;       // K1p schedule + state (device pointers)
+    ProgDev prog;       // K1p cell programs
+    size_t state_bytes; // bytes of counter + flags to zero before each fill
 };
 
-// K1p (rkr_persist.cu)
-size_t persistent_sched_bytes(const Geometry& g);
 int launch_fill_persistent(const LaunchCtx& c);
+int launch_prep_programs(const LaunchCtx& c);
 constexpr int64_t kOptSlack = 4096;  // elements past the last row (tile over-reads)
 
 int launch_init_pads(const LaunchCtx& c);

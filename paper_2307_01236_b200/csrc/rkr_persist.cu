@@ -1,31 +1,38 @@
 // rkr_persist.cu -- K1p: the whole table fill as ONE persistent, dataflow-
-// scheduled launch (sm_100a).
+// scheduled launch (sm_100a), plus the per-table cell-program precompute.
 //
-// Work item = one cell row segment (s, t = s + k, budget tile j of TM slots).
-// Items are dequeued from a global counter in (column group, diagonal k,
-// tile j, s) order.  An item of diagonal k may start once diagonal k-1 is
-// complete on tiles [j - dj, j] (dj = halo tiles for the largest budget
-// shift); by induction that covers every row the cell reads
-// (chain_dp.hpp:148, :166-167 read only smaller spans at m' <= m).
-// Completion is published per (k, j) with a release fence + atomic counter
-// and observed with an acquire load -- no grid barrier, no per-diagonal launch.
+// Work item = one row segment of one cell: (s, t = s + k, budget tile j of
+// TM slots).  Items are dequeued from a global counter in the order of the
+// host-built plan (PersistPlan: key lambda*j + k, then s).  An item of
+// diagonal k may start once diagonal k-1 is complete on tiles [j - dj, j]
+// (dj = halo tiles of the largest budget shift); by induction that covers
+// every row the cell reads (chain_dp.hpp:148, :166-167 read only smaller
+// spans at m' <= m).  Completion is published per (k, j) with a release
+// fence + atomic add and observed with relaxed polls + one acquire fence --
+// no grid barrier, no per-diagonal launch, no deadlock (items wait only on
+// items dequeued earlier).
 //
-// Column-group ordering keeps the working set of all rows restricted to a
-// group of GW tiles (plus the halo) inside the 126 MB L2 while the wavefront
-// sweeps all diagonals over it; the next group's early diagonals overlap
-// this group's deep (low-parallelism) diagonals.
+// Cell programs.  Everything about cell (s, t) that does not depend on the
+// table -- the option thresholds of chain_dp.hpp:141-147, the row addresses
+// of every cut, the option-0 sweep prefix sums (:162) and the `break` gate
+// (:164) as a prefix maximum -- is computed once per table by prep_programs
+// and copied into shared memory by each item before it waits on its
+// dependencies, so the critical path of an item is: wait -> option window ->
+// candidate loop -> store -> publish.
 //
-// Inside an item: the candidate parameters are staged in shared memory
-// (sweep prefix sums and the `break` gate as a prefix maximum, computed with
-// a block scan), each lane computes how many cuts its budget slot admits
-// (binary search on the monotone gate), and the cut loop then runs without
-// data-dependent exits so loads stay in flight.  The option window (row
-// (s+1, t) at shifts m - pack_chg) is staged once in shared memory.
-// Tie-break: options in menu order, then cuts ascending, strict '<' -- the
-// reference's first-minimum (chain_dp.hpp:139-174).
+// Candidate loop.  Each lane first counts the cuts its budget slot admits
+// (binary search on the monotone gate), then runs the cut loop in batches of
+// U iterations whose 2*U*R loads are issued before any is consumed.  The
+// option window (row (s+1, t) at shifts m - pack_chg) is staged in shared
+// memory.  Tie-break: options in menu order, then cuts ascending, strict '<'
+// -- the reference's first minimum (chain_dp.hpp:139-174).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
+#include <vector>
 
 #include "rkr_internal.h"
 
@@ -50,229 +57,236 @@ __device__ __forceinline__ int32_t clampm(int64_t x, int32_t M) {
     return x < -1 ? -1 : (x > (int64_t)M + 1 ? M + 1 : (int32_t)x);
 }
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+__device__ __forceinline__ int ld_relaxed(const int* p) {
     int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
-struct PCfg {
-    int32_t TM;        // budget slots per item
-    int32_t J;         // tiles per row
-    int32_t GW;        // tiles per column group
-    int32_t dj;        // halo tiles
-    int32_t seg_cap;   // option-window slots staged in smem (0: read global)
-    int32_t kcap;      // max cuts per cell staged (L - 1)
-    int32_t ocap;      // max saved options per block
-    int64_t total;     // items
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <typename V>
+struct Programs {
+    longlong2* ptr;   // per cut entry: {&L(s, c-1)[0], &R(c, t)[-act_u[c]]}
+    V* sweep;         // per cut entry: sum_{j=s}^{c-1} time_fwd0[j]
+    int32_t* gate;    // per cut entry: prefix-max gate, clamped to [-1, M+1]
+    int32_t* thr;     // per (row, option): validity threshold, clamped
+    int32_t* pc;      // per saved option: pack shift clamped to pad
+    V* otot;          // per saved option: time_fwd + time_bwd
+    int64_t nq;
 };
 
+// first cut-program entry of diagonal k: sum_{k' < k} (L - k') k'
+__host__ __device__ inline int64_t diag_cut_off(int64_t L, int64_t k) {
+    return L * k * (k - 1) / 2 - (k - 1) * k * (2 * k - 1) / 6;
+}
+
+// ---------------------------------------------------------------------------
+// prep_programs: one thread per cell (s, t).
+// ---------------------------------------------------------------------------
+template <typename V>
+__global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> pr, int ocap) {
+    const int L = g.L, M = g.M;
+    for (int64_t rid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; rid < g.rows;
+         rid += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = L - 1;  // rid -> (k, s): rows are diagonal-major
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (diag_off(L, mid) <= rid)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        const int k = lo;
+        const int s = (int)(rid - diag_off(L, k));
+        const int t = s + k;
+        const bool seeded = t < L - 1;                              // chain_dp.hpp:126
+        const int64_t seed = seeded ? 2 * dm.act_u[t + 1] : 0;      // chain_dp.hpp:127
+        const int o0 = dm.blk_off[s], nopt = dm.blk_off[s + 1] - o0;
+        for (int i = 0; i < nopt; ++i) {
+            const int q = o0 + i;
+            const int64_t need = (k == 0 && seeded) ? dm.fwd_req_pre[q] + dm.act_u[t + 1]
+                                                    : dm.fwd_req[q] + seed;  // :141-143
+            int64_t th = need > dm.bwd_req[q] ? need : dm.bwd_req[q];         // :144
+            if (k > 0 && dm.pack_chg[q] > th) th = dm.pack_chg[q];            // :147
+            pr.thr[rid * ocap + i] = clampm(th, M);
+        }
+        if (k == 0) continue;
+        const int64_t base = diag_cut_off(L, k) + (int64_t)s * k;
+        const int64_t gate0 = dm.fwd0_own[s] + seed;                          // :159
+        V sweep = 0;
+        int64_t gmax = gate0;
+        for (int i = 0; i < k; ++i) {
+            const int c = s + 1 + i;
+            sweep += (V)dm.tf0[c - 1];                                        // :162
+            if (c - 1 > s) {                                                  // :164
+                const int64_t gv = dm.fwd0_full[c - 1] + seed;
+                gmax = gv > gmax ? gv : gmax;
+            }
+            const int64_t a = dm.act_u[c];
+            const int sh = a > g.pad ? g.pad : (int)a;
+            longlong2 p;
+            p.x = (long long)(opt + row_id(L, s, c - 1) * g.sr + g.pad);
+            p.y = (long long)(opt + row_id(L, c, t) * g.sr + g.pad - sh);
+            pr.ptr[base + i] = p;
+            pr.sweep[base + i] = sweep;
+            pr.gate[base + i] = clampm(gmax, M);
+        }
+    }
+    // per saved option: clamped pack shift and pass time
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < pr.nq;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = dm.pack_chg[q];
+        pr.pc[q] = p > g.pad ? g.pad : (int)p;
+        pr.otot[q] = (V)dm.tftb[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fill_persistent
+// ---------------------------------------------------------------------------
 template <typename V>
 struct PSmem {
-    long long* lptr;   // [kcap] address of L(s, c-1)[0]
-    long long* rptr;   // [kcap] address of R(c, t)[-act_u[c]]
-    V* sweep;          // [kcap] sum_{j=s}^{c-1} time_fwd0[j]
-    int32_t* gate;     // [kcap] prefix-max gate (clamped to [-1, M+1])
-    V* otot;           // [ocap]
-    int32_t* thr;      // [ocap]
-    int32_t* pc;       // [ocap]
-    V* seg;            // [seg_cap + TM]
-    V* wsum;           // [32]
-    long long* wmax;   // [32]
-    long long* item;   // [1]
+    longlong2* ptr;   // [kcap]
+    V* sweep;         // [kcap]
+    int32_t* gate;    // [kcap]
+    V* otot;          // [ocap]
+    int32_t* thr;     // [ocap]
+    int32_t* pc;      // [ocap]
+    V* seg;           // [seg_cap + TM]
+    long long* item;  // [1]
+};
+
+struct Caps {
+    int32_t kcap, ocap, seg_cap, TM;
 };
 
 template <typename V>
-__host__ __device__ inline size_t psmem_bytes(int kcap, int ocap, int seg_cap, int TM) {
-    size_t b = 0;
-    b += (size_t)kcap * 16;
-    b += (size_t)kcap * sizeof(V);
-    b = (b + 7) & ~size_t(7);
-    b += (size_t)kcap * 4;
-    b = (b + 7) & ~size_t(7);
-    b += (size_t)ocap * sizeof(V);
-    b = (b + 7) & ~size_t(7);
-    b += (size_t)ocap * 8;
-    b = (b + 7) & ~size_t(7);
-    b += (size_t)(seg_cap > 0 ? seg_cap + TM : 0) * sizeof(V);
-    b = (b + 7) & ~size_t(7);
-    b += 32 * sizeof(V) + 32 * 8 + 8;
+__host__ __device__ inline size_t psmem_bytes(const Caps& c) {
+    size_t b = (size_t)c.kcap * 16;
+    b += (size_t)c.kcap * sizeof(V);
+    b = (b + 15) & ~size_t(15);
+    b += (size_t)c.kcap * 4;
+    b = (b + 15) & ~size_t(15);
+    b += (size_t)c.ocap * sizeof(V);
+    b = (b + 15) & ~size_t(15);
+    b += (size_t)c.ocap * 8;
+    b = (b + 15) & ~size_t(15);
+    b += (size_t)(c.seg_cap > 0 ? c.seg_cap + c.TM : 0) * sizeof(V);
+    b = (b + 15) & ~size_t(15);
     return b + 16;
 }
 
 template <typename V>
-__device__ inline PSmem<V> pcarve(unsigned char* p, const PCfg& c) {
+__device__ inline PSmem<V> pcarve(unsigned char* p, const Caps& c) {
     PSmem<V> s;
     size_t b = 0;
-    s.lptr = reinterpret_cast<long long*>(p);
-    s.rptr = s.lptr + c.kcap;
+    s.ptr = reinterpret_cast<longlong2*>(p);
     b += (size_t)c.kcap * 16;
     s.sweep = reinterpret_cast<V*>(p + b);
     b += (size_t)c.kcap * sizeof(V);
-    b = (b + 7) & ~size_t(7);
+    b = (b + 15) & ~size_t(15);
     s.gate = reinterpret_cast<int32_t*>(p + b);
     b += (size_t)c.kcap * 4;
-    b = (b + 7) & ~size_t(7);
+    b = (b + 15) & ~size_t(15);
     s.otot = reinterpret_cast<V*>(p + b);
     b += (size_t)c.ocap * sizeof(V);
-    b = (b + 7) & ~size_t(7);
+    b = (b + 15) & ~size_t(15);
     s.thr = reinterpret_cast<int32_t*>(p + b);
     s.pc = s.thr + c.ocap;
     b += (size_t)c.ocap * 8;
-    b = (b + 7) & ~size_t(7);
+    b = (b + 15) & ~size_t(15);
     s.seg = reinterpret_cast<V*>(p + b);
     b += (size_t)(c.seg_cap > 0 ? c.seg_cap + c.TM : 0) * sizeof(V);
-    b = (b + 7) & ~size_t(7);
-    s.wsum = reinterpret_cast<V*>(p + b);
-    b += 32 * sizeof(V);
-    s.wmax = reinterpret_cast<long long*>(p + b);
-    b += 32 * 8;
+    b = (b + 15) & ~size_t(15);
     s.item = reinterpret_cast<long long*>(p + b);
     return s;
 }
 
-// item index -> (k, j, s); order: group, diagonal, tile, s.
-__device__ inline void decode_item(int64_t idx, int L, int64_t rows, const PCfg& c, int& k, int& j,
-                                   int& s) {
-    const int64_t per_group = (int64_t)c.GW * rows;
-    const int ng = (c.J + c.GW - 1) / c.GW;
-    int g = (int)(idx / per_group);
-    if (g > ng - 1) g = ng - 1;
-    const int64_t ig = idx - (int64_t)g * per_group;
-    const int gw = (g == ng - 1) ? c.J - g * c.GW : c.GW;
-    const int64_t q = ig / gw;  // off(k) <= q < off(k+1)
-    int lo = 0, hi = L - 1;
+// item index -> (k, j, s) through the plan table (binary search on start).
+__device__ inline void decode_item(int64_t idx, const PlanDev& p, int& k, int& j, int& s) {
+    int lo = 0, hi = p.n_plan - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (diag_off(L, mid) <= q)
+        if (__ldg(p.start + mid) <= idx)
             lo = mid;
         else
             hi = mid - 1;
     }
-    k = lo;
-    const int64_t rem = ig - (int64_t)gw * diag_off(L, k);
-    const int n = L - k;
-    j = g * c.GW + (int)(rem / n);
-    s = (int)(rem % n);
+    k = __ldg(p.k + lo);
+    j = __ldg(p.g + lo);
+    s = (int)(idx - __ldg(p.start + lo));
 }
 
-template <typename V, int NT, int R>
+template <typename V, int NT, int R, int U>
 __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V* __restrict__ opt,
-                                                      uint16_t* __restrict__ arg,
-                                                      int* __restrict__ done,
-                                                      unsigned long long* __restrict__ counter,
-                                                      PCfg c) {
+                                                      uint16_t* __restrict__ arg, PlanDev pl,
+                                                      Programs<V> pr, Caps c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr V INF = CostP<V>::inf;
-    constexpr int NW = NT / 32;
     PSmem<V> sm = pcarve<V>(smem_raw, c);
     const int L = g.L, M = g.M;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
+    int* __restrict__ done = pl.done;
+    long long next = 0;
+    if (tid == 0) next = (long long)atomicAdd(pl.counter, 1ull);
 
     for (;;) {
-        if (tid == 0) sm.item[0] = (long long)atomicAdd(counter, 1ull);
+        if (tid == 0) sm.item[0] = next;
         __syncthreads();
         const int64_t idx = sm.item[0];
-        if (idx >= c.total) break;
+        if (idx >= pl.total) break;
+        // prefetch the next item while this one runs (the earliest unfinished
+        // item is always one being processed, so this cannot deadlock)
+        if (tid == 0) next = (long long)atomicAdd(pl.counter, 1ull);
+        unsigned long long t0 = 0;
+        if (pl.trace && tid == 0) t0 = gtimer();
         int k, j, s;
-        decode_item(idx, L, g.rows, c, k, j, s);
+        decode_item(idx, pl, k, j, s);
         const int t = s + k;
-        const int m0 = j * c.TM;
-        const bool seeded = t < L - 1;                              // chain_dp.hpp:126
-        const int64_t seed = seeded ? 2 * dm.act_u[t + 1] : 0;      // chain_dp.hpp:127
-        const int o0 = dm.blk_off[s];
-        const int nopt = dm.blk_off[s + 1] - o0;
+        const int m0 = j * pl.TM;
+        const int64_t rid = row_id(L, s, t);
 
-        // ---- stage menu-derived parameters (no table reads: overlaps the wait)
+        // ---- cell program -> smem (independent of the table: overlaps the wait)
+        const int o0 = __ldg(dm.blk_off + s);
+        const int nopt = __ldg(dm.blk_off + s + 1) - o0;
         for (int i = tid; i < nopt; i += NT) {
-            const int q = o0 + i;
-            int64_t need = (k == 0 && seeded) ? dm.fwd_req_pre[q] + dm.act_u[t + 1]
-                                              : dm.fwd_req[q] + seed;  // :141-143
-            int64_t th = need > dm.bwd_req[q] ? need : dm.bwd_req[q];   // :144
-            if (k > 0 && dm.pack_chg[q] > th) th = dm.pack_chg[q];      // :147
-            sm.thr[i] = clampm(th, M);
-            const int64_t p = dm.pack_chg[q];
-            sm.pc[i] = p > g.pad ? g.pad : (int)p;
-            sm.otot[i] = (V)dm.tftb[q];
+            sm.thr[i] = pr.thr[rid * c.ocap + i];
+            sm.pc[i] = pr.pc[o0 + i];
+            sm.otot[i] = pr.otot[o0 + i];
         }
-        const int32_t gate0 = clampm(dm.fwd0_own[s] + seed, M);      // :159
         if (k > 0) {
-            // pointers, then (sweep, gate) as a block-wide inclusive scan
+            const int64_t base = diag_cut_off(L, k) + (int64_t)s * k;
             for (int i = tid; i < k; i += NT) {
-                const int cc = s + 1 + i;
-                sm.lptr[i] = (long long)(opt + row_id(L, s, cc - 1) * g.sr + g.pad);
-                const int64_t a = dm.act_u[cc];
-                const int sh = a > g.pad ? g.pad : (int)a;
-                sm.rptr[i] = (long long)(opt + row_id(L, cc, t) * g.sr + g.pad - sh);
-            }
-            const int per = (k + NT - 1) / NT;
-            const int b0 = tid * per, b1 = min(k, b0 + per);
-            V acc = 0;
-            long long mx = LLONG_MIN;
-            for (int i = b0; i < b1; ++i) {
-                acc += (V)dm.tf0[s + i];                               // :162
-                if (i >= 1) {                                          // :164 (c-1 > s)
-                    const long long gv = dm.fwd0_full[s + i] + seed;
-                    mx = gv > mx ? gv : mx;
-                }
-            }
-            V inc_acc = acc;
-            long long inc_mx = mx;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const V y = __shfl_up_sync(0xffffffffu, inc_acc, off);
-                const long long ym = __shfl_up_sync(0xffffffffu, inc_mx, off);
-                if (lane >= off) {
-                    inc_acc += y;
-                    inc_mx = ym > inc_mx ? ym : inc_mx;
-                }
-            }
-            if (lane == 31) {
-                sm.wsum[warp] = inc_acc;
-                sm.wmax[warp] = inc_mx;
-            }
-            __syncthreads();
-            V ex = __shfl_up_sync(0xffffffffu, inc_acc, 1);
-            long long exm = __shfl_up_sync(0xffffffffu, inc_mx, 1);
-            if (lane == 0) {
-                ex = 0;
-                exm = LLONG_MIN;
-            }
-            for (int w = 0; w < warp; ++w) {
-                ex += sm.wsum[w];
-                exm = sm.wmax[w] > exm ? sm.wmax[w] : exm;
-            }
-            for (int i = b0; i < b1; ++i) {
-                ex += (V)dm.tf0[s + i];
-                if (i >= 1) {
-                    const long long gv = dm.fwd0_full[s + i] + seed;
-                    exm = gv > exm ? gv : exm;
-                }
-                sm.sweep[i] = ex;
-                const long long gg = exm > (long long)gate0 ? exm : (long long)gate0;
-                sm.gate[i] = clampm(gg, M);
+                sm.ptr[i] = pr.ptr[base + i];
+                sm.sweep[i] = pr.sweep[base + i];
+                sm.gate[i] = pr.gate[base + i];
             }
         }
 
-        // ---- wait for diagonal k-1 on tiles [j - dj, j] ----------------------
-        if (k > 0 && tid == 0) {
-            const int need = L - k + 1;
-            const int* row = done + (int64_t)(k - 1) * c.J;
-            for (int jj = (j - c.dj > 0 ? j - c.dj : 0); jj <= j; ++jj)
-                while (ld_acquire(row + jj) < need) __nanosleep(40);
-        }
-        __syncthreads();
+        // Only three candidate groups of cell (s, t) read diagonal k-1: the
+        // options (row (s+1, t)), cut c = s+1 (right operand (s+1, t)) and
+        // cut c = t (left operand (s, t-1)).  Cuts c in [s+2, t-1] read
+        // diagonals <= k-2, so they run first ("bulk", overlapping diagonal
+        // k-1) and only the short "tail" sits on the critical path.
+        auto wait_diag = [&](int kk) {
+            if (tid == 0) {
+                const int need = L - kk;
+                const int* row = done + (int64_t)kk * pl.J;
+                for (int jj = (j - pl.dj > 0 ? j - pl.dj : 0); jj <= j; ++jj)
+                    while (ld_relaxed(row + jj) < need) __nanosleep(20);
+                fence_acq_rel();
+            }
+        };
+        if (k >= 3) wait_diag(k - 2);
+        __syncthreads();  // program in smem (+ diagonal k-2 visible)
 
-        // ---- option window (row (s+1, t), slots [m0 - seg_cap, m0 + TM)) -----
-        const bool use_seg = k > 0 && c.seg_cap > 0;
-        const V* nxt = k > 0 ? opt + row_id(L, s + 1, t) * g.sr + g.pad : nullptr;
-        if (use_seg) {
-            const int n = c.seg_cap + c.TM;
-            for (int i = tid; i < n; i += NT) sm.seg[i] = __ldcg(nxt + (m0 - c.seg_cap + i));
-            __syncthreads();
-        }
-
-        // ---- lanes over budget slots mb + NT*jj -------------------------------
         const int mb = m0 + tid;
         V best[R];
         uint16_t code[R];
@@ -281,7 +295,107 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
         for (int r = 0; r < R; ++r) {
             best[r] = INF;
             code[r] = 0;
+            nlive[r] = 0;
         }
+        const uint16_t cb = (uint16_t)(kCutBit | (s + 1));
+        // ---- Case 2 bulk: cuts i in [1, k-2] ascending, strict '<' ------------
+        if (k > 0) {
+            int nmax = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {  // cuts admitted by the sweep gate and the `break`
+                const int m = mb + NT * r;
+                int lo = 0, hi = k;        // first i with gate[i] > m
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (sm.gate[mid] <= m)
+                        lo = mid + 1;
+                    else
+                        hi = mid;
+                }
+                nlive[r] = lo;
+                nmax = lo > nmax ? lo : nmax;
+            }
+            const int iend = nmax < k - 1 ? nmax : k - 1;  // exclusive; i = k-1 is tail
+            for (int i0 = 1; i0 < iend; i0 += U) {
+                V lv[U][R], rv[U][R];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u;
+                    const longlong2 p = sm.ptr[i < iend ? i : 0];
+                    const V* lp = reinterpret_cast<const V*>(p.x) + mb;
+                    const V* rp = reinterpret_cast<const V*>(p.y) + mb;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        if (i < iend && i < nlive[r]) {
+                            lv[u][r] = __ldcg(lp + NT * r);
+                            rv[u][r] = __ldcg(rp + NT * r);
+                        } else {
+                            lv[u][r] = INF;
+                            rv[u][r] = INF;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u;
+                    const V sw = sm.sweep[i < iend ? i : 0];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const V tot = sw + lv[u][r] + rv[u][r];
+                        bool ok = tot < best[r];
+                        if constexpr (CostP<V>::checked) ok = ok && lv[u][r] < INF && rv[u][r] < INF;
+                        if (ok) {
+                            best[r] = tot;
+                            code[r] = (uint16_t)(cb + i);
+                        }
+                    }
+                }
+            }
+        }
+
+        // ---- tail: wait for diagonal k-1 on tiles [j - dj, j] ------------------
+        if (k >= 1) wait_diag(k - 1);
+        __syncthreads();
+        unsigned long long t1 = 0;
+        if (pl.trace && tid == 0) t1 = gtimer();
+        const bool use_seg = k > 0 && c.seg_cap > 0;
+        const V* nxt = k > 0 ? opt + row_id(L, s + 1, t) * g.sr + g.pad : nullptr;
+        // tail cut operands: i = 0 (c = s+1) and i = k-1 (c = t); issue the
+        // loads together with the option-window staging
+        V tl[2][R], tr[2][R];
+        if (k > 0) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = e == 0 ? 0 : k - 1;
+                const longlong2 p = sm.ptr[i];
+                const V* lp = reinterpret_cast<const V*>(p.x) + mb;
+                const V* rp = reinterpret_cast<const V*>(p.y) + mb;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (i < nlive[r] && (e == 0 || k > 1)) {
+                        tl[e][r] = __ldcg(lp + NT * r);
+                        tr[e][r] = __ldcg(rp + NT * r);
+                    } else {
+                        tl[e][r] = INF;
+                        tr[e][r] = INF;
+                    }
+                }
+            }
+        }
+        if (use_seg) {
+            const int n = c.seg_cap + pl.TM;
+            for (int i = tid; i < n; i += NT) sm.seg[i] = __ldcg(nxt + (m0 - c.seg_cap + i));
+            __syncthreads();
+        }
+        // lexicographic (value, code) update: the reference's first minimum
+        // in candidate order (options by menu position, then cuts ascending)
+        auto offer = [&](int r, V tot, uint16_t cd, bool ok) {
+            ok = ok && (tot < best[r] || (tot == best[r] && cd < code[r]));
+            if (ok) {
+                best[r] = tot;
+                code[r] = cd;
+            }
+        };
         // Case 1 (chain_dp.hpp:139-156)
         for (int i = 0; i < nopt; ++i) {
             const V tt = sm.otot[i];
@@ -297,61 +411,28 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
                     if constexpr (CostP<V>::checked) ok = ok && sub < INF;
                     tot = tt + sub;
                 }
-                if (ok && tot < best[r]) {
-                    best[r] = tot;
-                    code[r] = (uint16_t)(i + 1);
-                }
+                if constexpr (!CostP<V>::checked) ok = ok && tot < INF;
+                offer(r, tot, (uint16_t)(i + 1), ok);
             }
         }
-        // Case 2 (chain_dp.hpp:158-174)
+        // Case 2 tail cuts (chain_dp.hpp:158-174)
         if (k > 0) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) {  // cuts admitted by the sweep gate / break
-                const int m = mb + NT * r;
-                int lo = 0, hi = k;  // first i with gate[i] > m
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (sm.gate[mid] <= m)
-                        lo = mid + 1;
-                    else
-                        hi = mid;
-                }
-                nlive[r] = lo;
-            }
-            int nmax = 0;
-#pragma unroll
-            for (int r = 0; r < R; ++r) nmax = nlive[r] > nmax ? nlive[r] : nmax;
-            const uint16_t cb = (uint16_t)(kCutBit | (s + 1));
-#pragma unroll 2
-            for (int i = 0; i < nmax; ++i) {
-                const V* lp = reinterpret_cast<const V*>(sm.lptr[i]) + mb;
-                const V* rp = reinterpret_cast<const V*>(sm.rptr[i]) + mb;
+            for (int e = 0; e < 2; ++e) {
+                const int i = e == 0 ? 0 : k - 1;
                 const V sw = sm.sweep[i];
-                V lv[R], rv[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    if (i < nlive[r]) {
-                        lv[r] = __ldcg(lp + NT * r);
-                        rv[r] = __ldcg(rp + NT * r);
-                    } else {
-                        lv[r] = INF;
-                        rv[r] = INF;
-                    }
-                }
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const V tot = sw + lv[r] + rv[r];
-                    bool ok = tot < best[r];
-                    if constexpr (CostP<V>::checked) ok = ok && lv[r] < INF && rv[r] < INF;
-                    if (ok) {
-                        best[r] = tot;
-                        code[r] = (uint16_t)(cb + i);
-                    }
+                    const V tot = sw + tl[e][r] + tr[e][r];
+                    bool ok = tot < INF;
+                    if constexpr (CostP<V>::checked) ok = tl[e][r] < INF && tr[e][r] < INF;
+                    offer(r, tot, (uint16_t)(cb + i), ok && (e == 0 || k > 1));
                 }
             }
         }
+        unsigned long long t2 = 0;
+        if (pl.trace && tid == 0) t2 = gtimer();
         // ---- store (chain_dp.hpp:176-177) and publish ---------------------------
-        const int64_t rid = row_id(L, s, t);
         V* orow = opt + rid * g.sr + g.pad;
         uint16_t* arow = arg + rid * g.sa;
 #pragma unroll
@@ -365,32 +446,44 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
         __syncthreads();
         if (tid == 0) {
             __threadfence();
-            atomicAdd(done + (int64_t)k * c.J + j, 1);
+            atomicAdd(done + (int64_t)k * pl.J + j, 1);
+            if (pl.trace) {
+                unsigned long long* tr = pl.trace + 4 * idx;
+                tr[0] = t0;
+                tr[1] = t1;
+                tr[2] = t2;
+                tr[3] = gtimer();
+            }
         }
     }
 }
 
+template <typename V>
+Programs<V> programs_of(const LaunchCtx& cx) {
+    Programs<V> p;
+    p.ptr = static_cast<longlong2*>(cx.prog.ptr);
+    p.sweep = static_cast<V*>(cx.prog.sweep);
+    p.gate = cx.prog.gate;
+    p.thr = cx.prog.thr;
+    p.pc = cx.prog.pc;
+    p.otot = static_cast<V*>(cx.prog.otot);
+    p.nq = cx.prog.nq;
+    return p;
+}
+
 template <typename V, int R>
 int launch_t(const LaunchCtx& cx) {
-    constexpr int NT = 256;
+    constexpr int NT = 256, U = 4;
     cudaStream_t st = static_cast<cudaStream_t>(cx.stream);
     const Geometry& g = cx.g;
-    PCfg c;
-    c.TM = NT * R;
-    c.J = (g.M + 1 + c.TM - 1) / c.TM;
-    c.dj = (g.pad + c.TM - 1) / c.TM;
-    c.seg_cap = (g.pad + c.TM <= 4096) ? g.pad : 0;
+    const PlanDev& pl = cx.plan;
+    Caps c;
+    c.TM = pl.TM;
+    c.seg_cap = pl.seg_cap;
     c.kcap = g.L > 1 ? g.L - 1 : 1;
     c.ocap = cx.max_opts > 0 ? cx.max_opts : 1;
-    // column group: keep rows x (GW*TM + pad) cost values near 48 MB of L2
-    const double budget = 48.0 * (1 << 20) / ((double)g.rows * sizeof(V));
-    int gw = (int)((budget - g.pad) / c.TM);
-    if (gw < 1) gw = 1;
-    if (gw > c.J) gw = c.J;
-    c.GW = gw;
-    c.total = (int64_t)c.J * g.rows;
-    const size_t smem = psmem_bytes<V>(c.kcap, c.ocap, c.seg_cap, c.TM);
-    auto kern = fill_persistent<V, NT, R>;
+    const size_t smem = psmem_bytes<V>(c);
+    auto kern = fill_persistent<V, NT, R, U>;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
@@ -403,35 +496,76 @@ int launch_t(const LaunchCtx& cx) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = (int64_t)per_sm * sms;
-    if (grid > c.total) grid = c.total;
-    const size_t flag_bytes = (size_t)g.L * c.J * sizeof(int);
-    if (cx.sched_bytes < flag_bytes + 8) return 3;
-    int* done = reinterpret_cast<int*>(static_cast<unsigned char*>(cx.sched) + 8);
-    unsigned long long* counter = static_cast<unsigned long long*>(cx.sched);
-    if (cudaMemsetAsync(cx.sched, 0, flag_bytes + 8, st) != cudaSuccess) return 3;
-    kern<<<(unsigned)grid, NT, smem, st>>>(g, cx.dm, static_cast<V*>(cx.opt), cx.arg, done, counter,
-                                           c);
+    if (grid > pl.total) grid = pl.total;
+    if (cudaMemsetAsync(pl.counter, 0, cx.state_bytes, st) != cudaSuccess) return 3;
+    kern<<<(unsigned)grid, NT, smem, st>>>(g, cx.dm, static_cast<V*>(cx.opt), cx.arg, pl,
+                                           programs_of<V>(cx), c);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+template <typename V>
+int prep_t(const LaunchCtx& cx) {
+    cudaStream_t st = static_cast<cudaStream_t>(cx.stream);
+    int64_t n = cx.g.rows > cx.prog.nq ? cx.g.rows : cx.prog.nq;
+    int blocks = (int)((n + 127) / 128);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    prep_programs<V><<<blocks, 128, 0, st>>>(cx.g, cx.dm, static_cast<const V*>(cx.opt),
+                                             programs_of<V>(cx), cx.max_opts > 0 ? cx.max_opts : 1);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 }  // namespace
 
-size_t persistent_sched_bytes(const Geometry& g) {
-    // worst case over the R choices (smallest tile): flags for L x J tiles + counter
-    const int TM = 256;
-    const int64_t J = (g.M + 1 + TM - 1) / TM;
-    return 8 + (size_t)g.L * J * sizeof(int);
+void persistent_plan(const Geometry& g, int width, PersistPlan& p) {
+    const int L = g.L;
+    const size_t vb = width == 32 ? 4 : 8;
+    p.R = (g.M + 1 >= 8192) ? 2 : 1;
+    if (const char* e = getenv("RKR_R")) p.R = atoi(e) == 2 ? 2 : 1;  // tuning knob
+    p.TM = 256 * p.R;
+    p.J = (g.M + 1 + p.TM - 1) / p.TM;
+    p.dj = (g.pad + p.TM - 1) / p.TM;
+    p.seg_cap = (g.pad + p.TM <= 4096) ? g.pad : 0;
+    // Order key lambda*j + k.  lambda = 1 is the 2D (tile, diagonal)
+    // wavefront: critical path L + J - 1 item steps, every tile in flight.
+    // lambda = 0 is diagonal-major (critical path L steps) and wins when the
+    // whole table fits in L2.  Larger lambda trades parallelism for L2
+    // locality (profiles/r01_persist: never paid off at this item latency).
+    const double table_bytes = (double)g.rows * g.sr * vb;
+    p.lambda = table_bytes <= 48.0 * (1 << 20) ? 0 : 1;
+    if (const char* e = getenv("RKR_LAMBDA")) p.lambda = atoi(e) >= 0 ? atoi(e) : 1;  // tuning knob
+    std::vector<std::pair<int64_t, int64_t>> order;  // (key, j * L + k)
+    order.reserve((size_t)p.J * L);
+    for (int64_t jj = 0; jj < p.J; ++jj)
+        for (int64_t k = 0; k < L; ++k) order.push_back({(int64_t)p.lambda * jj + k, jj * L + k});
+    std::sort(order.begin(), order.end());
+    p.start.clear();
+    p.g.clear();
+    p.k.clear();
+    int64_t cur = 0;
+    for (const auto& e : order) {
+        const int64_t jj = e.second / L, k = e.second % L;
+        p.start.push_back(cur);
+        p.g.push_back((int32_t)jj);
+        p.k.push_back((int32_t)k);
+        cur += L - k;
+    }
+    p.total = cur;
 }
 
-int persistent_r(const Geometry& g) {
-    if (g.M + 1 >= 8192) return 2;
-    return 1;
+size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p) {
+    return 8 + (size_t)g.L * p.J * sizeof(int);
+}
+
+int64_t program_cut_entries(const Geometry& g) { return diag_cut_off(g.L, g.L); }
+
+int launch_prep_programs(const LaunchCtx& c) {
+    return c.width == 32 ? prep_t<uint32_t>(c) : prep_t<int64_t>(c);
 }
 
 int launch_fill_persistent(const LaunchCtx& c) {
-    const int R = persistent_r(c.g);
-    if (c.width == 32) return R == 2 ? launch_t<uint32_t, 2>(c) : launch_t<uint32_t, 1>(c);
-    return R == 2 ? launch_t<int64_t, 2>(c) : launch_t<int64_t, 1>(c);
+    if (c.width == 32) return c.plan.R == 2 ? launch_t<uint32_t, 2>(c) : launch_t<uint32_t, 1>(c);
+    return c.plan.R == 2 ? launch_t<int64_t, 2>(c) : launch_t<int64_t, 1>(c);
 }
 
 }  // namespace rkr

@@ -106,6 +106,10 @@ def lib() -> ctypes.CDLL:
     L.rkr_table_h2d_bytes.restype = i64
     L.rkr_table_device_bytes.argtypes = [p]
     L.rkr_table_device_bytes.restype = i64
+    L.rkr_debug_trace.argtypes = [p, i32]
+    L.rkr_debug_trace_items.argtypes = [p]
+    L.rkr_debug_trace_items.restype = i64
+    L.rkr_debug_trace_read.argtypes = [p, p, p, p]
     L.rkr_backtrack_async.argtypes = [p, i32, i32, i32]
     L.rkr_backtrack_fetch.argtypes = [p, P(RkrOp), i64, P(i64)]
     _lib = L
@@ -255,6 +259,18 @@ class DpTable:
 
     def device_bytes(self) -> int:
         return self._lib.rkr_table_device_bytes(self._h)
+
+    def trace(self, enable: bool = True) -> None:
+        """Record per-item timestamps on the next fills (persistent kernel)."""
+        _check(self._lib.rkr_debug_trace(self._h, 1 if enable else 0))
+
+    def trace_read(self):
+        n = self._lib.rkr_debug_trace_items(self._h)
+        st = np.zeros((n, 4), np.uint64)
+        k = np.zeros(n, np.int32)
+        j = np.zeros(n, np.int32)
+        _check(self._lib.rkr_debug_trace_read(self._h, st.ctypes.data, k.ctypes.data, j.ctypes.data))
+        return st, k, j
 
     def backtrack_async(self, s: int, t: int, m: int) -> None:
         _check(self._lib.rkr_backtrack_async(self._h, s, t, m))

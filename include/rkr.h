@@ -187,9 +187,10 @@ int64_t rkr_table_h2d_bytes(const rkr_table* table);
 /* Device bytes the table holds (menu, scratch, opt and arg rows). */
 int64_t rkr_table_device_bytes(const rkr_table* table);
 
-/* Diagnostics (persistent kernel only): per-item globaltimer stamps
- * {dequeued, dependencies met, candidates done, published} of the next
- * fills; item_k/item_j (nullable) receive each item's diagonal and tile. */
+/* Diagnostics (persistent kernel only): 6 globaltimer stamps per item of the
+ * next fills {dequeued, diagonal k-2 met, bulk cuts done, diagonal k-1 met,
+ * tail done, published}; item_k/item_j (nullable) receive each item's
+ * diagonal and tile. */
 rkr_status rkr_debug_trace(rkr_table* table, int32_t enable);
 int64_t rkr_debug_trace_items(const rkr_table* table);
 rkr_status rkr_debug_trace_read(const rkr_table* table, uint64_t* stamps, int32_t* item_k,

@@ -730,9 +730,9 @@ rkr_status rkr_debug_trace(rkr_table* t, int32_t enable) {
     if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
     DeviceGuard dg(t->device);
     if (enable && !t->trace && t->kernel == RKR_KERNEL_PERSISTENT) {
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->trace), (size_t)t->plan.total * 32,
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->trace), (size_t)t->plan.total * 48,
                            t->stream));
-        CK(cudaMemsetAsync(t->trace, 0, (size_t)t->plan.total * 32, t->stream));
+        CK(cudaMemsetAsync(t->trace, 0, (size_t)t->plan.total * 48, t->stream));
     } else if (!enable && t->trace) {
         CK(cudaFreeAsync(t->trace, t->stream));
         t->trace = nullptr;
@@ -749,7 +749,7 @@ rkr_status rkr_debug_trace_read(const rkr_table* t, uint64_t* out, int32_t* item
     if (!t || !t->trace) return fail(RKR_ERR_ARGUMENT, "tracing not enabled");
     DeviceGuard dg(t->device);
     CK(cudaStreamSynchronize(t->stream));
-    CK(cudaMemcpy(out, t->trace, (size_t)t->plan.total * 32, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, t->trace, (size_t)t->plan.total * 48, cudaMemcpyDeviceToHost));
     // item -> (k, j) from the host copy of the plan
     const PersistPlan& p = t->plan;
     for (size_t e = 0; e < p.start.size(); ++e) {

@@ -275,17 +275,26 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
         // cut c = t (left operand (s, t-1)).  Cuts c in [s+2, t-1] read
         // diagonals <= k-2, so they run first ("bulk", overlapping diagonal
         // k-1) and only the short "tail" sits on the critical path.
+        // Thread 0 polls (relaxed) and fences once; the CTA barrier after it
+        // orders every thread's table reads after the acquire.  (Per-warp
+        // polling/publishing was measured 7x slower: 8x the pollers and
+        // atomics on the same flag lines, profiles/r01_persist.)
         auto wait_diag = [&](int kk) {
             if (tid == 0) {
                 const int need = L - kk;
                 const int* row = done + (int64_t)kk * pl.J;
                 for (int jj = (j - pl.dj > 0 ? j - pl.dj : 0); jj <= j; ++jj)
-                    while (ld_relaxed(row + jj) < need) __nanosleep(20);
+                    while (ld_relaxed(row + jj) < need) __nanosleep(32);
                 fence_acq_rel();
             }
+            __syncthreads();
         };
-        if (k >= 3) wait_diag(k - 2);
-        __syncthreads();  // program in smem (+ diagonal k-2 visible)
+        if (k >= 3)
+            wait_diag(k - 2);  // (its barrier also publishes the program in smem)
+        else
+            __syncthreads();
+        unsigned long long ta = 0;
+        if (pl.trace && tid == 0) ta = gtimer();
 
         const int mb = m0 + tid;
         V best[R];
@@ -354,11 +363,11 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
         }
 
         // ---- tail: wait for diagonal k-1 on tiles [j - dj, j] ------------------
+        unsigned long long tb = 0;
+        if (pl.trace && tid == 0) tb = gtimer();
         if (k >= 1) wait_diag(k - 1);
-        __syncthreads();
         unsigned long long t1 = 0;
         if (pl.trace && tid == 0) t1 = gtimer();
-        const bool use_seg = k > 0 && c.seg_cap > 0;
         const V* nxt = k > 0 ? opt + row_id(L, s + 1, t) * g.sr + g.pad : nullptr;
         // tail cut operands: i = 0 (c = s+1) and i = k-1 (c = t); issue the
         // loads together with the option-window staging
@@ -382,11 +391,6 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
                 }
             }
         }
-        if (use_seg) {
-            const int n = c.seg_cap + pl.TM;
-            for (int i = tid; i < n; i += NT) sm.seg[i] = __ldcg(nxt + (m0 - c.seg_cap + i));
-            __syncthreads();
-        }
         // lexicographic (value, code) update: the reference's first minimum
         // in candidate order (options by menu position, then cuts ascending)
         auto offer = [&](int r, V tot, uint16_t cd, bool ok) {
@@ -407,7 +411,9 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
                 V tot = tt;
                 bool ok = m >= th;
                 if (k > 0) {
-                    const V sub = use_seg ? sm.seg[m - m0 + c.seg_cap - p] : __ldcg(nxt + (m - p));
+                    // option window: L1-cached (the acquire fence above
+                    // invalidated L1, so every line is fetched after publish)
+                    const V sub = __ldca(nxt + (m - p));
                     if constexpr (CostP<V>::checked) ok = ok && sub < INF;
                     tot = tt + sub;
                 }
@@ -447,13 +453,15 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
         if (tid == 0) {
             __threadfence();
             atomicAdd(done + (int64_t)k * pl.J + j, 1);
-            if (pl.trace) {
-                unsigned long long* tr = pl.trace + 4 * idx;
-                tr[0] = t0;
-                tr[1] = t1;
-                tr[2] = t2;
-                tr[3] = gtimer();
-            }
+        }
+        if (pl.trace && tid == 0) {
+            unsigned long long* tr = pl.trace + 6 * idx;
+            tr[0] = t0;
+            tr[1] = ta;
+            tr[2] = tb;
+            tr[3] = t1;
+            tr[4] = t2;
+            tr[5] = gtimer();
         }
     }
 }
@@ -525,7 +533,7 @@ void persistent_plan(const Geometry& g, int width, PersistPlan& p) {
     p.TM = 256 * p.R;
     p.J = (g.M + 1 + p.TM - 1) / p.TM;
     p.dj = (g.pad + p.TM - 1) / p.TM;
-    p.seg_cap = (g.pad + p.TM <= 4096) ? g.pad : 0;
+    p.seg_cap = 0;  // option window read through L1 (ld.ca) after the acquire fence
     // Order key lambda*j + k.  lambda = 1 is the 2D (tile, diagonal)
     // wavefront: critical path L + J - 1 item steps, every tile in flight.
     // lambda = 0 is diagonal-major (critical path L steps) and wins when the

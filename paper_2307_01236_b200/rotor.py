@@ -266,7 +266,7 @@ class DpTable:
 
     def trace_read(self):
         n = self._lib.rkr_debug_trace_items(self._h)
-        st = np.zeros((n, 4), np.uint64)
+        st = np.zeros((n, 6), np.uint64)
         k = np.zeros(n, np.int32)
         j = np.zeros(n, np.int32)
         _check(self._lib.rkr_debug_trace_read(self._h, st.ctypes.data, k.ctypes.data, j.ctypes.data))

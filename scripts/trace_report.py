@@ -1,6 +1,7 @@
 """Per-item timing of the persistent fill (diagnostics for kernel tuning).
 
     python scripts/trace_report.py --config 3
+Stamps per item: dequeued, diag k-2 met, bulk done, diag k-1 met, tail done, published.
 """
 import argparse
 import os
@@ -24,18 +25,15 @@ for _ in range(3):
 t.sync()
 st, k, j = t.trace_read()
 st = st.astype(np.float64)
-t0 = st[:, 0].min()
-s = (st - t0) / 1e3  # us
-span = s[:, 3].max()
-wait = s[:, 1] - s[:, 0]
-comp = s[:, 2] - s[:, 1]
-pub = s[:, 3] - s[:, 2]
+s = (st - st[:, 0].min()) / 1e3  # us
+span = s[:, 5].max()
+d = np.diff(s, axis=1)  # wait2, bulk, wait1, tail, publish
+names = ["wait_k-2", "bulk", "wait_k-1", "tail", "publish"]
 print(f"config {a.config}: items {len(k)}, fill span {span:.1f} us")
-print(f"  per item us: wait {wait.mean():.2f} (p90 {np.percentile(wait, 90):.2f})  "
-      f"compute {comp.mean():.2f} (p90 {np.percentile(comp, 90):.2f})  publish {pub.mean():.2f}")
+print("  mean us: " + "  ".join(f"{n} {d[:, i].mean():.2f}" for i, n in enumerate(names)))
 L = c["L"]
 for kk in sorted(set(list(range(0, L, max(1, L // 12))) + [L - 1])):
     m = k == kk
-    print(f"  k={kk:4d} n={m.sum():6d} start {s[m, 0].min():9.1f} end {s[m, 3].max():9.1f} "
-          f"wait {wait[m].mean():7.2f} compute {comp[m].mean():7.2f} publish {pub[m].mean():6.2f}")
-# handoff latency: for each (k, j), first start of diag k+1 after last end of diag k
+    print(f"  k={kk:4d} n={m.sum():6d} start {s[m, 0].min():8.1f} k-1met {s[m, 3].min():8.1f}.."
+          f"{s[m, 3].max():8.1f} end {s[m, 5].max():8.1f} | " +
+          " ".join(f"{d[m, i].mean():6.2f}" for i in range(5)))

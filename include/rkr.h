@@ -187,6 +187,39 @@ int64_t rkr_table_h2d_bytes(const rkr_table* table);
 /* Device bytes the table holds (menu, scratch, opt and arg rows). */
 int64_t rkr_table_device_bytes(const rkr_table* table);
 
+/* ---- Batches: many independent tables, ONE persistent fill launch ---------
+ * (BASELINE config 4: budget sweeps x model instances.)  Table i is built
+ * exactly as rkr_table_create(menus[i], units[i], m_max[i], exec) would build
+ * it; all tables share one cost width (64 if any table needs it).
+ * rkr_batch_table returns a borrowed handle with the whole per-table API
+ * (opt/arg/row/download/backtrack/first_feasible); do not destroy it. */
+typedef struct rkr_batch rkr_batch;
+rkr_status rkr_batch_create(const rkr_menu* const* menus, const int64_t* units,
+                            const int32_t* m_max, int32_t n, const rkr_exec* exec,
+                            rkr_batch** out);
+int32_t rkr_batch_size(const rkr_batch* batch);
+rkr_table* rkr_batch_table(rkr_batch* batch, int32_t i);
+rkr_status rkr_batch_refill(rkr_batch* batch);
+void* rkr_batch_stream(const rkr_batch* batch);
+rkr_status rkr_batch_sync(const rkr_batch* batch);
+void rkr_batch_destroy(rkr_batch* batch);
+
+/* remat::solve_chain for n budgets of one chain (the per-budget loop of the
+ * reference's cmd_sweep, tools/remat.cpp:240-255), all tables in one batched
+ * fill; top cells, schedules and the min-feasible search of infeasible
+ * budgets are batched too.  Per budget i: status[i] is RKR_OK or
+ * RKR_ERR_INFEASIBLE (min_feasible[i] then holds the threshold in bytes, or
+ * -1); opt_time/unit/m_top as rkr_solve_chain.  Schedules are concatenated in
+ * ops; budget i's ops are [ops_offsets[i], ops_offsets[i+1]).  If ops_cap is
+ * too small, returns RKR_ERR_CAPACITY with ops_offsets[n] = ops needed (every
+ * other output is valid).  Budgets are processed in the given order; sorting,
+ * de-duplication and the monotonicity check (remat.cpp:232-263) are the
+ * caller's (see the host sweep helpers). */
+rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, int32_t units,
+                     const rkr_exec* exec, int32_t* status, int64_t* opt_time, int64_t* unit,
+                     int32_t* m_top, int64_t* min_feasible, rkr_op* ops, int64_t ops_cap,
+                     int64_t* ops_offsets);
+
 /* Diagnostics (persistent kernel only): 6 globaltimer stamps per item of the
  * next fills {dequeued, diagonal k-2 met, bulk cuts done, diagonal k-1 met,
  * tail done, published}; item_k/item_j (nullable) receive each item's

@@ -247,6 +247,8 @@ struct rkr_table {
     size_t state_bytes = 0;
     unsigned long long* trace = nullptr;
     int32_t bt_s = 0, bt_t = 0, bt_m = 0;
+    InstDesc hdesc{};             // this table as the persistent kernel sees it
+    InstDesc* ddesc = nullptr;    // device copy (single-table fills)
 
     LaunchCtx ctx() const {
         LaunchCtx c;
@@ -304,25 +306,76 @@ rkr_status alloc_and_upload(rkr_table* t) {
     take(np * 8);                              // 12 plan start
     take(np * 4);                              // 13 plan g
     take(np * 4);                              // 14 plan k
+    take(sizeof(InstDesc));                    // 15 kernel descriptor
     const size_t menu_bytes = bytes;
-    take(sizeof(int4) * (2 * L + 16));         // 15 backtrack stack
-    take(8 * sizeof(int64_t));                 // 16 dout
+    take(sizeof(int4) * (2 * L + 16));         // 16 backtrack stack
+    take(8 * sizeof(int64_t));                 // 17 dout
     const size_t vbytes = t->width == 32 ? 4 : 8;
-    take(((size_t)t->g.rows * t->g.sr + kOptSlack) * vbytes);  // 17 opt
-    take((size_t)t->g.rows * t->g.sa * 2);       // 18 arg
+    take(((size_t)t->g.rows * t->g.sr + kOptSlack) * vbytes);  // 18 opt
+    take((size_t)t->g.rows * t->g.sa * 2);       // 19 arg
     t->state_bytes = persistent_state_bytes(t->g, t->plan);
-    take(t->state_bytes);                        // 19 K1p counter + done flags
+    take(t->state_bytes);                        // 20 K1p counter + done flags
     const bool progs = t->kernel == RKR_KERNEL_PERSISTENT;
     const size_t nc = progs ? (size_t)program_cut_entries(t->g) : 0;
     const size_t ocap = std::max<int32_t>(h.max_opts, 1);
-    take(nc * 16);                               // 20 program ptr
-    take(nc * vbytes);                           // 21 program sweep
-    take(nc * 4);                                // 22 program gate
-    take(progs ? (size_t)t->g.rows * ocap * 4 : 0);  // 23 program thr
-    take(progs ? nq * 4 : 0);                    // 24 program pc
-    take(progs ? nq * vbytes : 0);               // 25 program otot
+    take(nc * 16);                               // 21 program ptr
+    take(nc * vbytes);                           // 22 program sweep
+    take(nc * 4);                                // 23 program gate
+    take(progs ? (size_t)t->g.rows * ocap * 4 : 0);  // 24 program thr
+    take(progs ? nq * 4 : 0);                    // 25 program pc
+    take(progs ? nq * vbytes : 0);               // 26 program otot
     t->menu_bytes = menu_bytes;
     t->block_bytes = bytes;
+
+    CK(cudaMallocAsync(&t->block, bytes, t->stream));
+    unsigned char* b = static_cast<unsigned char*>(t->block);
+    t->dm.blk_off = reinterpret_cast<const int32_t*>(b + off[0]);
+    t->dm.fwd_req = reinterpret_cast<const int64_t*>(b + off[1]);
+    t->dm.fwd_req_pre = reinterpret_cast<const int64_t*>(b + off[2]);
+    t->dm.bwd_req = reinterpret_cast<const int64_t*>(b + off[3]);
+    t->dm.pack_chg = reinterpret_cast<const int64_t*>(b + off[4]);
+    t->dm.tftb = reinterpret_cast<const int64_t*>(b + off[5]);
+    t->dm.chg_bt = reinterpret_cast<const int64_t*>(b + off[6]);
+    t->dm.ids = reinterpret_cast<const int32_t*>(b + off[7]);
+    t->dm.act_u = reinterpret_cast<const int64_t*>(b + off[8]);
+    t->dm.fwd0_own = reinterpret_cast<const int64_t*>(b + off[9]);
+    t->dm.fwd0_full = reinterpret_cast<const int64_t*>(b + off[10]);
+    t->dm.tf0 = reinterpret_cast<const int64_t*>(b + off[11]);
+    t->ddesc = reinterpret_cast<InstDesc*>(b + off[15]);
+    t->stack = reinterpret_cast<int4*>(b + off[16]);
+    t->dout = reinterpret_cast<int64_t*>(b + off[17]);
+    t->opt = b + off[18];
+    t->arg = reinterpret_cast<uint16_t*>(b + off[19]);
+    PlanDev& pd = t->pdev;
+    pd.R = t->plan.R;
+    pd.TM = t->plan.TM;
+    pd.J = t->plan.J;
+    pd.dj = t->plan.dj;
+    pd.seg_cap = t->plan.seg_cap;
+    pd.n_plan = (int32_t)np;
+    pd.total = t->plan.total;
+    pd.start = reinterpret_cast<const int64_t*>(b + off[12]);
+    pd.g = reinterpret_cast<const int32_t*>(b + off[13]);
+    pd.k = reinterpret_cast<const int32_t*>(b + off[14]);
+    pd.counter = reinterpret_cast<unsigned long long*>(b + off[20]);
+    pd.done = reinterpret_cast<int32_t*>(b + off[20] + 8);
+    pd.trace = nullptr;
+    t->prog.ptr = b + off[21];
+    t->prog.sweep = b + off[22];
+    t->prog.gate = reinterpret_cast<int32_t*>(b + off[23]);
+    t->prog.thr = reinterpret_cast<int32_t*>(b + off[24]);
+    t->prog.pc = reinterpret_cast<int32_t*>(b + off[25]);
+    t->prog.otot = b + off[26];
+    t->prog.nq = (int64_t)h.ids.size();
+    t->prog.ocap = (int32_t)ocap;
+    t->hdesc.g = t->g;
+    t->hdesc.dm = t->dm;
+    t->hdesc.opt = t->opt;
+    t->hdesc.arg = t->arg;
+    t->hdesc.plan = t->pdev;
+    t->hdesc.prog = t->prog;
+    t->hdesc.stack = t->stack;
+    t->hdesc.item_base = 0;
 
     void* stage = nullptr;
     CK(t_stage.get(menu_bytes, &stage));
@@ -346,59 +399,34 @@ rkr_status alloc_and_upload(rkr_table* t) {
     put(12, t->plan.start.data(), np * 8);
     put(13, t->plan.g.data(), np * 4);
     put(14, t->plan.k.data(), np * 4);
-    CK(cudaMallocAsync(&t->block, bytes, t->stream));
+    put(15, &t->hdesc, sizeof(InstDesc));
     CK(cudaMemcpyAsync(t->block, blob, menu_bytes, cudaMemcpyHostToDevice, t->stream));
     CK(cudaEventRecord(t_stage.done, t->stream));
-    unsigned char* b = static_cast<unsigned char*>(t->block);
-    t->dm.blk_off = reinterpret_cast<const int32_t*>(b + off[0]);
-    t->dm.fwd_req = reinterpret_cast<const int64_t*>(b + off[1]);
-    t->dm.fwd_req_pre = reinterpret_cast<const int64_t*>(b + off[2]);
-    t->dm.bwd_req = reinterpret_cast<const int64_t*>(b + off[3]);
-    t->dm.pack_chg = reinterpret_cast<const int64_t*>(b + off[4]);
-    t->dm.tftb = reinterpret_cast<const int64_t*>(b + off[5]);
-    t->dm.chg_bt = reinterpret_cast<const int64_t*>(b + off[6]);
-    t->dm.ids = reinterpret_cast<const int32_t*>(b + off[7]);
-    t->dm.act_u = reinterpret_cast<const int64_t*>(b + off[8]);
-    t->dm.fwd0_own = reinterpret_cast<const int64_t*>(b + off[9]);
-    t->dm.fwd0_full = reinterpret_cast<const int64_t*>(b + off[10]);
-    t->dm.tf0 = reinterpret_cast<const int64_t*>(b + off[11]);
-    t->stack = reinterpret_cast<int4*>(b + off[15]);
-    t->dout = reinterpret_cast<int64_t*>(b + off[16]);
-    t->opt = b + off[17];
-    t->arg = reinterpret_cast<uint16_t*>(b + off[18]);
-    PlanDev& pd = t->pdev;
-    pd.R = t->plan.R;
-    pd.TM = t->plan.TM;
-    pd.J = t->plan.J;
-    pd.dj = t->plan.dj;
-    pd.seg_cap = t->plan.seg_cap;
-    pd.n_plan = (int32_t)np;
-    pd.total = t->plan.total;
-    pd.start = reinterpret_cast<const int64_t*>(b + off[12]);
-    pd.g = reinterpret_cast<const int32_t*>(b + off[13]);
-    pd.k = reinterpret_cast<const int32_t*>(b + off[14]);
-    pd.counter = reinterpret_cast<unsigned long long*>(b + off[19]);
-    pd.done = reinterpret_cast<int32_t*>(b + off[19] + 8);
-    pd.trace = nullptr;
-    t->prog.ptr = b + off[20];
-    t->prog.sweep = b + off[21];
-    t->prog.gate = reinterpret_cast<int32_t*>(b + off[22]);
-    t->prog.thr = reinterpret_cast<int32_t*>(b + off[23]);
-    t->prog.pc = reinterpret_cast<int32_t*>(b + off[24]);
-    t->prog.otot = b + off[25];
-    t->prog.nq = (int64_t)h.ids.size();
     return RKR_OK;
 }
 
 rkr_status enqueue_fill(rkr_table* t) {
-    t->pdev.trace = t->trace;
-    LaunchCtx c = t->ctx();
-    if (launch_init_pads(c) || launch_fill_all(c)) return cuda_fail(cudaGetLastError(), "fill launch");
+    if (t->kernel != RKR_KERNEL_PERSISTENT) {
+        if (launch_init_pads(t->ctx())) return cuda_fail(cudaGetLastError(), "pad launch");
+        if (launch_fill_all(t->ctx())) return cuda_fail(cudaGetLastError(), "fill launch");
+        return RKR_OK;
+    }
+    CK(cudaMemsetAsync(t->pdev.counter, 0, t->state_bytes, t->stream));
+    if (launch_fill_batch(t->ddesc, 1, t->plan.total, t->width, t->plan.R,
+                          std::max(t->g.L - 1, 1), std::max(t->hm.max_opts, 1), t->pdev.counter,
+                          t->stream))
+        return cuda_fail(cudaGetLastError(), "fill launch");
     return RKR_OK;
 }
 
-rkr_status create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max, const rkr_exec* exec,
-                       rkr_table** out) {
+// Everything rkr_table_create does except the fill: validation and unit
+// precompute, geometry, plan, one pooled allocation + one H2D copy, pads,
+// cell programs.  R = 0 lets the plan choose the per-thread slot count.
+rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, const rkr_exec* exec,
+                         int R, rkr_table** out);
+
+rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, const rkr_exec* exec,
+                         int R, rkr_table** out) {
     if (!out) return fail(RKR_ERR_ARGUMENT, "null output handle");
     *out = nullptr;
     if (m_max < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
@@ -440,17 +468,31 @@ rkr_status create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max, const 
     t->g.sr = round_up((int64_t)t->g.pad + m_max + 1, 32);
     t->g.sa = round_up((int64_t)m_max + 1, 64);
     t->g.rows = (int64_t)h.L * (h.L + 1) / 2;
-    if (t->kernel == RKR_KERNEL_PERSISTENT) persistent_plan(t->g, t->width, t->plan);
+    if (t->kernel == RKR_KERNEL_PERSISTENT)
+        persistent_plan(t->g, t->width, R > 0 ? R : persistent_choose_r(m_max), t->plan);
     st = alloc_and_upload(t);
+    if (st == RKR_OK && launch_init_pads(t->ctx())) st = cuda_fail(cudaGetLastError(), "pad launch");
     if (st == RKR_OK && t->kernel == RKR_KERNEL_PERSISTENT && launch_prep_programs(t->ctx()))
         st = cuda_fail(cudaGetLastError(), "program launch");
-    if (st == RKR_OK) st = enqueue_fill(t);
     if (st != RKR_OK) {
         free_table(t);
         return st;
     }
     *out = t;
     return RKR_OK;
+}
+
+rkr_status create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max, const rkr_exec* exec,
+                       rkr_table** out) {
+    rkr_status st = prepare_table(menu, unit, m_max, exec, 0, out);
+    if (st != RKR_OK) return st;
+    DeviceGuard dg((*out)->device);
+    st = enqueue_fill(*out);
+    if (st != RKR_OK) {
+        free_table(*out);
+        *out = nullptr;
+    }
+    return st;
 }
 
 template <typename V>
@@ -737,6 +779,10 @@ rkr_status rkr_debug_trace(rkr_table* t, int32_t enable) {
         CK(cudaFreeAsync(t->trace, t->stream));
         t->trace = nullptr;
     }
+    t->pdev.trace = t->trace;
+    t->hdesc.plan.trace = t->trace;
+    CK(cudaMemcpyAsync(t->ddesc, &t->hdesc, sizeof(InstDesc), cudaMemcpyHostToDevice, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
     return RKR_OK;
 }
 
@@ -849,6 +895,330 @@ rkr_status rkr_solve_chain(const rkr_menu* menu, int64_t budget_bytes, int32_t u
     st = rkr_backtrack(t, 0, L - 1, (int32_t)m_top, ops, cap, n_ops);     // :293
     rkr_table_destroy(t);
     return st;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Batches: many independent tables, one persistent fill (config 4 sweeps).
+// ---------------------------------------------------------------------------
+struct rkr_batch {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int width = 32, R = 1, kcap = 1, ocap = 1;
+    std::vector<rkr_table*> tables;
+    void* block = nullptr;               // desc array | counter | flags of every table
+    InstDesc* ddesc = nullptr;
+    unsigned long long* counter = nullptr;
+    size_t state_bytes = 0;              // counter + flags
+    int64_t total = 0;
+};
+
+namespace {
+
+void free_batch(rkr_batch* b) {
+    if (!b) return;
+    DeviceGuard dg(b->device);
+    for (rkr_table* t : b->tables) free_table(t);
+    if (b->block) cudaFreeAsync(b->block, b->stream);
+    delete b;
+}
+
+rkr_status batch_fill(rkr_batch* b) {
+    CK(cudaMemsetAsync(b->counter, 0, b->state_bytes, b->stream));
+    if (launch_fill_batch(b->ddesc, (int)b->tables.size(), b->total, b->width, b->R, b->kcap,
+                          b->ocap, b->counter, b->stream))
+        return cuda_fail(cudaGetLastError(), "batch fill launch");
+    return RKR_OK;
+}
+
+rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
+                             const int32_t* m_max, int32_t n, const rkr_exec* exec,
+                             rkr_batch** out) {
+    if (!out || !menus || !units || !m_max) return fail(RKR_ERR_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (n < 1) return fail(RKR_ERR_ARGUMENT, "empty batch");
+    // common cost width: 32 only if every table's overflow proof holds
+    bool all32 = !(exec && exec->width == RKR_WIDTH_64);
+    int32_t min_m = INT32_MAX;
+    for (int32_t i = 0; i < n; ++i) {
+        HostMenu h;
+        rkr_status st = build_host_menu(menus[i], units[i], h);
+        if (st != RKR_OK) return st;
+        if (m_max[i] < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
+        all32 = all32 && h.bounded32;
+        min_m = std::min(min_m, m_max[i]);
+    }
+    rkr_exec ex{};
+    if (exec) ex = *exec;
+    ex.width = all32 ? RKR_WIDTH_AUTO : RKR_WIDTH_64;
+    ex.kernel = RKR_KERNEL_PERSISTENT;
+    rkr_batch* b = new rkr_batch();
+    b->device = ex.device;
+    b->R = persistent_choose_r(min_m);
+    DeviceGuard dg(b->device);
+    for (int32_t i = 0; i < n; ++i) {
+        rkr_table* t = nullptr;
+        rkr_status st = prepare_table(menus[i], units[i], m_max[i], &ex, b->R, &t);
+        if (st != RKR_OK) {
+            free_batch(b);
+            return st;
+        }
+        b->tables.push_back(t);
+    }
+    b->stream = b->tables[0]->stream;
+    b->width = b->tables[0]->width;
+    size_t flags = 0;
+    for (rkr_table* t : b->tables) {
+        b->kcap = std::max(b->kcap, t->g.L - 1);
+        b->ocap = std::max(b->ocap, t->hm.max_opts);
+        flags += (size_t)t->g.L * t->plan.J;
+    }
+    const size_t desc_bytes = (size_t)round_up((int64_t)(sizeof(InstDesc) * n), 256);
+    b->state_bytes = 8 + flags * sizeof(int);
+    CK(cudaMallocAsync(&b->block, desc_bytes + b->state_bytes, b->stream));
+    unsigned char* base = static_cast<unsigned char*>(b->block);
+    b->ddesc = reinterpret_cast<InstDesc*>(base);
+    b->counter = reinterpret_cast<unsigned long long*>(base + desc_bytes);
+    int32_t* flag = reinterpret_cast<int32_t*>(base + desc_bytes + 8);
+    std::vector<InstDesc> hd(n);
+    int64_t item = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        rkr_table* t = b->tables[i];
+        hd[i] = t->hdesc;
+        hd[i].plan.done = flag;
+        hd[i].plan.trace = nullptr;
+        hd[i].item_base = item;
+        flag += (size_t)t->g.L * t->plan.J;
+        item += t->plan.total;
+    }
+    b->total = item;
+    void* stage = nullptr;
+    CK(t_stage.get(sizeof(InstDesc) * n, &stage));
+    std::memcpy(stage, hd.data(), sizeof(InstDesc) * n);
+    CK(cudaMemcpyAsync(b->ddesc, stage, sizeof(InstDesc) * n, cudaMemcpyHostToDevice, b->stream));
+    CK(cudaEventRecord(t_stage.done, b->stream));
+    rkr_status st = batch_fill(b);
+    if (st != RKR_OK) {
+        free_batch(b);
+        return st;
+    }
+    *out = b;
+    return RKR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rkr_status rkr_batch_create(const rkr_menu* const* menus, const int64_t* units,
+                            const int32_t* m_max, int32_t n, const rkr_exec* exec,
+                            rkr_batch** out) {
+    return batch_create_impl(menus, units, m_max, n, exec, out);
+}
+
+int32_t rkr_batch_size(const rkr_batch* b) { return b ? (int32_t)b->tables.size() : 0; }
+
+rkr_table* rkr_batch_table(rkr_batch* b, int32_t i) {
+    if (!b || i < 0 || i >= (int32_t)b->tables.size()) return nullptr;
+    return b->tables[i];
+}
+
+rkr_status rkr_batch_refill(rkr_batch* b) {
+    if (!b) return fail(RKR_ERR_ARGUMENT, "null batch");
+    DeviceGuard dg(b->device);
+    return batch_fill(b);
+}
+
+void* rkr_batch_stream(const rkr_batch* b) { return b ? (void*)b->stream : nullptr; }
+
+rkr_status rkr_batch_sync(const rkr_batch* b) {
+    if (!b) return fail(RKR_ERR_ARGUMENT, "null batch");
+    DeviceGuard dg(b->device);
+    CK(cudaStreamSynchronize(b->stream));
+    return RKR_OK;
+}
+
+void rkr_batch_destroy(rkr_batch* b) { free_batch(b); }
+
+// remat::solve_chain for many budgets of one chain (cmd_sweep's loop,
+// remat.cpp:240-255) with every table in one batched fill, the top cells
+// gathered in one launch, the schedules walked in one launch (a thread per
+// budget) and the infeasible budgets' min-feasible search batched the same way.
+rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, int32_t units,
+                     const rkr_exec* exec, int32_t* status, int64_t* opt_time, int64_t* unit_out,
+                     int32_t* m_top_out, int64_t* min_feasible, rkr_op* ops, int64_t ops_cap,
+                     int64_t* ops_offsets) {
+    if (!menu || !budgets || !status || !opt_time || !unit_out || !m_top_out || !min_feasible ||
+        !ops_offsets)
+        return fail(RKR_ERR_ARGUMENT, "null argument");
+    if (n < 1) return fail(RKR_ERR_ARGUMENT, "empty sweep");
+    if (menu->n_blocks <= 0 || !menu->act_sizes) return fail(RKR_ERR_INVALID, "empty option menu");
+    const int L = menu->n_blocks;
+    std::vector<int64_t> unit(n), a0u(n);
+    std::vector<int32_t> mtop(n, -1);
+    std::vector<int32_t> idx;  // budgets with a table
+    for (int32_t i = 0; i < n; ++i) {
+        int64_t bu;
+        rkr_status st = rkr_quantize(budgets[i], units, &unit[i], &bu);       // :257
+        if (st) return st;
+        a0u[i] = to_units(menu->act_sizes[0], unit[i]);                        // :258
+        const int64_t mt = bu - a0u[i];                                        // :259
+        status[i] = RKR_ERR_INFEASIBLE;
+        opt_time[i] = 0;
+        unit_out[i] = unit[i];
+        m_top_out[i] = 0;
+        min_feasible[i] = -1;
+        if (mt < 0) continue;                                                  // :260-261
+        if (mt > 0x7ffffffe) return fail(RKR_ERR_INVALID, "budget slots exceed int range");
+        mtop[i] = (int32_t)mt;
+        idx.push_back(i);
+    }
+    const int nb = (int)idx.size();
+    std::vector<int64_t> top(nb, kInf64);
+    std::vector<int64_t> walk_out(4 * (size_t)nb, 0);
+    int64_t cap_each = 0;
+    std::vector<int32_t> walk_ops;
+    std::vector<std::vector<rkr_op>> big(nb);  // schedules that overflowed the batch slots
+    if (nb > 0) {
+        std::vector<const rkr_menu*> ms(nb, menu);
+        std::vector<int64_t> us(nb);
+        std::vector<int32_t> mm(nb);
+        for (int q = 0; q < nb; ++q) {
+            us[q] = unit[idx[q]];
+            mm[q] = mtop[idx[q]];
+        }
+        rkr_batch* b = nullptr;
+        rkr_status st = rkr_batch_create(ms.data(), us.data(), mm.data(), nb, exec, &b);
+        if (st) return st;
+        DeviceGuard dg(b->device);
+        // scratch: m_at[nb] | active[nb] | tops[nb] | walk out[4 nb] | ops[nb * cap]
+        cap_each = std::max<int64_t>(256, 16 * (int64_t)L);
+        const size_t bytes = (size_t)nb * (4 + 1 + 8 + 32) + 64 + (size_t)nb * cap_each * 12;
+        void* scr = nullptr;
+        cudaError_t e = cudaMallocAsync(&scr, bytes, b->stream);
+        if (e != cudaSuccess) {
+            rkr_batch_destroy(b);
+            return cuda_fail(e, "sweep scratch");
+        }
+        unsigned char* p = static_cast<unsigned char*>(scr);
+        int64_t* d_tops = reinterpret_cast<int64_t*>(p);
+        int64_t* d_wout = d_tops + nb;
+        int32_t* d_ops = reinterpret_cast<int32_t*>(d_wout + 4 * (size_t)nb);
+        int32_t* d_mat = d_ops + (size_t)nb * cap_each * 3;
+        uint8_t* d_act = reinterpret_cast<uint8_t*>(d_mat + nb);
+        std::vector<uint8_t> act(nb, 1);
+        auto run = [&]() -> rkr_status {
+            CK(cudaMemcpyAsync(d_mat, mm.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, b->stream));
+            if (launch_batch_tops(b->ddesc, d_mat, nb, b->width, d_tops, b->stream))
+                return cuda_fail(cudaGetLastError(), "tops launch");
+            CK(cudaMemcpyAsync(top.data(), d_tops, 8 * (size_t)nb, cudaMemcpyDeviceToHost, b->stream));
+            CK(cudaStreamSynchronize(b->stream));
+            for (int q = 0; q < nb; ++q) act[q] = top[q] < kInf64 ? 1 : 0;   // :264-265
+            CK(cudaMemcpyAsync(d_act, act.data(), nb, cudaMemcpyHostToDevice, b->stream));
+            if (launch_batch_walk(b->ddesc, d_mat, d_act, nb, b->width, d_ops, cap_each, d_wout,
+                                  b->stream))
+                return cuda_fail(cudaGetLastError(), "walk launch");
+            CK(cudaMemcpyAsync(walk_out.data(), d_wout, 32 * (size_t)nb, cudaMemcpyDeviceToHost,
+                               b->stream));
+            walk_ops.resize((size_t)nb * cap_each * 3);
+            CK(cudaMemcpyAsync(walk_ops.data(), d_ops, walk_ops.size() * 4, cudaMemcpyDeviceToHost,
+                               b->stream));
+            CK(cudaStreamSynchronize(b->stream));
+            return RKR_OK;
+        };
+        st = run();
+        cudaFreeAsync(scr, b->stream);
+        // schedules longer than cap_each: walk those tables again on their own
+        for (int q = 0; q < nb && st == RKR_OK; ++q) {
+            if (!act[q] || walk_out[4 * q] <= cap_each) continue;
+            big[q].resize((size_t)walk_out[4 * q]);
+            int64_t nn = 0;
+            st = rkr_backtrack(b->tables[q], 0, L - 1, mm[q], big[q].data(),
+                               (int64_t)big[q].size(), &nn);
+        }
+        rkr_batch_destroy(b);
+        if (st) return st;
+    }
+    // infeasible budgets with a table: the wide-table min-feasible search (:265-288)
+    std::vector<int> inf_q;
+    for (int q = 0; q < nb; ++q)
+        if (top[q] >= kInf64) inf_q.push_back(q);
+    if (!inf_q.empty()) {
+        const int ni = (int)inf_q.size();
+        std::vector<const rkr_menu*> ms(ni, menu);
+        std::vector<int64_t> us(ni);
+        std::vector<int32_t> caps(ni);
+        for (int r = 0; r < ni; ++r) {
+            const int i = idx[inf_q[r]];
+            const int64_t u = unit[i];
+            int64_t capu = 0;
+            for (int bl = 0; bl < L; ++bl) {
+                int64_t worst = 0;
+                for (int o = menu->option_offsets[bl]; o < menu->option_offsets[bl + 1]; ++o)
+                    worst = std::max({worst, to_units(menu->peak_fwd[o], u),
+                                      to_units(menu->peak_bwd[o], u), to_units(menu->save_mem[o], u)});
+                capu += worst;
+            }
+            for (int bl = 0; bl <= L; ++bl) capu += 2 * to_units(menu->act_sizes[bl], u);
+            if (capu > 0x7ffffffe) return fail(RKR_ERR_INVALID, "feasibility cap exceeds int range");
+            us[r] = u;
+            caps[r] = (int32_t)capu;
+        }
+        rkr_batch* w = nullptr;
+        rkr_status st = rkr_batch_create(ms.data(), us.data(), caps.data(), ni, exec, &w);
+        if (st) return st;
+        DeviceGuard dg(w->device);
+        int32_t* d_ff = nullptr;
+        std::vector<int32_t> ff(ni, -1);
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_ff), 4 * (size_t)ni, w->stream);
+        if (e == cudaSuccess && launch_batch_first_feasible(w->ddesc, ni, w->width, d_ff, w->stream))
+            e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(ff.data(), d_ff, 4 * (size_t)ni, cudaMemcpyDeviceToHost, w->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(w->stream);
+        if (d_ff) cudaFreeAsync(d_ff, w->stream);
+        rkr_batch_destroy(w);
+        if (e != cudaSuccess) return cuda_fail(e, "min-feasible search");
+        for (int r = 0; r < ni; ++r) {
+            const int i = idx[inf_q[r]];
+            if (ff[r] >= 0) min_feasible[i] = (ff[r] + a0u[i]) * unit[i];       // :282
+        }
+    }
+    // results and schedules, in budget order
+    int64_t off = 0;
+    ops_offsets[0] = 0;
+    std::vector<int> qof(n, -1);
+    for (int q = 0; q < nb; ++q) qof[idx[q]] = q;
+    rkr_status result = RKR_OK;
+    for (int32_t i = 0; i < n; ++i) {
+        const int q = qof[i];
+        int64_t cnt = 0;
+        if (q >= 0 && top[q] < kInf64) {
+            status[i] = RKR_OK;
+            opt_time[i] = top[q];
+            m_top_out[i] = mtop[i];
+            cnt = walk_out[4 * q];
+            if (walk_out[4 * q + 1] != 0) {
+                result = fail(RKR_ERR_INFEASIBLE, "schedule walk failed for budget %d", i);
+                cnt = 0;
+            }
+            for (int64_t o = 0; o < cnt; ++o)
+                if (ops && off + o < ops_cap) {
+                    if (!big[q].empty()) {
+                        ops[off + o] = big[q][o];
+                    } else {
+                        const int32_t* src = &walk_ops[3 * ((size_t)q * cap_each + o)];
+                        ops[off + o] = rkr_op{src[0], src[1], src[2]};
+                    }
+                }
+        }
+        off += cnt;
+        ops_offsets[i + 1] = off;
+    }
+    if (result == RKR_OK && off > ops_cap)
+        return fail(RKR_ERR_CAPACITY, "sweep schedules need %lld ops", (long long)off);
+    return result;
 }
 
 }  // extern "C"

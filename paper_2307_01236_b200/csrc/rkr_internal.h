@@ -75,8 +75,8 @@ struct PlanDev {
     const int32_t* g;
     const int32_t* k;
     int32_t* done;                   // [L * J] rows completed per (diagonal, tile)
-    unsigned long long* counter;     // next item
-    unsigned long long* trace;       // optional: 4 globaltimer stamps per item (nullptr = off)
+    unsigned long long* counter;     // unused (the launch owns the item counter)
+    unsigned long long* trace;       // optional: 6 globaltimer stamps per item (nullptr = off)
 };
 // Per-table cell programs (K1p), filled by launch_prep_programs.
 struct ProgDev {
@@ -87,9 +87,34 @@ struct ProgDev {
     int32_t* pc;      // [saved options]
     void* otot;       // V [saved options]
     int64_t nq;
+    int32_t ocap;     // row stride of thr (the table's max saved options, >= 1)
 };
 int64_t program_cut_entries(const Geometry& g);
-void persistent_plan(const Geometry& g, int width, PersistPlan& p);
+
+// One table of a (possibly batched) persistent fill, as the kernel sees it.
+// Items of instance i are global items [item_base, item_base + plan.total).
+struct InstDesc {
+    Geometry g;
+    DevMenu dm;
+    void* opt;
+    uint16_t* arg;
+    PlanDev plan;
+    ProgDev prog;
+    void* stack;        // backtrack stack (int4[2L + 16])
+    int64_t item_base;
+};
+int launch_batch_walk(const InstDesc* d, const int32_t* m_at, const uint8_t* active, int n,
+                      int width, int32_t* ops, int64_t cap, int64_t* out, void* stream);
+int launch_batch_tops(const InstDesc* d, const int32_t* m_at, int n, int width, int64_t* out,
+                      void* stream);
+int launch_batch_first_feasible(const InstDesc* d, int n, int width, int32_t* out, void* stream);
+// Fill n tables with ONE persistent launch.  All tables share the cost
+// width and the plan's R.  The counter and every table's done flags must be
+// zeroed on `stream` before the call (they are, by the callers in rkr_capi).
+int launch_fill_batch(const InstDesc* dev_desc, int n, int64_t total_items, int width, int R,
+                      int kcap, int ocap, unsigned long long* counter, void* stream);
+void persistent_plan(const Geometry& g, int width, int R, PersistPlan& p);
+int persistent_choose_r(int32_t M);
 size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p);  // counter + flags
 
 // Launch entry points (rkr_kernels.cu).
@@ -107,7 +132,6 @@ struct LaunchCtx {
     size_t state_bytes; // bytes of counter + flags to zero before each fill
 };
 
-int launch_fill_persistent(const LaunchCtx& c);
 int launch_prep_programs(const LaunchCtx& c);
 constexpr int64_t kOptSlack = 4096;  // elements past the last row (tile over-reads)
 

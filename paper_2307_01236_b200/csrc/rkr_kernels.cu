@@ -215,14 +215,14 @@ __global__ void init_pads(Geometry g, V* opt) {
     }
 }
 
-// K2: build_schedule_rec on one thread.  Stack entries are int4
-// {type, s, t, m}: type 0 = cell to expand, type 1 = pending BlockBwd(s, t=option).
+// K2: build_schedule_rec as an explicit stack walk on one thread.  Stack
+// entries are int4 {type, s, t, m}: type 0 = cell to expand, type 1 =
+// pending BlockBwd(s, t = option).  Returns {n_ops, status, bad_s, bad_t}.
 template <typename V>
-__global__ void backtrack(Geometry g, DevMenu dm, const V* __restrict__ opt,
-                          const uint16_t* __restrict__ arg, int s0, int t0, int m0,
-                          int32_t* __restrict__ ops, int64_t cap, int4* __restrict__ stack,
-                          int64_t* __restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void walk(const Geometry& g, const DevMenu& dm, const V* __restrict__ opt,
+                     const uint16_t* __restrict__ arg, int s0, int t0, int m0,
+                     int32_t* __restrict__ ops, int64_t cap, int4* __restrict__ stack,
+                     int64_t* __restrict__ out) {
     const int L = g.L, M = g.M;
     int64_t n = 0;
     int sp = 0;
@@ -284,6 +284,69 @@ __global__ void backtrack(Geometry g, DevMenu dm, const V* __restrict__ opt,
     out[1] = status;
     out[2] = bad_s;
     out[3] = bad_t;
+}
+
+template <typename V>
+__global__ void backtrack(Geometry g, DevMenu dm, const V* __restrict__ opt,
+                          const uint16_t* __restrict__ arg, int s0, int t0, int m0,
+                          int32_t* __restrict__ ops, int64_t cap, int4* __restrict__ stack,
+                          int64_t* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    walk<V>(g, dm, opt, arg, s0, t0, m0, ops, cap, stack, out);
+}
+
+// Batched K2: thread i walks table i from (0, L-1, m_at[i]) when active[i];
+// ops of table i go to ops + 3 * cap * i (at most cap of them).
+template <typename V>
+__global__ void batch_walk(const InstDesc* __restrict__ d, const int32_t* __restrict__ m_at,
+                           const uint8_t* __restrict__ active, int n, int32_t* __restrict__ ops,
+                           int64_t cap, int64_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (!active[i]) {
+        out[4 * i] = 0;
+        out[4 * i + 1] = -1;
+        return;
+    }
+    const InstDesc& D = d[i];
+    walk<V>(D.g, D.dm, static_cast<const V*>(D.opt), D.arg, 0, D.g.L - 1, m_at[i],
+            ops + 3 * cap * (int64_t)i, cap, static_cast<int4*>(D.stack), out + 4 * i);
+}
+
+// Batched top cells: out[i] = opt(0, L-1, min(m_at[i], M)) as int64 (kInf64 when infinite).
+template <typename V>
+__global__ void batch_tops(const InstDesc* __restrict__ d, const int32_t* __restrict__ m_at, int n,
+                           int64_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const InstDesc& D = d[i];
+    int m = m_at[i];
+    if (m < 0) {
+        out[i] = kInf64;
+        return;
+    }
+    if (m > D.g.M) m = D.g.M;
+    const V v = static_cast<const V*>(D.opt)[row_id(D.g.L, 0, D.g.L - 1) * D.g.sr + D.g.pad + m];
+    out[i] = v >= Cost<V>::inf ? kInf64 : (int64_t)v;
+}
+
+// Batched K3: block i finds the first finite m of table i's top row.
+template <typename V>
+__global__ void batch_first_feasible(const InstDesc* __restrict__ d, int n, int32_t* __restrict__ out) {
+    const int i = blockIdx.x;
+    if (i >= n) return;
+    __shared__ int best;
+    if (threadIdx.x == 0) best = 0x7fffffff;
+    __syncthreads();
+    const InstDesc& D = d[i];
+    const V* row = static_cast<const V*>(D.opt) + row_id(D.g.L, 0, D.g.L - 1) * D.g.sr + D.g.pad;
+    for (int m = threadIdx.x; m <= D.g.M; m += blockDim.x)
+        if (row[m] < Cost<V>::inf) {
+            atomicMin(&best, m);
+            break;
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) out[i] = best == 0x7fffffff ? -1 : best;
 }
 
 // K3: first m with opt(s,t,m) < inf.
@@ -368,7 +431,6 @@ int launch_init_pads(const LaunchCtx& c) {
 }
 
 int launch_fill_all(const LaunchCtx& c) {
-    if (c.kernel == 0) return launch_fill_persistent(c);
     return c.width == 32 ? fill_all_t<uint32_t>(c) : fill_all_t<int64_t>(c);
 }
 
@@ -382,6 +444,37 @@ int launch_backtrack(const LaunchCtx& c, int32_t s, int32_t t, int32_t m, int32_
     else
         backtrack<int64_t><<<1, 32, 0, st>>>(c.g, c.dm, static_cast<const int64_t*>(c.opt),
                                              c.arg, s, t, m, dev_ops, cap, stk, dev_out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int launch_batch_walk(const InstDesc* d, const int32_t* m_at, const uint8_t* active, int n,
+                      int width, int32_t* ops, int64_t cap, int64_t* out, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int blocks = (n + 31) / 32;
+    if (width == 32)
+        batch_walk<uint32_t><<<blocks, 32, 0, st>>>(d, m_at, active, n, ops, cap, out);
+    else
+        batch_walk<int64_t><<<blocks, 32, 0, st>>>(d, m_at, active, n, ops, cap, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int launch_batch_tops(const InstDesc* d, const int32_t* m_at, int n, int width, int64_t* out,
+                      void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int blocks = (n + 127) / 128;
+    if (width == 32)
+        batch_tops<uint32_t><<<blocks, 128, 0, st>>>(d, m_at, n, out);
+    else
+        batch_tops<int64_t><<<blocks, 128, 0, st>>>(d, m_at, n, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int launch_batch_first_feasible(const InstDesc* d, int n, int width, int32_t* out, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (width == 32)
+        batch_first_feasible<uint32_t><<<n, 256, 0, st>>>(d, n, out);
+    else
+        batch_first_feasible<int64_t><<<n, 256, 0, st>>>(d, n, out);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

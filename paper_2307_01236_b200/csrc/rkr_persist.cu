@@ -80,6 +80,7 @@ struct Programs {
     int32_t* pc;      // per saved option: pack shift clamped to pad
     V* otot;          // per saved option: time_fwd + time_bwd
     int64_t nq;
+    int32_t ocap;     // thr row stride
 };
 
 // first cut-program entry of diagonal k: sum_{k' < k} (L - k') k'
@@ -91,7 +92,8 @@ __host__ __device__ inline int64_t diag_cut_off(int64_t L, int64_t k) {
 // prep_programs: one thread per cell (s, t).
 // ---------------------------------------------------------------------------
 template <typename V>
-__global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> pr, int ocap) {
+__global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> pr) {
+    const int ocap = pr.ocap;
     const int L = g.L, M = g.M;
     for (int64_t rid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; rid < g.rows;
          rid += (int64_t)gridDim.x * blockDim.x) {
@@ -224,28 +226,60 @@ __device__ inline void decode_item(int64_t idx, const PlanDev& p, int& k, int& j
     s = (int)(idx - __ldg(p.start + lo));
 }
 
+template <typename V>
+__device__ inline Programs<V> programs_of(const ProgDev& q) {
+    Programs<V> p;
+    p.ptr = static_cast<longlong2*>(q.ptr);
+    p.sweep = static_cast<V*>(q.sweep);
+    p.gate = q.gate;
+    p.thr = q.thr;
+    p.pc = q.pc;
+    p.otot = static_cast<V*>(q.otot);
+    p.nq = q.nq;
+    p.ocap = q.ocap;
+    return p;
+}
+
 template <typename V, int NT, int R, int U>
-__global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V* __restrict__ opt,
-                                                      uint16_t* __restrict__ arg, PlanDev pl,
-                                                      Programs<V> pr, Caps c) {
+__global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict__ inst, int n_inst,
+                                                      int64_t total,
+                                                      unsigned long long* __restrict__ counter,
+                                                      Caps c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr V INF = CostP<V>::inf;
     PSmem<V> sm = pcarve<V>(smem_raw, c);
-    const int L = g.L, M = g.M;
     const int tid = threadIdx.x;
-    int* __restrict__ done = pl.done;
     long long next = 0;
-    if (tid == 0) next = (long long)atomicAdd(pl.counter, 1ull);
+    if (tid == 0) next = (long long)atomicAdd(counter, 1ull);
 
     for (;;) {
         if (tid == 0) sm.item[0] = next;
         __syncthreads();
-        const int64_t idx = sm.item[0];
-        if (idx >= pl.total) break;
+        const int64_t gidx = sm.item[0];
+        if (gidx >= total) break;
         // prefetch the next item while this one runs (the earliest unfinished
         // item is always one being processed, so this cannot deadlock)
-        if (tid == 0) next = (long long)atomicAdd(pl.counter, 1ull);
+        if (tid == 0) next = (long long)atomicAdd(counter, 1ull);
         unsigned long long t0 = 0;
+        // instance of this item (tables are laid out back to back in item space)
+        int ia = 0, ib = n_inst - 1;
+        while (ia < ib) {
+            const int mid = (ia + ib + 1) >> 1;
+            if (__ldg(&inst[mid].item_base) <= gidx)
+                ia = mid;
+            else
+                ib = mid - 1;
+        }
+        const InstDesc& D = inst[ia];
+        const Geometry g = D.g;
+        const DevMenu dm = D.dm;
+        const PlanDev pl = D.plan;
+        const Programs<V> pr = programs_of<V>(D.prog);
+        V* __restrict__ opt = static_cast<V*>(D.opt);
+        uint16_t* __restrict__ arg = D.arg;
+        int* __restrict__ done = pl.done;
+        const int64_t idx = gidx - D.item_base;
+        const int L = g.L, M = g.M;
         if (pl.trace && tid == 0) t0 = gtimer();
         int k, j, s;
         decode_item(idx, pl, k, j, s);
@@ -257,7 +291,7 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
         const int o0 = __ldg(dm.blk_off + s);
         const int nopt = __ldg(dm.blk_off + s + 1) - o0;
         for (int i = tid; i < nopt; i += NT) {
-            sm.thr[i] = pr.thr[rid * c.ocap + i];
+            sm.thr[i] = pr.thr[rid * pr.ocap + i];
             sm.pc[i] = pr.pc[o0 + i];
             sm.otot[i] = pr.otot[o0 + i];
         }
@@ -455,7 +489,7 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
             atomicAdd(done + (int64_t)k * pl.J + j, 1);
         }
         if (pl.trace && tid == 0) {
-            unsigned long long* tr = pl.trace + 6 * idx;
+            unsigned long long* tr = pl.trace + 6 * idx;  // per-table item index
             tr[0] = t0;
             tr[1] = ta;
             tr[2] = tb;
@@ -466,30 +500,15 @@ __global__ void __launch_bounds__(NT) fill_persistent(Geometry g, DevMenu dm, V*
     }
 }
 
-template <typename V>
-Programs<V> programs_of(const LaunchCtx& cx) {
-    Programs<V> p;
-    p.ptr = static_cast<longlong2*>(cx.prog.ptr);
-    p.sweep = static_cast<V*>(cx.prog.sweep);
-    p.gate = cx.prog.gate;
-    p.thr = cx.prog.thr;
-    p.pc = cx.prog.pc;
-    p.otot = static_cast<V*>(cx.prog.otot);
-    p.nq = cx.prog.nq;
-    return p;
-}
-
 template <typename V, int R>
-int launch_t(const LaunchCtx& cx) {
+int launch_t(const InstDesc* dev_desc, int n, int64_t total, int kcap, int ocap,
+             unsigned long long* counter, cudaStream_t st) {
     constexpr int NT = 256, U = 4;
-    cudaStream_t st = static_cast<cudaStream_t>(cx.stream);
-    const Geometry& g = cx.g;
-    const PlanDev& pl = cx.plan;
     Caps c;
-    c.TM = pl.TM;
-    c.seg_cap = pl.seg_cap;
-    c.kcap = g.L > 1 ? g.L - 1 : 1;
-    c.ocap = cx.max_opts > 0 ? cx.max_opts : 1;
+    c.TM = NT * R;
+    c.seg_cap = 0;
+    c.kcap = kcap > 0 ? kcap : 1;
+    c.ocap = ocap > 0 ? ocap : 1;
     const size_t smem = psmem_bytes<V>(c);
     auto kern = fill_persistent<V, NT, R, U>;
     if (smem > 48 * 1024 &&
@@ -504,11 +523,24 @@ int launch_t(const LaunchCtx& cx) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = (int64_t)per_sm * sms;
-    if (grid > pl.total) grid = pl.total;
-    if (cudaMemsetAsync(pl.counter, 0, cx.state_bytes, st) != cudaSuccess) return 3;
-    kern<<<(unsigned)grid, NT, smem, st>>>(g, cx.dm, static_cast<V*>(cx.opt), cx.arg, pl,
-                                           programs_of<V>(cx), c);
+    if (grid > total) grid = total;
+    if (grid < 1) return 0;
+    kern<<<(unsigned)grid, NT, smem, st>>>(dev_desc, n, total, counter, c);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+template <typename V>
+Programs<V> host_programs_of(const LaunchCtx& cx) {
+    Programs<V> p;
+    p.ptr = static_cast<longlong2*>(cx.prog.ptr);
+    p.sweep = static_cast<V*>(cx.prog.sweep);
+    p.gate = cx.prog.gate;
+    p.thr = cx.prog.thr;
+    p.pc = cx.prog.pc;
+    p.otot = static_cast<V*>(cx.prog.otot);
+    p.nq = cx.prog.nq;
+    p.ocap = cx.prog.ocap;
+    return p;
 }
 
 template <typename V>
@@ -519,17 +551,22 @@ int prep_t(const LaunchCtx& cx) {
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
     prep_programs<V><<<blocks, 128, 0, st>>>(cx.g, cx.dm, static_cast<const V*>(cx.opt),
-                                             programs_of<V>(cx), cx.max_opts > 0 ? cx.max_opts : 1);
+                                             host_programs_of<V>(cx));
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 }  // namespace
 
-void persistent_plan(const Geometry& g, int width, PersistPlan& p) {
+int persistent_choose_r(int32_t M) {
+    int R = (M + 1 >= 8192) ? 2 : 1;
+    if (const char* e = getenv("RKR_R")) R = atoi(e) == 2 ? 2 : 1;  // tuning knob
+    return R;
+}
+
+void persistent_plan(const Geometry& g, int width, int R, PersistPlan& p) {
     const int L = g.L;
     const size_t vb = width == 32 ? 4 : 8;
-    p.R = (g.M + 1 >= 8192) ? 2 : 1;
-    if (const char* e = getenv("RKR_R")) p.R = atoi(e) == 2 ? 2 : 1;  // tuning knob
+    p.R = R;
     p.TM = 256 * p.R;
     p.J = (g.M + 1 + p.TM - 1) / p.TM;
     p.dj = (g.pad + p.TM - 1) / p.TM;
@@ -571,9 +608,14 @@ int launch_prep_programs(const LaunchCtx& c) {
     return c.width == 32 ? prep_t<uint32_t>(c) : prep_t<int64_t>(c);
 }
 
-int launch_fill_persistent(const LaunchCtx& c) {
-    if (c.width == 32) return c.plan.R == 2 ? launch_t<uint32_t, 2>(c) : launch_t<uint32_t, 1>(c);
-    return c.plan.R == 2 ? launch_t<int64_t, 2>(c) : launch_t<int64_t, 1>(c);
+int launch_fill_batch(const InstDesc* dev_desc, int n, int64_t total, int width, int R, int kcap,
+                      int ocap, unsigned long long* counter, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (width == 32)
+        return R == 2 ? launch_t<uint32_t, 2>(dev_desc, n, total, kcap, ocap, counter, st)
+                      : launch_t<uint32_t, 1>(dev_desc, n, total, kcap, ocap, counter, st);
+    return R == 2 ? launch_t<int64_t, 2>(dev_desc, n, total, kcap, ocap, counter, st)
+                  : launch_t<int64_t, 1>(dev_desc, n, total, kcap, ocap, counter, st);
 }
 
 }  // namespace rkr

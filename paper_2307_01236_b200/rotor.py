@@ -110,6 +110,19 @@ def lib() -> ctypes.CDLL:
     L.rkr_debug_trace_items.argtypes = [p]
     L.rkr_debug_trace_items.restype = i64
     L.rkr_debug_trace_read.argtypes = [p, p, p, p]
+    L.rkr_batch_create.argtypes = [P(P(RkrMenu)), P(i64), P(i32), i32, P(RkrExec), P(p)]
+    L.rkr_batch_size.argtypes = [p]
+    L.rkr_batch_size.restype = i32
+    L.rkr_batch_table.argtypes = [p, i32]
+    L.rkr_batch_table.restype = p
+    L.rkr_batch_refill.argtypes = [p]
+    L.rkr_batch_stream.argtypes = [p]
+    L.rkr_batch_stream.restype = p
+    L.rkr_batch_sync.argtypes = [p]
+    L.rkr_batch_destroy.argtypes = [p]
+    L.rkr_batch_destroy.restype = None
+    L.rkr_sweep.argtypes = [P(RkrMenu), P(i64), i32, i32, P(RkrExec), P(i32), P(i64), P(i64), P(i32),
+                            P(i64), P(RkrOp), i64, P(i64)]
     L.rkr_backtrack_async.argtypes = [p, i32, i32, i32]
     L.rkr_backtrack_fetch.argtypes = [p, P(RkrOp), i64, P(i64)]
     _lib = L
@@ -203,6 +216,7 @@ class DpTable:
                  stream: Optional[int] = None, kernel: str = "persistent"):
         self._lib = lib()
         self._h = ctypes.c_void_p()
+        self._owned = True
         self._menu_struct = menu.struct()
         ex = _exec(device, width, stream, kernel)
         _check(self._lib.rkr_table_create(ctypes.byref(self._menu_struct), unit, m_max,
@@ -210,10 +224,21 @@ class DpTable:
         self.menu = menu
         self._host: Optional[Tuple[np.ndarray, np.ndarray, np.ndarray]] = None
 
+    @classmethod
+    def _borrow(cls, handle, menu: Menu, owner) -> "DpTable":
+        t = cls.__new__(cls)
+        t._lib = lib()
+        t._h = ctypes.c_void_p(handle)
+        t._owned = False
+        t._owner = owner  # keeps the batch alive
+        t.menu = menu
+        t._host = None
+        return t
+
     def close(self) -> None:
-        if self._h:
+        if self._h and self._owned:
             self._lib.rkr_table_destroy(self._h)
-            self._h = ctypes.c_void_p()
+        self._h = ctypes.c_void_p()
 
     def __del__(self):
         try:
@@ -401,3 +426,115 @@ def solve_chain(chain: Chain, menu: Menu, budget_bytes: int, units: int, device:
         _check(st, mf.value)
         raw = [(buf[i].kind, buf[i].block, buf[i].option) for i in range(n.value)]
         return ChainSolution(_named(raw, chain), ot.value, un.value, mt.value, raw)
+
+
+class Batch:
+    """Many independent DP tables filled by ONE persistent launch (rkr_batch_*)."""
+
+    def __init__(self, menus: Sequence[Menu], units: Sequence[int], m_maxs: Sequence[int],
+                 device: int = 0, width: str = "auto", stream: Optional[int] = None):
+        self._lib = lib()
+        n = len(menus)
+        self._structs = [m.struct() for m in menus]
+        arr = (ctypes.POINTER(RkrMenu) * n)(*[ctypes.pointer(x) for x in self._structs])
+        u = (ctypes.c_int64 * n)(*units)
+        mm = (ctypes.c_int32 * n)(*m_maxs)
+        ex = _exec(device, width, stream)
+        self._h = ctypes.c_void_p()
+        _check(self._lib.rkr_batch_create(arr, u, mm, n, ctypes.byref(ex), ctypes.byref(self._h)))
+        self.menus = list(menus)
+
+    def __len__(self) -> int:
+        return self._lib.rkr_batch_size(self._h)
+
+    def table(self, i: int) -> DpTable:
+        h = self._lib.rkr_batch_table(self._h, i)
+        if not h:
+            raise IndexError(i)
+        return DpTable._borrow(h, self.menus[i], self)
+
+    def refill(self) -> None:
+        _check(self._lib.rkr_batch_refill(self._h))
+
+    def stream(self) -> int:
+        return self._lib.rkr_batch_stream(self._h) or 0
+
+    def sync(self) -> None:
+        _check(self._lib.rkr_batch_sync(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.rkr_batch_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+@dataclass
+class SweepRow:
+    budget: int
+    feasible: bool
+    opt_time: int = 0
+    unit: int = 1
+    m_top: int = 0
+    min_feasible: int = -1
+    ops: List[Tuple[int, int, int]] = field(default_factory=list)
+
+
+def sweep_raw(menu: Menu, budgets: Sequence[int], units: int, device: int = 0,
+              width: str = "auto") -> List[SweepRow]:
+    """rkr_sweep: solve_chain for every budget (given order) in batched device calls."""
+    L = lib()
+    n = len(budgets)
+    ms = menu.struct()
+    ex = _exec(device, width)
+    b = (ctypes.c_int64 * n)(*budgets)
+    st = (ctypes.c_int32 * n)()
+    ot = (ctypes.c_int64 * n)()
+    un = (ctypes.c_int64 * n)()
+    mt = (ctypes.c_int32 * n)()
+    mf = (ctypes.c_int64 * n)()
+    offs = (ctypes.c_int64 * (n + 1))()
+    cap = max(1024, 8 * n * menu.L)
+    while True:
+        ops = (RkrOp * cap)()
+        rc = L.rkr_sweep(ctypes.byref(ms), b, n, units, ctypes.byref(ex), st, ot, un, mt, mf, ops,
+                         cap, offs)
+        if rc == RKR_ERR_CAPACITY and offs[n] > cap:
+            cap = offs[n]
+            continue
+        _check(rc)
+        break
+    rows = []
+    for i in range(n):
+        r = SweepRow(int(budgets[i]), st[i] == RKR_OK, ot[i], un[i], mt[i], mf[i])
+        r.ops = [(ops[o].kind, ops[o].block, ops[o].option) for o in range(offs[i], offs[i + 1])]
+        rows.append(r)
+    return rows
+
+
+def sweep(menu: Menu, budgets: Sequence[int], units: int, device: int = 0,
+          width: str = "auto") -> List[SweepRow]:
+    """The reference's cmd_sweep loop (tools/remat.cpp:217-263) on the device:
+    budgets sorted and de-duplicated, every solve batched, then the makespan
+    monotonicity check (optimality implies it never rises with budget)."""
+    bs = sorted(set(int(x) for x in budgets))
+    rows = sweep_raw(menu, bs, units, device, width)
+    prev = K_INF_TIME
+    for r in rows:
+        if not r.feasible:
+            continue
+        if r.opt_time > prev:
+            raise RuntimeError("sweep makespan increased with budget")
+        prev = r.opt_time
+    return rows

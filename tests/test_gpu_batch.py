@@ -1,0 +1,88 @@
+"""Batched device solves (rkr_batch_*, rkr_sweep): every table of a batch and
+every budget of a sweep bit-exact against the CPU oracle."""
+import numpy as np
+import pytest
+
+from paper_2307_01236_b200 import rotor
+from paper_2307_01236_b200.menu import BlockOption, Menu, synthetic_menu, tiny_chain_menu
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(a, b):
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+
+
+def _mixed_menus(random_suites):
+    ms = [(tiny_chain_menu(), 1, 64)]
+    for e in random_suites["enumeration"]["menus"][:12]:
+        ms.append((Menu.from_json(e["menu"]), 1, 20))
+    ms += [
+        (synthetic_menu(17, 5, 300, 12), 1, 300),
+        (synthetic_menu(40, 12, 700, 13, tie_stress=True), 1, 700),
+        (synthetic_menu(24, 8, 500, 41, byte_scale=1024), 997, 480),
+        (synthetic_menu(3, 2, 40, 5), 1, 0),
+    ]
+    return ms
+
+
+def test_batch_tables_match_oracle(orc, random_suites):
+    items = _mixed_menus(random_suites)
+    with rotor.Batch([m for m, _, _ in items], [u for _, u, _ in items],
+                     [M for _, _, M in items]) as b:
+        assert len(b) == len(items)
+        for rep in range(2):
+            if rep:
+                b.refill()
+            for i, (m, u, M) in enumerate(items):
+                st, *ref = orc.fill(m, u, M)
+                assert st == 0
+                t = b.table(i)
+                _same(t.download(), ref[:3])
+                top = ref[0][m.L - 1]  # row (0, L-1) in the s-major order
+                fin = np.nonzero(top < rotor.K_INF_TIME)[0]
+                if len(fin):
+                    mm = int(fin[0])
+                    _, ops = orc.build_schedule(m, u, M, tuple(ref[:3]), 0, m.L - 1, mm)
+                    assert t.backtrack(0, m.L - 1, mm) == ops
+
+
+def test_batch_falls_back_to_64bit_width(orc):
+    big = 10**15
+    wide = Menu.from_options([
+        [BlockOption(0, big, None, 2, 5, 5, 0), BlockOption(1, big, big, 6, 7, 6, 8)],
+        [BlockOption(0, big, None, 2, 5, 5, 0), BlockOption(1, big + 1, big, 5, 6, 6, 7)],
+    ], [2, 2, 2])
+    items = [(synthetic_menu(9, 3, 90, 3), 1, 90), (wide, 1, 30)]
+    with rotor.Batch([m for m, _, _ in items], [1, 1], [90, 30]) as b:
+        for i, (m, u, M) in enumerate(items):
+            t = b.table(i)
+            assert t.width() == 64
+            _same(t.download(), orc.fill(m, u, M)[1:4])
+
+
+def test_sweep_matches_solve_chain_per_budget(orc):
+    menu = synthetic_menu(24, 8, 500, 41, byte_scale=1024)
+    budgets = [1000, 20000, 70000, 71000, 80000, 90000, 120000, 200000, 512000, 2000000, 5]
+    rows = rotor.sweep_raw(menu, budgets, 500)
+    for r in rows:
+        st, ops, ot, un, mt, mf = orc.solve_chain(menu, r.budget, 500)
+        if st == 0:
+            assert r.feasible
+            assert (r.opt_time, r.unit, r.m_top) == (ot, un, mt)
+            assert r.ops == ops
+        else:
+            assert st == 2 and not r.feasible
+            assert r.min_feasible == mf
+
+
+def test_sweep_helper_sorts_dedups_and_is_monotone():
+    menu = synthetic_menu(33, 16, 4096, 44, byte_scale=64)
+    lo, hi = 5000, 400000
+    budgets = list(np.linspace(lo, hi, 40).astype(np.int64)) + [hi, lo]
+    rows = rotor.sweep(menu, budgets, 500)
+    assert [r.budget for r in rows] == sorted(set(int(b) for b in budgets))
+    feas = [r.opt_time for r in rows if r.feasible]
+    assert len(feas) > 10
+    assert all(a >= b for a, b in zip(feas, feas[1:]))

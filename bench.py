@@ -343,18 +343,226 @@ def b200_arm(args, world, rank, local):
     table.close()
 
 
+# ---------------------------------------------------------------------------
+# config 4: budget sweep (256 budgets x 4 chains), instances sharded by LPT
+# ---------------------------------------------------------------------------
+def sweep_instances():
+    """All config-4 instances with their quantization (host arithmetic only)."""
+    from paper_2307_01236_b200 import rotor
+    from paper_2307_01236_b200.sweep import SWEEP_UNITS, sweep_workload
+
+    menus, inst = sweep_workload()
+    rows = []
+    for i, x in enumerate(inst):
+        q = rotor.quantize(x.budget, SWEEP_UNITS)
+        a0 = rotor.to_units(int(menus[x.chain].act_sizes[0]), q.unit)
+        rows.append((i, x.chain, x.budget, q.unit, q.budget_units - a0))
+    return menus, rows
+
+
+def sweep_cells(menus, rows):
+    return sum(menus[ci].L * (menus[ci].L + 1) // 2 * (mt + 1) for _, ci, _, _, mt in rows if mt >= 0)
+
+
+def sweep_alg_bytes(menus, rows):
+    return sum(alg_bytes(menus[ci].L, mt) for _, ci, _, _, mt in rows if mt >= 0)
+
+
+def b200_arm_sweep(args, world, rank, local):
+    import torch
+
+    from paper_2307_01236_b200 import rotor
+    from paper_2307_01236_b200.sweep import SWEEP_CHAINS, SWEEP_UNITS, instance_cost, partition_lpt
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    menus, rows_all = sweep_instances()
+    costs = [instance_cost(menus[ci], max(mt, 0)) for _, ci, _, _, mt in rows_all]
+    mine = set(partition_lpt(costs, world)[rank])
+    rows = [r for r in rows_all if r[0] in mine]
+    res = [r for r in rows if r[4] >= 0]
+    stream = torch.cuda.Stream(device=local)
+    batch = rotor.Batch([menus[ci] for _, ci, _, _, _ in res], [u for *_, u, _ in res],
+                        [mt for *_, mt in res], device=local, stream=stream.cuda_stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    sampler = ClockSampler(local)
+    with sampler:
+        for _ in range(args.warmup):
+            batch.refill()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            evs[i][0].record(stream)
+            batch.refill()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    fill_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    tot_s = max_over_ranks(sum(fill_ms) / 1e3)
+    batch.close()
+
+    # end to end: rkr_sweep per chain from host menus (fill, tops, schedules, min-feasible)
+    by_chain = {}
+    for _, ci, b, _, _ in rows:
+        by_chain.setdefault(ci, []).append(b)
+    e2e = []
+    n_ops = 0
+    n_feas = 0
+    h2d = 0
+    for it in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        n_ops = n_feas = 0
+        for ci, bs in sorted(by_chain.items()):
+            out = rotor.sweep_raw(menus[ci], bs, SWEEP_UNITS, device=local)
+            n_ops += sum(len(r.ops) for r in out)
+            n_feas += sum(r.feasible for r in out)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            e2e.append(dt)
+    e2e_s = max_over_ranks(sum(e2e))
+    cells_rank = sweep_cells(menus, rows)
+    cells_total = sweep_cells(menus, rows_all)
+    if rank != 0:
+        return
+    peak, peak_src = measured_peak()
+    ab = sweep_alg_bytes(menus, rows)
+    achieved = ab / (statistics.mean(fill_ms) / 1e3) / 1e9
+    line = {
+        "metric": "DP cell-updates/sec (rk-Rotor chain DP, budget sweep)",
+        "value": cells_total * args.steps / tot_s,
+        "unit": "cells/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64 (stored as u32, overflow-proven)",
+        "data": "synthetic (SURVEY.md 8(d) generator, byte-sized menus, units=500)",
+        "config": {
+            "workload": "config4: budget sweep, 4 chains x 256 budgets "
+                        + "/".join(f"{L}x{B}" for _, L, B in SWEEP_CHAINS)
+                        + ", every instance's full DP table in one persistent launch per GPU",
+            "instances": len(rows_all), "cells_per_step": cells_total,
+            "l2": "flushed between timed steps (256 MiB write, outside the events)",
+            "parallelism": f"instances LPT-sharded over {world} GPU(s), no data-path collective",
+        },
+        "e2e": {"value": cells_total * args.steps / e2e_s, "unit": "cells/s",
+                "ms_per_step": 1e3 * e2e_s / args.steps,
+                "h2d_bytes_per_step": None, "d2h_bytes_per_step": 12 * n_ops,
+                "path": "rkr_sweep per chain from host menus: fill + tops + schedules + "
+                        "min-feasible search, schedules copied back",
+                "feasible_budgets_rank0": n_feas},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "fill_persistent (one batched launch per step)",
+                     "alg_bytes_per_fill": ab, "fill_ms": statistics.mean(fill_ms),
+                     "peak_source": peak_src},
+        "clocks": sampler.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sweep(menus, rows_all)
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sweep(menus, rows_all, per_chain=3):
+    """Reference solve_chain on a bounded sample of the sweep (per_chain budgets
+    of each chain, spread over the range), 1 thread; rate in cells/s."""
+    from oracle.pyoracle import HAVE_REF, Orc, Ref
+
+    from paper_2307_01236_b200.sweep import SWEEP_UNITS
+
+    ref = Ref() if HAVE_REF else Orc()
+    sample = []
+    for ci in range(len(menus)):
+        rs = [r for r in rows_all if r[1] == ci and r[4] >= 0]
+        for k in range(per_chain):
+            sample.append(rs[(k + 1) * len(rs) // (per_chain + 1)])
+    t0 = time.perf_counter()
+    for _, ci, b, _, _ in sample:
+        ref.solve_chain(menus[ci], b, SWEEP_UNITS)
+    secs = time.perf_counter() - t0
+    return {"value": sweep_cells(menus, sample) / secs, "unit": "cells/s", "cores": 1,
+            "kind": "reference" if HAVE_REF else "port",
+            "sample": f"{len(sample)} sweep instances ({per_chain} budgets per chain), "
+                      f"reference solve_chain, 1 thread, {secs:.1f} s"}
+
+
+def reference_arm_sweep(args, world, rank):
+    if rank != 0:
+        return
+    import concurrent.futures as cf
+
+    from oracle.pyoracle import HAVE_REF, Orc, Ref
+
+    from paper_2307_01236_b200.sweep import SWEEP_UNITS
+
+    menus, rows_all = sweep_instances()
+    threads = os.cpu_count() or 1
+    ref = Ref() if HAVE_REF else Orc()
+    # bounded sample per step: 2 instances per host thread, spread over the sweep
+    k = 2 * threads
+    sample = [rows_all[(i * len(rows_all)) // k] for i in range(k)]
+    sample = [r for r in sample if r[4] >= 0]
+
+    def step():
+        t0 = time.perf_counter()
+        with cf.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda r: ref.solve_chain(menus[r[1]], r[2], SWEEP_UNITS), sample))
+        return time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    value = sweep_cells(menus, sample) * args.steps / sum(times)
+    print(json.dumps({
+        "impl": "reference", "metric": "DP cell-updates/sec (rk-Rotor chain DP, budget sweep)",
+        "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (SURVEY.md 8(d) generator, byte-sized menus, units=500)",
+        "config": {"workload": f"config4 sample: {len(sample)} sweep instances per step on "
+                               f"{threads} host threads (reference solve_chain)"},
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": threads,
+                         "kind": "reference" if HAVE_REF else "port",
+                         "sample": f"{len(sample)} instances per step spread over the sweep"},
+        "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU leg (tuning runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     world, rank, local = dist_setup()
-    if args.impl == "reference":
+    if args.config == 4:
+        if args.impl == "reference":
+            reference_arm_sweep(args, world, rank)
+        else:
+            b200_arm_sweep(args, world, rank, local)
+    elif args.impl == "reference":
         reference_arm(args, world, rank)
     else:
         b200_arm(args, world, rank, local)

@@ -249,6 +249,7 @@ struct rkr_table {
     int32_t bt_s = 0, bt_t = 0, bt_m = 0;
     InstDesc hdesc{};             // this table as the persistent kernel sees it
     InstDesc* ddesc = nullptr;    // device copy (single-table fills)
+    LaunchPlan lplan{};           // single-table launch order (device pointers)
 
     LaunchCtx ctx() const {
         LaunchCtx c;
@@ -307,23 +308,24 @@ rkr_status alloc_and_upload(rkr_table* t) {
     take(np * 4);                              // 13 plan g
     take(np * 4);                              // 14 plan k
     take(sizeof(InstDesc));                    // 15 kernel descriptor
+    take(np * 4);                              // 16 plan instance ids (all 0)
     const size_t menu_bytes = bytes;
-    take(sizeof(int4) * (2 * L + 16));         // 16 backtrack stack
-    take(8 * sizeof(int64_t));                 // 17 dout
+    take(sizeof(int4) * (2 * L + 16));         // 17 backtrack stack
+    take(8 * sizeof(int64_t));                 // 18 dout
     const size_t vbytes = t->width == 32 ? 4 : 8;
-    take(((size_t)t->g.rows * t->g.sr + kOptSlack) * vbytes);  // 18 opt
-    take((size_t)t->g.rows * t->g.sa * 2);       // 19 arg
+    take(((size_t)t->g.rows * t->g.sr + kOptSlack) * vbytes);  // 19 opt
+    take((size_t)t->g.rows * t->g.sa * 2);       // 20 arg
     t->state_bytes = persistent_state_bytes(t->g, t->plan);
-    take(t->state_bytes);                        // 20 K1p counter + done flags
+    take(t->state_bytes);                        // 21 K1p counter + done flags
     const bool progs = t->kernel == RKR_KERNEL_PERSISTENT;
     const size_t nc = progs ? (size_t)program_cut_entries(t->g) : 0;
     const size_t ocap = std::max<int32_t>(h.max_opts, 1);
-    take(nc * 16);                               // 21 program ptr
-    take(nc * vbytes);                           // 22 program sweep
-    take(nc * 4);                                // 23 program gate
-    take(progs ? (size_t)t->g.rows * ocap * 4 : 0);  // 24 program thr
-    take(progs ? nq * 4 : 0);                    // 25 program pc
-    take(progs ? nq * vbytes : 0);               // 26 program otot
+    take(nc * 16);                               // 22 program ptr
+    take(nc * vbytes);                           // 23 program sweep
+    take(nc * 4);                                // 24 program gate
+    take(progs ? (size_t)t->g.rows * ocap * 4 : 0);  // 25 program thr
+    take(progs ? nq * 4 : 0);                    // 26 program pc
+    take(progs ? nq * vbytes : 0);               // 27 program otot
     t->menu_bytes = menu_bytes;
     t->block_bytes = bytes;
 
@@ -342,10 +344,16 @@ rkr_status alloc_and_upload(rkr_table* t) {
     t->dm.fwd0_full = reinterpret_cast<const int64_t*>(b + off[10]);
     t->dm.tf0 = reinterpret_cast<const int64_t*>(b + off[11]);
     t->ddesc = reinterpret_cast<InstDesc*>(b + off[15]);
-    t->stack = reinterpret_cast<int4*>(b + off[16]);
-    t->dout = reinterpret_cast<int64_t*>(b + off[17]);
-    t->opt = b + off[18];
-    t->arg = reinterpret_cast<uint16_t*>(b + off[19]);
+    t->lplan.start = reinterpret_cast<const int64_t*>(b + off[12]);
+    t->lplan.j = reinterpret_cast<const int32_t*>(b + off[13]);
+    t->lplan.k = reinterpret_cast<const int32_t*>(b + off[14]);
+    t->lplan.inst = reinterpret_cast<const int32_t*>(b + off[16]);
+    t->lplan.n = (int32_t)np;
+    t->lplan.total = t->plan.total;
+    t->stack = reinterpret_cast<int4*>(b + off[17]);
+    t->dout = reinterpret_cast<int64_t*>(b + off[18]);
+    t->opt = b + off[19];
+    t->arg = reinterpret_cast<uint16_t*>(b + off[20]);
     PlanDev& pd = t->pdev;
     pd.R = t->plan.R;
     pd.TM = t->plan.TM;
@@ -357,15 +365,15 @@ rkr_status alloc_and_upload(rkr_table* t) {
     pd.start = reinterpret_cast<const int64_t*>(b + off[12]);
     pd.g = reinterpret_cast<const int32_t*>(b + off[13]);
     pd.k = reinterpret_cast<const int32_t*>(b + off[14]);
-    pd.counter = reinterpret_cast<unsigned long long*>(b + off[20]);
-    pd.done = reinterpret_cast<int32_t*>(b + off[20] + 8);
+    pd.counter = reinterpret_cast<unsigned long long*>(b + off[21]);
+    pd.done = reinterpret_cast<int32_t*>(b + off[21] + 8);
     pd.trace = nullptr;
-    t->prog.ptr = b + off[21];
-    t->prog.sweep = b + off[22];
-    t->prog.gate = reinterpret_cast<int32_t*>(b + off[23]);
-    t->prog.thr = reinterpret_cast<int32_t*>(b + off[24]);
-    t->prog.pc = reinterpret_cast<int32_t*>(b + off[25]);
-    t->prog.otot = b + off[26];
+    t->prog.ptr = b + off[22];
+    t->prog.sweep = b + off[23];
+    t->prog.gate = reinterpret_cast<int32_t*>(b + off[24]);
+    t->prog.thr = reinterpret_cast<int32_t*>(b + off[25]);
+    t->prog.pc = reinterpret_cast<int32_t*>(b + off[26]);
+    t->prog.otot = b + off[27];
     t->prog.nq = (int64_t)h.ids.size();
     t->prog.ocap = (int32_t)ocap;
     t->hdesc.g = t->g;
@@ -412,7 +420,7 @@ rkr_status enqueue_fill(rkr_table* t) {
         return RKR_OK;
     }
     CK(cudaMemsetAsync(t->pdev.counter, 0, t->state_bytes, t->stream));
-    if (launch_fill_batch(t->ddesc, 1, t->plan.total, t->width, t->plan.R,
+    if (launch_fill_batch(t->ddesc, &t->hdesc, t->lplan, t->width, t->plan.R,
                           std::max(t->g.L - 1, 1), std::max(t->hm.max_opts, 1), t->pdev.counter,
                           t->stream))
         return cuda_fail(cudaGetLastError(), "fill launch");
@@ -912,6 +920,7 @@ struct rkr_batch {
     unsigned long long* counter = nullptr;
     size_t state_bytes = 0;              // counter + flags
     int64_t total = 0;
+    LaunchPlan lplan{};                  // merged launch order (device pointers)
 };
 
 namespace {
@@ -926,8 +935,8 @@ void free_batch(rkr_batch* b) {
 
 rkr_status batch_fill(rkr_batch* b) {
     CK(cudaMemsetAsync(b->counter, 0, b->state_bytes, b->stream));
-    if (launch_fill_batch(b->ddesc, (int)b->tables.size(), b->total, b->width, b->R, b->kcap,
-                          b->ocap, b->counter, b->stream))
+    if (launch_fill_batch(b->ddesc, nullptr, b->lplan, b->width, b->R, b->kcap, b->ocap,
+                          b->counter, b->stream))
         return cuda_fail(cudaGetLastError(), "batch fill launch");
     return RKR_OK;
 }
@@ -974,13 +983,33 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
         b->ocap = std::max(b->ocap, t->hm.max_opts);
         flags += (size_t)t->g.L * t->plan.J;
     }
+    // merged launch order: tables advance their wavefronts together
+    std::vector<const PersistPlan*> plans;
+    std::vector<int32_t> Ls;
+    for (rkr_table* t : b->tables) {
+        plans.push_back(&t->plan);
+        Ls.push_back(t->g.L);
+    }
+    HostLaunchPlan hp;
+    merge_plans(plans, Ls, hp);
+    const size_t np = hp.start.size();
     const size_t desc_bytes = (size_t)round_up((int64_t)(sizeof(InstDesc) * n), 256);
+    const size_t plan_bytes = (size_t)round_up((int64_t)(np * 8), 256) + 3 * (size_t)round_up((int64_t)(np * 4), 256);
     b->state_bytes = 8 + flags * sizeof(int);
-    CK(cudaMallocAsync(&b->block, desc_bytes + b->state_bytes, b->stream));
+    CK(cudaMallocAsync(&b->block, desc_bytes + plan_bytes + b->state_bytes, b->stream));
     unsigned char* base = static_cast<unsigned char*>(b->block);
     b->ddesc = reinterpret_cast<InstDesc*>(base);
-    b->counter = reinterpret_cast<unsigned long long*>(base + desc_bytes);
-    int32_t* flag = reinterpret_cast<int32_t*>(base + desc_bytes + 8);
+    unsigned char* pb = base + desc_bytes;
+    const size_t o_start = 0, o_inst = round_up((int64_t)(np * 8), 256);
+    const size_t o_k = o_inst + round_up((int64_t)(np * 4), 256), o_j = o_k + round_up((int64_t)(np * 4), 256);
+    b->lplan.start = reinterpret_cast<const int64_t*>(pb + o_start);
+    b->lplan.inst = reinterpret_cast<const int32_t*>(pb + o_inst);
+    b->lplan.k = reinterpret_cast<const int32_t*>(pb + o_k);
+    b->lplan.j = reinterpret_cast<const int32_t*>(pb + o_j);
+    b->lplan.n = (int32_t)np;
+    b->lplan.total = hp.total;
+    b->counter = reinterpret_cast<unsigned long long*>(base + desc_bytes + plan_bytes);
+    int32_t* flag = reinterpret_cast<int32_t*>(base + desc_bytes + plan_bytes + 8);
     std::vector<InstDesc> hd(n);
     int64_t item = 0;
     for (int32_t i = 0; i < n; ++i) {
@@ -993,10 +1022,16 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
         item += t->plan.total;
     }
     b->total = item;
+    const size_t up = desc_bytes + plan_bytes;
     void* stage = nullptr;
-    CK(t_stage.get(sizeof(InstDesc) * n, &stage));
-    std::memcpy(stage, hd.data(), sizeof(InstDesc) * n);
-    CK(cudaMemcpyAsync(b->ddesc, stage, sizeof(InstDesc) * n, cudaMemcpyHostToDevice, b->stream));
+    CK(t_stage.get(up, &stage));
+    unsigned char* sb = static_cast<unsigned char*>(stage);
+    std::memcpy(sb, hd.data(), sizeof(InstDesc) * n);
+    std::memcpy(sb + desc_bytes + o_start, hp.start.data(), np * 8);
+    std::memcpy(sb + desc_bytes + o_inst, hp.inst.data(), np * 4);
+    std::memcpy(sb + desc_bytes + o_k, hp.k.data(), np * 4);
+    std::memcpy(sb + desc_bytes + o_j, hp.j.data(), np * 4);
+    CK(cudaMemcpyAsync(b->block, stage, up, cudaMemcpyHostToDevice, b->stream));
     CK(cudaEventRecord(t_stage.done, b->stream));
     rkr_status st = batch_fill(b);
     if (st != RKR_OK) {

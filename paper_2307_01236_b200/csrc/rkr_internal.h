@@ -92,7 +92,6 @@ struct ProgDev {
 int64_t program_cut_entries(const Geometry& g);
 
 // One table of a (possibly batched) persistent fill, as the kernel sees it.
-// Items of instance i are global items [item_base, item_base + plan.total).
 struct InstDesc {
     Geometry g;
     DevMenu dm;
@@ -101,8 +100,29 @@ struct InstDesc {
     PlanDev plan;
     ProgDev prog;
     void* stack;        // backtrack stack (int4[2L + 16])
-    int64_t item_base;
+    int64_t item_base;  // unused by the kernel (kept for diagnostics)
 };
+// The launch-wide item order: entry e covers items [start[e], start[e] +
+// L_inst - k[e]) = rows s = 0.. of (instance inst[e], diagonal k[e], tile
+// j[e]).  Entries are sorted by (lambda_inst * j + k, inst, j), so tables of
+// a batch advance their wavefronts together and every item only waits on
+// items of smaller index.
+struct LaunchPlan {
+    const int64_t* start;
+    const int32_t* inst;
+    const int32_t* k;
+    const int32_t* j;
+    int32_t n;
+    int64_t total;
+};
+// Host side: merge per-table plans into one launch order.
+struct HostLaunchPlan {
+    std::vector<int64_t> start;
+    std::vector<int32_t> inst, k, j;
+    int64_t total = 0;
+};
+void merge_plans(const std::vector<const PersistPlan*>& plans, const std::vector<int32_t>& L,
+                 HostLaunchPlan& out);
 int launch_batch_walk(const InstDesc* d, const int32_t* m_at, const uint8_t* active, int n,
                       int width, int32_t* ops, int64_t cap, int64_t* out, void* stream);
 int launch_batch_tops(const InstDesc* d, const int32_t* m_at, int n, int width, int64_t* out,
@@ -111,8 +131,10 @@ int launch_batch_first_feasible(const InstDesc* d, int n, int width, int32_t* ou
 // Fill n tables with ONE persistent launch.  All tables share the cost
 // width and the plan's R.  The counter and every table's done flags must be
 // zeroed on `stream` before the call (they are, by the callers in rkr_capi).
-int launch_fill_batch(const InstDesc* dev_desc, int n, int64_t total_items, int width, int R,
-                      int kcap, int ocap, unsigned long long* counter, void* stream);
+// single != nullptr: a one-table launch whose descriptor is passed by value.
+int launch_fill_batch(const InstDesc* dev_desc, const InstDesc* single, const LaunchPlan& lp,
+                      int width, int R, int kcap, int ocap, unsigned long long* counter,
+                      void* stream);
 void persistent_plan(const Geometry& g, int width, int R, PersistPlan& p);
 int persistent_choose_r(int32_t M);
 size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p);  // counter + flags

@@ -211,21 +211,6 @@ __device__ inline PSmem<V> pcarve(unsigned char* p, const Caps& c) {
     return s;
 }
 
-// item index -> (k, j, s) through the plan table (binary search on start).
-__device__ inline void decode_item(int64_t idx, const PlanDev& p, int& k, int& j, int& s) {
-    int lo = 0, hi = p.n_plan - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(p.start + mid) <= idx)
-            lo = mid;
-        else
-            hi = mid - 1;
-    }
-    k = __ldg(p.k + lo);
-    j = __ldg(p.g + lo);
-    s = (int)(idx - __ldg(p.start + lo));
-}
-
 template <typename V>
 __device__ inline Programs<V> programs_of(const ProgDev& q) {
     Programs<V> p;
@@ -240,9 +225,13 @@ __device__ inline Programs<V> programs_of(const ProgDev& q) {
     return p;
 }
 
-template <typename V, int NT, int R, int U>
-__global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict__ inst, int n_inst,
-                                                      int64_t total,
+// SINGLE: one table whose descriptor travels as a kernel parameter (constant
+// bank); batches read their descriptors from global memory (measured 22%
+// slower per item on config 3, so the single-table path keeps the param).
+template <typename V, int NT, int R, int U, bool SINGLE>
+__global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict__ inst,
+                                                      const __grid_constant__ InstDesc d0,
+                                                      LaunchPlan lp,
                                                       unsigned long long* __restrict__ counter,
                                                       Caps c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -256,21 +245,24 @@ __global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict
         if (tid == 0) sm.item[0] = next;
         __syncthreads();
         const int64_t gidx = sm.item[0];
-        if (gidx >= total) break;
+        if (gidx >= lp.total) break;
         // prefetch the next item while this one runs (the earliest unfinished
         // item is always one being processed, so this cannot deadlock)
         if (tid == 0) next = (long long)atomicAdd(counter, 1ull);
         unsigned long long t0 = 0;
-        // instance of this item (tables are laid out back to back in item space)
-        int ia = 0, ib = n_inst - 1;
-        while (ia < ib) {
-            const int mid = (ia + ib + 1) >> 1;
-            if (__ldg(&inst[mid].item_base) <= gidx)
-                ia = mid;
+        // item -> (instance, diagonal, tile, s) through the launch plan
+        int ea = 0, eb = lp.n - 1;
+        while (ea < eb) {
+            const int mid = (ea + eb + 1) >> 1;
+            if (__ldg(lp.start + mid) <= gidx)
+                ea = mid;
             else
-                ib = mid - 1;
+                eb = mid - 1;
         }
-        const InstDesc& D = inst[ia];
+        const int k = __ldg(lp.k + ea);
+        const int j = __ldg(lp.j + ea);
+        const int s = (int)(gidx - __ldg(lp.start + ea));
+        const InstDesc& D = SINGLE ? d0 : inst[__ldg(lp.inst + ea)];
         const Geometry g = D.g;
         const DevMenu dm = D.dm;
         const PlanDev pl = D.plan;
@@ -278,11 +270,9 @@ __global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict
         V* __restrict__ opt = static_cast<V*>(D.opt);
         uint16_t* __restrict__ arg = D.arg;
         int* __restrict__ done = pl.done;
-        const int64_t idx = gidx - D.item_base;
+        const int64_t idx = gidx;  // trace slot (traced fills are single-table)
         const int L = g.L, M = g.M;
         if (pl.trace && tid == 0) t0 = gtimer();
-        int k, j, s;
-        decode_item(idx, pl, k, j, s);
         const int t = s + k;
         const int m0 = j * pl.TM;
         const int64_t rid = row_id(L, s, t);
@@ -500,8 +490,8 @@ __global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict
     }
 }
 
-template <typename V, int R>
-int launch_t(const InstDesc* dev_desc, int n, int64_t total, int kcap, int ocap,
+template <typename V, int R, bool SINGLE>
+int launch_t(const InstDesc* dev_desc, const InstDesc& d0, const LaunchPlan& lp, int kcap, int ocap,
              unsigned long long* counter, cudaStream_t st) {
     constexpr int NT = 256, U = 4;
     Caps c;
@@ -510,7 +500,7 @@ int launch_t(const InstDesc* dev_desc, int n, int64_t total, int kcap, int ocap,
     c.kcap = kcap > 0 ? kcap : 1;
     c.ocap = ocap > 0 ? ocap : 1;
     const size_t smem = psmem_bytes<V>(c);
-    auto kern = fill_persistent<V, NT, R, U>;
+    auto kern = fill_persistent<V, NT, R, U, SINGLE>;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
@@ -523,9 +513,9 @@ int launch_t(const InstDesc* dev_desc, int n, int64_t total, int kcap, int ocap,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = (int64_t)per_sm * sms;
-    if (grid > total) grid = total;
+    if (grid > lp.total) grid = lp.total;
     if (grid < 1) return 0;
-    kern<<<(unsigned)grid, NT, smem, st>>>(dev_desc, n, total, counter, c);
+    kern<<<(unsigned)grid, NT, smem, st>>>(dev_desc, d0, lp, counter, c);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -608,14 +598,59 @@ int launch_prep_programs(const LaunchCtx& c) {
     return c.width == 32 ? prep_t<uint32_t>(c) : prep_t<int64_t>(c);
 }
 
-int launch_fill_batch(const InstDesc* dev_desc, int n, int64_t total, int width, int R, int kcap,
-                      int ocap, unsigned long long* counter, void* stream) {
+int launch_fill_batch(const InstDesc* dev_desc, const InstDesc* single, const LaunchPlan& lp,
+                      int width, int R, int kcap, int ocap, unsigned long long* counter,
+                      void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    InstDesc d0{};
+    if (single) d0 = *single;
+    if (single) {
+        if (width == 32)
+            return R == 2 ? launch_t<uint32_t, 2, true>(dev_desc, d0, lp, kcap, ocap, counter, st)
+                          : launch_t<uint32_t, 1, true>(dev_desc, d0, lp, kcap, ocap, counter, st);
+        return R == 2 ? launch_t<int64_t, 2, true>(dev_desc, d0, lp, kcap, ocap, counter, st)
+                      : launch_t<int64_t, 1, true>(dev_desc, d0, lp, kcap, ocap, counter, st);
+    }
     if (width == 32)
-        return R == 2 ? launch_t<uint32_t, 2>(dev_desc, n, total, kcap, ocap, counter, st)
-                      : launch_t<uint32_t, 1>(dev_desc, n, total, kcap, ocap, counter, st);
-    return R == 2 ? launch_t<int64_t, 2>(dev_desc, n, total, kcap, ocap, counter, st)
-                  : launch_t<int64_t, 1>(dev_desc, n, total, kcap, ocap, counter, st);
+        return R == 2 ? launch_t<uint32_t, 2, false>(dev_desc, d0, lp, kcap, ocap, counter, st)
+                      : launch_t<uint32_t, 1, false>(dev_desc, d0, lp, kcap, ocap, counter, st);
+    return R == 2 ? launch_t<int64_t, 2, false>(dev_desc, d0, lp, kcap, ocap, counter, st)
+                  : launch_t<int64_t, 1, false>(dev_desc, d0, lp, kcap, ocap, counter, st);
+}
+
+void merge_plans(const std::vector<const PersistPlan*>& plans, const std::vector<int32_t>& L,
+                 HostLaunchPlan& out) {
+    struct E {
+        int64_t key;
+        int32_t inst, j, k;
+    };
+    std::vector<E> es;
+    size_t n = 0;
+    for (const PersistPlan* p : plans) n += p->start.size();
+    es.reserve(n);
+    for (size_t i = 0; i < plans.size(); ++i) {
+        const PersistPlan& p = *plans[i];
+        for (size_t e = 0; e < p.start.size(); ++e)
+            es.push_back({(int64_t)p.lambda * p.g[e] + p.k[e], (int32_t)i, p.g[e], p.k[e]});
+    }
+    std::stable_sort(es.begin(), es.end(), [](const E& a, const E& b) {
+        if (a.key != b.key) return a.key < b.key;
+        if (a.inst != b.inst) return a.inst < b.inst;
+        return a.j < b.j;
+    });
+    out.start.clear();
+    out.inst.clear();
+    out.k.clear();
+    out.j.clear();
+    int64_t cur = 0;
+    for (const E& e : es) {
+        out.start.push_back(cur);
+        out.inst.push_back(e.inst);
+        out.k.push_back(e.k);
+        out.j.push_back(e.j);
+        cur += L[e.inst] - e.k;
+    }
+    out.total = cur;
 }
 
 }  // namespace rkr

@@ -220,6 +220,33 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
                      int32_t* m_top, int64_t* min_feasible, rkr_op* ops, int64_t ops_cap,
                      int64_t* ops_offsets);
 
+/* ---- Budget-axis sharding (BASELINE config 5) -----------------------------
+ * One table split into n contiguous budget ranges ("shards"), shard i on
+ * devices[i] (NULL: all on exec->device).  Each shard is filled by the
+ * persistent kernel; an item whose slots are the next shard's halo (its
+ * lowest `pad` slots read shifted columns of this shard) stores them straight
+ * into the next shard's rows -- peer memory over NVLink when the shards live
+ * on different GPUs -- and signals it with a counter, so the exchange is
+ * fused into the fill (no collective call, no host round trip per diagonal).
+ * Every shard must own at least `pad` slots.  Reads take GLOBAL budget slots;
+ * results are bit-identical to the unsharded table. */
+typedef struct rkr_sharded rkr_sharded;
+rkr_status rkr_sharded_create(const rkr_menu* menu, int64_t unit, int32_t m_max, int32_t n_shards,
+                              const int32_t* devices, const rkr_exec* exec, rkr_sharded** out);
+int32_t rkr_sharded_count(const rkr_sharded* sharded);
+rkr_status rkr_sharded_range(const rkr_sharded* sharded, int32_t shard, int32_t* m_lo,
+                             int32_t* m_hi);
+rkr_table* rkr_sharded_shard(rkr_sharded* sharded, int32_t shard);  /* borrowed, local slots */
+rkr_status rkr_sharded_refill(rkr_sharded* sharded);
+rkr_status rkr_sharded_sync(const rkr_sharded* sharded);
+rkr_status rkr_sharded_opt(const rkr_sharded* sharded, int32_t s, int32_t t, int32_t m,
+                           int64_t* out);
+rkr_status rkr_sharded_row(const rkr_sharded* sharded, int32_t s, int32_t t, int64_t* opt,
+                           int8_t* kind, int32_t* value);
+rkr_status rkr_sharded_backtrack(rkr_sharded* sharded, int32_t s, int32_t t, int32_t m,
+                                 rkr_op* ops, int64_t cap, int64_t* n_ops);
+void rkr_sharded_destroy(rkr_sharded* sharded);
+
 /* Diagnostics (persistent kernel only): 6 globaltimer stamps per item of the
  * next fills {dequeued, diagonal k-2 met, bulk cuts done, diagonal k-1 met,
  * tail done, published}; item_k/item_j (nullable) receive each item's

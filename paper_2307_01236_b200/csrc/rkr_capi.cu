@@ -427,14 +427,17 @@ rkr_status enqueue_fill(rkr_table* t) {
     return RKR_OK;
 }
 
+// Budget-axis shard of a table: local slot 0 is global slot m_base; pad is
+// common to all shards; j_offset = global tile index of local tile 0.
+struct ShardSpec {
+    int32_t m_base, pad, j_offset;
+};
+
 // Everything rkr_table_create does except the fill: validation and unit
 // precompute, geometry, plan, one pooled allocation + one H2D copy, pads,
 // cell programs.  R = 0 lets the plan choose the per-thread slot count.
 rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, const rkr_exec* exec,
-                         int R, rkr_table** out);
-
-rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, const rkr_exec* exec,
-                         int R, rkr_table** out) {
+                         int R, rkr_table** out, const ShardSpec* spec = nullptr) {
     if (!out) return fail(RKR_ERR_ARGUMENT, "null output handle");
     *out = nullptr;
     if (m_max < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
@@ -473,11 +476,17 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
     t->g.M = m_max;
     t->g.pad = (int32_t)std::min<int64_t>(maxshift, (int64_t)m_max + 1);
     t->g.pad = (int32_t)round_up(t->g.pad, 8);
+    if (spec) {
+        t->g.pad = spec->pad;
+        t->g.m_base = spec->m_base;
+    }
     t->g.sr = round_up((int64_t)t->g.pad + m_max + 1, 32);
     t->g.sa = round_up((int64_t)m_max + 1, 64);
     t->g.rows = (int64_t)h.L * (h.L + 1) / 2;
-    if (t->kernel == RKR_KERNEL_PERSISTENT)
+    if (t->kernel == RKR_KERNEL_PERSISTENT) {
         persistent_plan(t->g, t->width, R > 0 ? R : persistent_choose_r(m_max), t->plan);
+        if (spec) t->plan.j_offset = spec->j_offset;
+    }
     st = alloc_and_upload(t);
     if (st == RKR_OK && launch_init_pads(t->ctx())) st = cuda_fail(cudaGetLastError(), "pad launch");
     if (st == RKR_OK && t->kernel == RKR_KERNEL_PERSISTENT && launch_prep_programs(t->ctx()))
@@ -921,6 +930,10 @@ struct rkr_batch {
     size_t state_bytes = 0;              // counter + flags
     int64_t total = 0;
     LaunchPlan lplan{};                  // merged launch order (device pointers)
+    HostLaunchPlan hp;
+    std::vector<InstDesc> hd;            // host copies of the descriptors
+    size_t desc_bytes = 0, plan_bytes = 0, o_inst = 0, o_k = 0, o_j = 0;
+    bool owns_tables = true;
 };
 
 namespace {
@@ -928,9 +941,22 @@ namespace {
 void free_batch(rkr_batch* b) {
     if (!b) return;
     DeviceGuard dg(b->device);
-    for (rkr_table* t : b->tables) free_table(t);
+    if (b->owns_tables)
+        for (rkr_table* t : b->tables) free_table(t);
     if (b->block) cudaFreeAsync(b->block, b->stream);
     delete b;
+}
+
+rkr_status batch_zero(rkr_batch* b) {
+    CK(cudaMemsetAsync(b->counter, 0, b->state_bytes, b->stream));
+    return RKR_OK;
+}
+
+rkr_status batch_launch(rkr_batch* b) {
+    if (launch_fill_batch(b->ddesc, nullptr, b->lplan, b->width, b->R, b->kcap, b->ocap,
+                          b->counter, b->stream))
+        return cuda_fail(cudaGetLastError(), "batch fill launch");
+    return RKR_OK;
 }
 
 rkr_status batch_fill(rkr_batch* b) {
@@ -938,6 +964,83 @@ rkr_status batch_fill(rkr_batch* b) {
     if (launch_fill_batch(b->ddesc, nullptr, b->lplan, b->width, b->R, b->kcap, b->ocap,
                           b->counter, b->stream))
         return cuda_fail(cudaGetLastError(), "batch fill launch");
+    return RKR_OK;
+}
+
+// Allocate a batch's descriptor array, merged plan and state (counter, done
+// flags and halo counters of every table) and fill the host descriptors
+// (b->hd); batch_upload copies them to the device.
+rkr_status batch_layout(rkr_batch* b) {
+    const int n = (int)b->tables.size();
+    b->stream = b->tables[0]->stream;
+    b->width = b->tables[0]->width;
+    size_t flags = 0, halos = 0;
+    for (rkr_table* t : b->tables) {
+        b->kcap = std::max(b->kcap, t->g.L - 1);
+        b->ocap = std::max(b->ocap, t->hm.max_opts);
+        flags += (size_t)t->g.L * t->plan.J;
+        halos += (size_t)t->g.L;
+    }
+    // merged launch order: tables advance their wavefronts together
+    std::vector<const PersistPlan*> plans;
+    std::vector<int32_t> Ls;
+    for (rkr_table* t : b->tables) {
+        plans.push_back(&t->plan);
+        Ls.push_back(t->g.L);
+    }
+    merge_plans(plans, Ls, b->hp);
+    const size_t np = b->hp.start.size();
+    b->desc_bytes = (size_t)round_up((int64_t)(sizeof(InstDesc) * n), 256);
+    b->o_inst = round_up((int64_t)(np * 8), 256);
+    b->o_k = b->o_inst + round_up((int64_t)(np * 4), 256);
+    b->o_j = b->o_k + round_up((int64_t)(np * 4), 256);
+    b->plan_bytes = b->o_j + round_up((int64_t)(np * 4), 256);
+    b->state_bytes = 8 + (flags + halos) * sizeof(int);
+    CK(cudaMallocAsync(&b->block, b->desc_bytes + b->plan_bytes + b->state_bytes, b->stream));
+    unsigned char* base = static_cast<unsigned char*>(b->block);
+    b->ddesc = reinterpret_cast<InstDesc*>(base);
+    unsigned char* pb = base + b->desc_bytes;
+    b->lplan.start = reinterpret_cast<const int64_t*>(pb);
+    b->lplan.inst = reinterpret_cast<const int32_t*>(pb + b->o_inst);
+    b->lplan.k = reinterpret_cast<const int32_t*>(pb + b->o_k);
+    b->lplan.j = reinterpret_cast<const int32_t*>(pb + b->o_j);
+    b->lplan.n = (int32_t)np;
+    b->lplan.total = b->hp.total;
+    b->counter = reinterpret_cast<unsigned long long*>(base + b->desc_bytes + b->plan_bytes);
+    int32_t* flag = reinterpret_cast<int32_t*>(base + b->desc_bytes + b->plan_bytes + 8);
+    int32_t* halo = flag + flags;
+    b->hd.assign(n, InstDesc{});
+    int64_t item = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        rkr_table* t = b->tables[i];
+        b->hd[i] = t->hdesc;
+        b->hd[i].plan.done = flag;
+        b->hd[i].plan.trace = nullptr;
+        b->hd[i].halo = halo;
+        b->hd[i].item_base = item;
+        flag += (size_t)t->g.L * t->plan.J;
+        halo += t->g.L;
+        item += t->plan.total;
+    }
+    b->total = item;
+    return RKR_OK;
+}
+
+rkr_status batch_upload(rkr_batch* b) {
+    const int n = (int)b->tables.size();
+    const size_t np = b->hp.start.size();
+    const size_t up = b->desc_bytes + b->plan_bytes;
+    void* stage = nullptr;
+    CK(t_stage.get(up, &stage));
+    unsigned char* sb = static_cast<unsigned char*>(stage);
+    std::memcpy(sb, b->hd.data(), sizeof(InstDesc) * n);
+    unsigned char* pb = sb + b->desc_bytes;
+    std::memcpy(pb, b->hp.start.data(), np * 8);
+    std::memcpy(pb + b->o_inst, b->hp.inst.data(), np * 4);
+    std::memcpy(pb + b->o_k, b->hp.k.data(), np * 4);
+    std::memcpy(pb + b->o_j, b->hp.j.data(), np * 4);
+    CK(cudaMemcpyAsync(b->block, stage, up, cudaMemcpyHostToDevice, b->stream));
+    CK(cudaEventRecord(t_stage.done, b->stream));
     return RKR_OK;
 }
 
@@ -975,65 +1078,9 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
         }
         b->tables.push_back(t);
     }
-    b->stream = b->tables[0]->stream;
-    b->width = b->tables[0]->width;
-    size_t flags = 0;
-    for (rkr_table* t : b->tables) {
-        b->kcap = std::max(b->kcap, t->g.L - 1);
-        b->ocap = std::max(b->ocap, t->hm.max_opts);
-        flags += (size_t)t->g.L * t->plan.J;
-    }
-    // merged launch order: tables advance their wavefronts together
-    std::vector<const PersistPlan*> plans;
-    std::vector<int32_t> Ls;
-    for (rkr_table* t : b->tables) {
-        plans.push_back(&t->plan);
-        Ls.push_back(t->g.L);
-    }
-    HostLaunchPlan hp;
-    merge_plans(plans, Ls, hp);
-    const size_t np = hp.start.size();
-    const size_t desc_bytes = (size_t)round_up((int64_t)(sizeof(InstDesc) * n), 256);
-    const size_t plan_bytes = (size_t)round_up((int64_t)(np * 8), 256) + 3 * (size_t)round_up((int64_t)(np * 4), 256);
-    b->state_bytes = 8 + flags * sizeof(int);
-    CK(cudaMallocAsync(&b->block, desc_bytes + plan_bytes + b->state_bytes, b->stream));
-    unsigned char* base = static_cast<unsigned char*>(b->block);
-    b->ddesc = reinterpret_cast<InstDesc*>(base);
-    unsigned char* pb = base + desc_bytes;
-    const size_t o_start = 0, o_inst = round_up((int64_t)(np * 8), 256);
-    const size_t o_k = o_inst + round_up((int64_t)(np * 4), 256), o_j = o_k + round_up((int64_t)(np * 4), 256);
-    b->lplan.start = reinterpret_cast<const int64_t*>(pb + o_start);
-    b->lplan.inst = reinterpret_cast<const int32_t*>(pb + o_inst);
-    b->lplan.k = reinterpret_cast<const int32_t*>(pb + o_k);
-    b->lplan.j = reinterpret_cast<const int32_t*>(pb + o_j);
-    b->lplan.n = (int32_t)np;
-    b->lplan.total = hp.total;
-    b->counter = reinterpret_cast<unsigned long long*>(base + desc_bytes + plan_bytes);
-    int32_t* flag = reinterpret_cast<int32_t*>(base + desc_bytes + plan_bytes + 8);
-    std::vector<InstDesc> hd(n);
-    int64_t item = 0;
-    for (int32_t i = 0; i < n; ++i) {
-        rkr_table* t = b->tables[i];
-        hd[i] = t->hdesc;
-        hd[i].plan.done = flag;
-        hd[i].plan.trace = nullptr;
-        hd[i].item_base = item;
-        flag += (size_t)t->g.L * t->plan.J;
-        item += t->plan.total;
-    }
-    b->total = item;
-    const size_t up = desc_bytes + plan_bytes;
-    void* stage = nullptr;
-    CK(t_stage.get(up, &stage));
-    unsigned char* sb = static_cast<unsigned char*>(stage);
-    std::memcpy(sb, hd.data(), sizeof(InstDesc) * n);
-    std::memcpy(sb + desc_bytes + o_start, hp.start.data(), np * 8);
-    std::memcpy(sb + desc_bytes + o_inst, hp.inst.data(), np * 4);
-    std::memcpy(sb + desc_bytes + o_k, hp.k.data(), np * 4);
-    std::memcpy(sb + desc_bytes + o_j, hp.j.data(), np * 4);
-    CK(cudaMemcpyAsync(b->block, stage, up, cudaMemcpyHostToDevice, b->stream));
-    CK(cudaEventRecord(t_stage.done, b->stream));
-    rkr_status st = batch_fill(b);
+    rkr_status st = batch_layout(b);
+    if (st == RKR_OK) st = batch_upload(b);
+    if (st == RKR_OK) st = batch_fill(b);
     if (st != RKR_OK) {
         free_batch(b);
         return st;
@@ -1255,5 +1302,304 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
         return fail(RKR_ERR_CAPACITY, "sweep schedules need %lld ops", (long long)off);
     return result;
 }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Budget-axis sharding (config 5): one table split into contiguous budget
+// ranges, each shard filled by the persistent kernel, halos pushed by the
+// producing items straight into the next shard (peer memory across GPUs).
+// ---------------------------------------------------------------------------
+struct rkr_sharded {
+    int n = 0, L = 0, M = 0, pad = 0, width = 32;
+    std::vector<int32_t> lo, hi, dev;
+    std::vector<rkr_table*> shards;
+    std::vector<rkr_batch*> batches;   // one per device, shards in order
+    ShardView* dview = nullptr;        // on shard 0's device
+    int32_t* dops = nullptr;
+    int64_t dops_cap = 0;
+    int64_t* dout = nullptr;
+    int32_t* dstack = nullptr;
+};
+
+namespace {
+
+void free_sharded(rkr_sharded* sh) {
+    if (!sh) return;
+    for (rkr_batch* b : sh->batches) free_batch(b);
+    for (rkr_table* t : sh->shards) free_table(t);
+    if (!sh->shards.empty()) {
+        DeviceGuard dg(sh->dev[0]);
+        cudaDeviceSynchronize();
+        cudaFree(sh->dview);
+        cudaFree(sh->dops);
+        cudaFree(sh->dout);
+        cudaFree(sh->dstack);
+    }
+    delete sh;
+}
+
+rkr_status sharded_fill(rkr_sharded* sh) {
+    for (rkr_batch* b : sh->batches) {
+        DeviceGuard dg(b->device);
+        rkr_status st = batch_zero(b);
+        if (st) return st;
+    }
+    // every device's counters are zero before any shard can signal another
+    for (rkr_batch* b : sh->batches) {
+        DeviceGuard dg(b->device);
+        CK(cudaStreamSynchronize(b->stream));
+    }
+    for (rkr_batch* b : sh->batches) {
+        DeviceGuard dg(b->device);
+        rkr_status st = batch_launch(b);
+        if (st) return st;
+    }
+    return RKR_OK;
+}
+
+rkr_status sharded_create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max, int32_t n,
+                               const int32_t* devices, const rkr_exec* exec, rkr_sharded** out) {
+    if (!out) return fail(RKR_ERR_ARGUMENT, "null output handle");
+    *out = nullptr;
+    if (n < 1 || n > 64) return fail(RKR_ERR_ARGUMENT, "n_shards must be in [1, 64]");
+    if (m_max < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
+    HostMenu h;
+    rkr_status st = build_host_menu(menu, unit, h);
+    if (st) return st;
+    int64_t maxshift = 0;
+    for (int64_t p : h.pack_chg) maxshift = std::max(maxshift, p);
+    for (int32_t c = 1; c < h.L; ++c) maxshift = std::max(maxshift, h.act_u[c]);
+    const int32_t pad = (int32_t)round_up(std::min<int64_t>(maxshift, (int64_t)m_max + 1), 8);
+    const int32_t W = (m_max + 1) / n;
+    if (n > 1 && W < std::max(pad, 1))
+        return fail(RKR_ERR_INVALID,
+                    "too many shards: each must own at least the halo of %d budget slots", pad);
+    rkr_sharded* sh = new rkr_sharded();
+    sh->n = n;
+    sh->L = h.L;
+    sh->M = m_max;
+    sh->pad = pad;
+    const int R = persistent_choose_r(W - 1);
+    int32_t jo = 0;
+    for (int r = 0; r < n; ++r) {
+        const int32_t lo = r * W, hi = (r == n - 1) ? m_max + 1 : (r + 1) * W;
+        rkr_exec ex{};
+        if (exec) ex = *exec;
+        ex.kernel = RKR_KERNEL_PERSISTENT;
+        if (devices) ex.device = devices[r];
+        if (devices && exec && exec->stream) ex.stream = nullptr;  // per-device library streams
+        ShardSpec spec{lo, pad, jo};
+        rkr_table* t = nullptr;
+        st = prepare_table(menu, unit, hi - lo - 1, &ex, R, &t, &spec);
+        if (st) {
+            free_sharded(sh);
+            return st;
+        }
+        sh->shards.push_back(t);
+        sh->lo.push_back(lo);
+        sh->hi.push_back(hi);
+        sh->dev.push_back(t->device);
+        jo += t->plan.J;
+    }
+    sh->width = sh->shards[0]->width;
+    // peer access: producer shard -> next shard (halo stores), shard 0's
+    // device -> every shard (the cross-shard walk)
+    auto enable_peer = [&](int from, int to) -> rkr_status {
+        if (from == to) return RKR_OK;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, from, to);
+        if (!can) return fail(RKR_ERR_CUDA, "GPU %d cannot access GPU %d (no peer path)", from, to);
+        DeviceGuard dg(from);
+        cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+        cudaGetLastError();
+        return RKR_OK;
+    };
+    for (int r = 0; r < n && st == RKR_OK; ++r) {
+        if (r + 1 < n) st = enable_peer(sh->dev[r], sh->dev[r + 1]);
+        if (st == RKR_OK) st = enable_peer(sh->dev[0], sh->dev[r]);
+    }
+    if (st) {
+        free_sharded(sh);
+        return st;
+    }
+    // one batch per device (shards in chain order)
+    std::vector<int> devs;
+    for (int d : sh->dev)
+        if (std::find(devs.begin(), devs.end(), d) == devs.end()) devs.push_back(d);
+    std::vector<std::pair<int, int>> where(n);  // shard -> (batch, index)
+    for (int d : devs) {
+        rkr_batch* b = new rkr_batch();
+        b->device = d;
+        b->R = R;
+        b->owns_tables = false;
+        for (int r = 0; r < n; ++r)
+            if (sh->dev[r] == d) {
+                where[r] = {(int)sh->batches.size(), (int)b->tables.size()};
+                b->tables.push_back(sh->shards[r]);
+            }
+        sh->batches.push_back(b);
+        DeviceGuard dg(d);
+        st = batch_layout(b);
+        if (st) {
+            free_sharded(sh);
+            return st;
+        }
+    }
+    for (int r = 0; r + 1 < n; ++r) {
+        InstDesc& a = sh->batches[where[r].first]->hd[where[r].second];
+        InstDesc& b2 = sh->batches[where[r + 1].first]->hd[where[r + 1].second];
+        rkr_table* tn = sh->shards[r + 1];
+        const PersistPlan& pr = sh->shards[r]->plan;
+        const int32_t Wr = sh->hi[r] - sh->lo[r];
+        a.next_opt = tn->opt;
+        a.next_sr = tn->g.sr;
+        a.next_halo = b2.halo;
+        a.next_peer = sh->dev[r] != sh->dev[r + 1] ? 1 : 0;
+        b2.halo_need = pr.J - std::max(0, (Wr - pad) / pr.TM);  // producer tiles meeting the halo
+    }
+    for (rkr_batch* b : sh->batches) {
+        DeviceGuard dg(b->device);
+        st = batch_upload(b);
+        if (st) {
+            free_sharded(sh);
+            return st;
+        }
+    }
+    // walk views on shard 0's device
+    {
+        DeviceGuard dg(sh->dev[0]);
+        std::vector<ShardView> v(n);
+        for (int r = 0; r < n; ++r) {
+            rkr_table* t = sh->shards[r];
+            v[r] = ShardView{t->opt, t->arg, t->g.sr, t->g.sa, t->g.pad, sh->lo[r]};
+        }
+        CK(cudaMalloc(reinterpret_cast<void**>(&sh->dview), sizeof(ShardView) * n));
+        CK(cudaMemcpy(sh->dview, v.data(), sizeof(ShardView) * n, cudaMemcpyHostToDevice));
+        CK(cudaMalloc(reinterpret_cast<void**>(&sh->dout), 8 * sizeof(int64_t)));
+        CK(cudaMalloc(reinterpret_cast<void**>(&sh->dstack), sizeof(int4) * (2 * (size_t)h.L + 16)));
+    }
+    for (rkr_batch* b : sh->batches) {
+        DeviceGuard dg(b->device);
+        CK(cudaStreamSynchronize(b->stream));  // programs, pads, descriptors in place
+    }
+    st = sharded_fill(sh);
+    if (st) {
+        free_sharded(sh);
+        return st;
+    }
+    *out = sh;
+    return RKR_OK;
+}
+
+int owner(const rkr_sharded* sh, int32_t m) {
+    int q = 0;
+    while (q + 1 < sh->n && m >= sh->lo[q + 1]) ++q;
+    return q;
+}
+
+}  // namespace
+
+extern "C" {
+
+rkr_status rkr_sharded_create(const rkr_menu* menu, int64_t unit, int32_t m_max, int32_t n_shards,
+                              const int32_t* devices, const rkr_exec* exec, rkr_sharded** out) {
+    return sharded_create_impl(menu, unit, m_max, n_shards, devices, exec, out);
+}
+
+int32_t rkr_sharded_count(const rkr_sharded* sh) { return sh ? sh->n : 0; }
+
+rkr_status rkr_sharded_range(const rkr_sharded* sh, int32_t i, int32_t* m_lo, int32_t* m_hi) {
+    if (!sh || i < 0 || i >= sh->n || !m_lo || !m_hi) return fail(RKR_ERR_ARGUMENT, "bad shard");
+    *m_lo = sh->lo[i];
+    *m_hi = sh->hi[i];
+    return RKR_OK;
+}
+
+rkr_table* rkr_sharded_shard(rkr_sharded* sh, int32_t i) {
+    return (sh && i >= 0 && i < sh->n) ? sh->shards[i] : nullptr;
+}
+
+rkr_status rkr_sharded_refill(rkr_sharded* sh) {
+    if (!sh) return fail(RKR_ERR_ARGUMENT, "null sharded table");
+    return sharded_fill(sh);
+}
+
+rkr_status rkr_sharded_sync(const rkr_sharded* sh) {
+    if (!sh) return fail(RKR_ERR_ARGUMENT, "null sharded table");
+    for (rkr_batch* b : sh->batches) {
+        DeviceGuard dg(b->device);
+        CK(cudaStreamSynchronize(b->stream));
+    }
+    return RKR_OK;
+}
+
+rkr_status rkr_sharded_opt(const rkr_sharded* sh, int32_t s, int32_t t, int32_t m, int64_t* out) {
+    if (!sh || !out) return fail(RKR_ERR_ARGUMENT, "null argument");
+    if (m < 0) {
+        *out = RKR_INF_TIME;
+        return RKR_OK;
+    }
+    if (m > sh->M) m = sh->M;
+    rkr_status st = rkr_sharded_sync(sh);
+    if (st) return st;
+    const int q = owner(sh, m);
+    return rkr_table_opt(sh->shards[q], s, t, m - sh->lo[q], out);
+}
+
+rkr_status rkr_sharded_row(const rkr_sharded* sh, int32_t s, int32_t t, int64_t* opt, int8_t* kind,
+                           int32_t* value) {
+    if (!sh) return fail(RKR_ERR_ARGUMENT, "null sharded table");
+    rkr_status st = rkr_sharded_sync(sh);
+    if (st) return st;
+    for (int q = 0; q < sh->n; ++q) {
+        const int32_t lo = sh->lo[q];
+        st = rkr_table_row(sh->shards[q], s, t, opt ? opt + lo : nullptr, kind ? kind + lo : nullptr,
+                           value ? value + lo : nullptr);
+        if (st) return st;
+    }
+    return RKR_OK;
+}
+
+rkr_status rkr_sharded_backtrack(rkr_sharded* sh, int32_t s, int32_t t, int32_t m, rkr_op* ops,
+                                 int64_t cap, int64_t* n_ops) {
+    if (!sh || !n_ops || (cap > 0 && !ops)) return fail(RKR_ERR_ARGUMENT, "null argument");
+    if (s < 0 || t < s || t >= sh->L) return fail(RKR_ERR_ARGUMENT, "cell outside the table");
+    rkr_status st = rkr_sharded_sync(sh);
+    if (st) return st;
+    DeviceGuard dg(sh->dev[0]);
+    rkr_table* t0 = sh->shards[0];
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if (sh->dops_cap == 0) {
+            sh->dops_cap = std::max<int64_t>(4096, 8 * (int64_t)sh->L + 64);
+            CK(cudaMalloc(reinterpret_cast<void**>(&sh->dops), (size_t)sh->dops_cap * 12));
+        }
+        if (launch_walk_sharded(sh->dview, sh->n, t0->dm, sh->L, sh->M, sh->width, s, t, m,
+                                sh->dops, sh->dops_cap, sh->dstack, sh->dout, t0->stream))
+            return cuda_fail(cudaGetLastError(), "sharded walk launch");
+        int64_t res[4];
+        CK(cudaMemcpyAsync(res, sh->dout, sizeof res, cudaMemcpyDeviceToHost, t0->stream));
+        CK(cudaStreamSynchronize(t0->stream));
+        if (res[0] > sh->dops_cap) {
+            cudaFree(sh->dops);
+            sh->dops_cap = res[0];
+            CK(cudaMalloc(reinterpret_cast<void**>(&sh->dops), (size_t)sh->dops_cap * 12));
+            continue;
+        }
+        const int64_t ncopy = std::min(res[0], cap);
+        if (ncopy > 0) CK(cudaMemcpy(ops, sh->dops, (size_t)ncopy * 12, cudaMemcpyDeviceToHost));
+        *n_ops = res[0];
+        if (res[1] == 2)
+            return fail(RKR_ERR_INFEASIBLE, "no feasible schedule for blocks %lld..%lld",
+                        (long long)res[2], (long long)res[3]);
+        if (res[0] > cap) return fail(RKR_ERR_CAPACITY, "schedule needs %lld ops", (long long)res[0]);
+        return RKR_OK;
+    }
+    return fail(RKR_ERR_CUDA, "sharded walk did not converge");
+}
+
+void rkr_sharded_destroy(rkr_sharded* sh) { free_sharded(sh); }
 
 }  // extern "C"

@@ -43,11 +43,12 @@ struct DevMenu {
 // (row stride SR).  Arg rows are uint16, stride SA, no pad.
 struct Geometry {
     int32_t L;
-    int32_t M;
-    int32_t pad;       // >= every clamped shift (pack_chg, act_u), <= M + 1
+    int32_t M;         // last LOCAL budget slot (a shard holds global m_base .. m_base + M)
+    int32_t pad;       // >= every clamped shift (pack_chg, act_u), <= global M + 1
     int64_t sr;        // opt row stride (elements)
     int64_t sa;        // arg row stride (elements)
     int64_t rows;      // L(L+1)/2
+    int32_t m_base;    // global budget slot of local slot 0 (0 unless budget-sharded)
 };
 
 __host__ __device__ inline int64_t diag_off(int32_t L, int32_t k) {
@@ -64,6 +65,7 @@ __host__ __device__ inline int64_t row_id(int32_t L, int32_t s, int32_t t) {
 // items to fill the GPU, few enough that their rows stay in L2.
 struct PersistPlan {
     int32_t R = 1, TM = 256, J = 1, dj = 0, seg_cap = 0, lambda = 1;
+    int32_t j_offset = 0;        // global tile index of local tile 0 (sharded tables)
     int64_t total = 0;
     std::vector<int64_t> start;  // first item index of each (g, k) plan entry, in key order
     std::vector<int32_t> g, k;   // the entry's group and diagonal
@@ -101,6 +103,17 @@ struct InstDesc {
     ProgDev prog;
     void* stack;        // backtrack stack (int4[2L + 16])
     int64_t item_base;  // unused by the kernel (kept for diagnostics)
+    // Budget-axis sharding (config 5).  This shard's local slots [M+1-pad, M]
+    // are the halo of the next shard (slots [-pad, 0) of its rows): the item
+    // that computes them also stores them there (next_opt may be peer memory)
+    // and counts them in next_halo[k].  halo_need > 0: items whose reads
+    // reach below local slot 0 also wait for halo[k-1] >= (L-k+1) * halo_need.
+    void* next_opt;
+    int64_t next_sr;
+    int32_t* next_halo;
+    int32_t* halo;
+    int32_t halo_need;
+    int32_t next_peer;  // 1: next shard lives on another GPU (system-scope fences)
 };
 // The launch-wide item order: entry e covers items [start[e], start[e] +
 // L_inst - k[e]) = rows s = 0.. of (instance inst[e], diagonal k[e], tile
@@ -125,6 +138,16 @@ void merge_plans(const std::vector<const PersistPlan*>& plans, const std::vector
                  HostLaunchPlan& out);
 int launch_batch_walk(const InstDesc* d, const int32_t* m_at, const uint8_t* active, int n,
                       int width, int32_t* ops, int64_t cap, int64_t* out, void* stream);
+// A budget shard as the cross-shard walk reads it.
+struct ShardView {
+    const void* opt;
+    const uint16_t* arg;
+    int64_t sr, sa;
+    int32_t pad, lo;   // local slot 0 = global slot lo
+};
+int launch_walk_sharded(const ShardView* sv, int n, const DevMenu& dm, int L, int M, int width,
+                        int s, int t, int m, int32_t* ops, int64_t cap, int32_t* stack,
+                        int64_t* out, void* stream);
 int launch_batch_tops(const InstDesc* d, const int32_t* m_at, int n, int width, int64_t* out,
                       void* stream);
 int launch_batch_first_feasible(const InstDesc* d, int n, int width, int32_t* out, void* stream);

@@ -313,6 +313,77 @@ __global__ void batch_walk(const InstDesc* __restrict__ d, const int32_t* __rest
             ops + 3 * cap * (int64_t)i, cap, static_cast<int4*>(D.stack), out + 4 * i);
 }
 
+// K2 across budget shards (config 5): identical walk, each cell read from the
+// shard that owns its budget slot (peer memory when shards live on other GPUs).
+template <typename V>
+__global__ void walk_sharded(const ShardView* __restrict__ sv, int n_shards, DevMenu dm, int L,
+                             int M, int s0, int t0, int m0, int32_t* __restrict__ ops, int64_t cap,
+                             int4* __restrict__ stack, int64_t* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t n = 0;
+    int sp = 0;
+    int64_t status = 0, bad_s = -1, bad_t = -1;
+    auto emit = [&](int kd, int b, int x) {
+        if (n < cap) {
+            ops[3 * n] = kd;
+            ops[3 * n + 1] = b;
+            ops[3 * n + 2] = x;
+        }
+        ++n;
+    };
+    stack[sp++] = make_int4(0, s0, t0, m0);
+    while (sp > 0) {
+        const int4 e = stack[--sp];
+        if (e.x == 1) {
+            emit(3, e.y, e.z);
+            continue;
+        }
+        const int s = e.y, t = e.z, m = e.w;
+        bool inf = m < 0;
+        uint16_t code = 0;
+        if (!inf) {
+            const int mm = m > M ? M : m;
+            int q = 0;
+            while (q + 1 < n_shards && mm >= sv[q + 1].lo) ++q;
+            const ShardView& v = sv[q];
+            const int64_t rid = row_id(L, s, t);
+            inf = static_cast<const V*>(v.opt)[rid * v.sr + v.pad + (mm - v.lo)] >= Cost<V>::inf;
+            code = v.arg[rid * v.sa + (mm - v.lo)];
+        }
+        if (inf || code == 0) {
+            status = 2;
+            bad_s = s;
+            bad_t = t;
+            break;
+        }
+        if (!(code & kCutBit)) {
+            const int q = dm.blk_off[s] + code - 1;
+            const int val = dm.ids[q];
+            emit(2, s, val);
+            if (s == t) {
+                if (t == L - 1) emit(0, t, -1);
+                emit(3, s, val);
+            } else {
+                stack[sp++] = make_int4(1, s, val, 0);
+                stack[sp++] = make_int4(0, s + 1, t, m - (int)dm.chg_bt[q]);
+            }
+        } else {
+            const int c = code & 0x7fff;
+            emit(2, s, 0);
+            for (int j = s + 1; j < c; ++j) {
+                emit(2, j, 0);
+                emit(1, j, -1);
+            }
+            stack[sp++] = make_int4(0, s, c - 1, m);
+            stack[sp++] = make_int4(0, c, t, m - (int)dm.act_u[c]);
+        }
+    }
+    out[0] = n;
+    out[1] = status;
+    out[2] = bad_s;
+    out[3] = bad_t;
+}
+
 // Batched top cells: out[i] = opt(0, L-1, min(m_at[i], M)) as int64 (kInf64 when infinite).
 template <typename V>
 __global__ void batch_tops(const InstDesc* __restrict__ d, const int32_t* __restrict__ m_at, int n,
@@ -455,6 +526,18 @@ int launch_batch_walk(const InstDesc* d, const int32_t* m_at, const uint8_t* act
         batch_walk<uint32_t><<<blocks, 32, 0, st>>>(d, m_at, active, n, ops, cap, out);
     else
         batch_walk<int64_t><<<blocks, 32, 0, st>>>(d, m_at, active, n, ops, cap, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int launch_walk_sharded(const ShardView* sv, int n, const DevMenu& dm, int L, int M, int width,
+                        int s, int t, int m, int32_t* ops, int64_t cap, int32_t* stack,
+                        int64_t* out, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int4* stk = reinterpret_cast<int4*>(stack);
+    if (width == 32)
+        walk_sharded<uint32_t><<<1, 32, 0, st>>>(sv, n, dm, L, M, s, t, m, ops, cap, stk, out);
+    else
+        walk_sharded<int64_t><<<1, 32, 0, st>>>(sv, n, dm, L, M, s, t, m, ops, cap, stk, out);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

@@ -65,6 +65,16 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
+__device__ __forceinline__ int ld_relaxed_sys(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void fence_acq_rel_sys() {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -117,7 +127,7 @@ __global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> 
                                                     : dm.fwd_req[q] + seed;  // :141-143
             int64_t th = need > dm.bwd_req[q] ? need : dm.bwd_req[q];         // :144
             if (k > 0 && dm.pack_chg[q] > th) th = dm.pack_chg[q];            // :147
-            pr.thr[rid * ocap + i] = clampm(th, M);
+            pr.thr[rid * ocap + i] = clampm(th - g.m_base, M);  // local slots
         }
         if (k == 0) continue;
         const int64_t base = diag_cut_off(L, k) + (int64_t)s * k;
@@ -138,7 +148,7 @@ __global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> 
             p.y = (long long)(opt + row_id(L, c, t) * g.sr + g.pad - sh);
             pr.ptr[base + i] = p;
             pr.sweep[base + i] = sweep;
-            pr.gate[base + i] = clampm(gmax, M);
+            pr.gate[base + i] = clampm(gmax - g.m_base, M);
         }
     }
     // per saved option: clamped pack shift and pass time
@@ -303,13 +313,20 @@ __global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict
         // orders every thread's table reads after the acquire.  (Per-warp
         // polling/publishing was measured 7x slower: 8x the pollers and
         // atomics on the same flag lines, profiles/r01_persist.)
+        const bool need_halo = D.halo_need > 0 && j - pl.dj < 0;
         auto wait_diag = [&](int kk) {
             if (tid == 0) {
                 const int need = L - kk;
                 const int* row = done + (int64_t)kk * pl.J;
                 for (int jj = (j - pl.dj > 0 ? j - pl.dj : 0); jj <= j; ++jj)
                     while (ld_relaxed(row + jj) < need) __nanosleep(32);
-                fence_acq_rel();
+                if (need_halo) {  // slots below 0 come from the previous shard
+                    const int* h = D.halo + kk;
+                    while (ld_relaxed_sys(h) < need * D.halo_need) __nanosleep(64);
+                    fence_acq_rel_sys();
+                } else {
+                    fence_acq_rel();
+                }
             }
             __syncthreads();
         };
@@ -465,16 +482,28 @@ __global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict
         // ---- store (chain_dp.hpp:176-177) and publish ---------------------------
         V* orow = opt + rid * g.sr + g.pad;
         uint16_t* arow = arg + rid * g.sa;
+        // this tile's slots that are the next shard's halo: [W - pad, W)
+        const int W = M + 1;
+        const bool feeds_next = D.next_opt != nullptr && m0 + pl.TM > W - g.pad && m0 < W;
+        V* nrow = feeds_next ? static_cast<V*>(D.next_opt) + rid * D.next_sr + g.pad - W : nullptr;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int m = mb + NT * r;
             if (m <= M) {
                 orow[m] = best[r];
                 arow[m] = code[r];
+                if (feeds_next && m >= W - g.pad) nrow[m] = best[r];
             }
         }
         __syncthreads();
         if (tid == 0) {
+            if (feeds_next) {
+                if (D.next_peer)
+                    __threadfence_system();
+                else
+                    __threadfence();
+                atomicAdd(D.next_halo + k, 1);
+            }
             __threadfence();
             atomicAdd(done + (int64_t)k * pl.J + j, 1);
         }
@@ -631,7 +660,8 @@ void merge_plans(const std::vector<const PersistPlan*>& plans, const std::vector
     for (size_t i = 0; i < plans.size(); ++i) {
         const PersistPlan& p = *plans[i];
         for (size_t e = 0; e < p.start.size(); ++e)
-            es.push_back({(int64_t)p.lambda * p.g[e] + p.k[e], (int32_t)i, p.g[e], p.k[e]});
+            es.push_back({(int64_t)p.lambda * (p.g[e] + p.j_offset) + p.k[e], (int32_t)i, p.g[e],
+                          p.k[e]});
     }
     std::stable_sort(es.begin(), es.end(), [](const E& a, const E& b) {
         if (a.key != b.key) return a.key < b.key;

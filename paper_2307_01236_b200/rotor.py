@@ -123,6 +123,19 @@ def lib() -> ctypes.CDLL:
     L.rkr_batch_destroy.restype = None
     L.rkr_sweep.argtypes = [P(RkrMenu), P(i64), i32, i32, P(RkrExec), P(i32), P(i64), P(i64), P(i32),
                             P(i64), P(RkrOp), i64, P(i64)]
+    L.rkr_sharded_create.argtypes = [P(RkrMenu), i64, i32, i32, P(i32), P(RkrExec), P(p)]
+    L.rkr_sharded_count.argtypes = [p]
+    L.rkr_sharded_count.restype = i32
+    L.rkr_sharded_range.argtypes = [p, i32, P(i32), P(i32)]
+    L.rkr_sharded_shard.argtypes = [p, i32]
+    L.rkr_sharded_shard.restype = p
+    L.rkr_sharded_refill.argtypes = [p]
+    L.rkr_sharded_sync.argtypes = [p]
+    L.rkr_sharded_opt.argtypes = [p, i32, i32, i32, P(i64)]
+    L.rkr_sharded_row.argtypes = [p, i32, i32, p, p, p]
+    L.rkr_sharded_backtrack.argtypes = [p, i32, i32, i32, P(RkrOp), i64, P(i64)]
+    L.rkr_sharded_destroy.argtypes = [p]
+    L.rkr_sharded_destroy.restype = None
     L.rkr_backtrack_async.argtypes = [p, i32, i32, i32]
     L.rkr_backtrack_fetch.argtypes = [p, P(RkrOp), i64, P(i64)]
     _lib = L
@@ -538,3 +551,86 @@ def sweep(menu: Menu, budgets: Sequence[int], units: int, device: int = 0,
             raise RuntimeError("sweep makespan increased with budget")
         prev = r.opt_time
     return rows
+
+
+class ShardedTable:
+    """One DP table split along the budget axis into shards (rkr_sharded_*):
+    config 5.  Shards may live on one GPU or on several (peer memory)."""
+
+    def __init__(self, menu: Menu, unit: int, m_max: int, n_shards: int,
+                 devices: Optional[Sequence[int]] = None, width: str = "auto"):
+        self._lib = lib()
+        self._ms = menu.struct()
+        ex = _exec(devices[0] if devices else 0, width)
+        dv = (ctypes.c_int32 * n_shards)(*devices) if devices else None
+        self._h = ctypes.c_void_p()
+        _check(self._lib.rkr_sharded_create(ctypes.byref(self._ms), unit, m_max, n_shards, dv,
+                                            ctypes.byref(ex), ctypes.byref(self._h)))
+        self.menu = menu
+        self.L = menu.L
+        self.M = m_max
+
+    def ranges(self) -> List[Tuple[int, int]]:
+        out = []
+        for i in range(self._lib.rkr_sharded_count(self._h)):
+            lo, hi = ctypes.c_int32(), ctypes.c_int32()
+            _check(self._lib.rkr_sharded_range(self._h, i, ctypes.byref(lo), ctypes.byref(hi)))
+            out.append((lo.value, hi.value))
+        return out
+
+    def shard(self, i: int) -> DpTable:
+        return DpTable._borrow(self._lib.rkr_sharded_shard(self._h, i), self.menu, self)
+
+    def refill(self) -> None:
+        _check(self._lib.rkr_sharded_refill(self._h))
+
+    def sync(self) -> None:
+        _check(self._lib.rkr_sharded_sync(self._h))
+
+    def opt(self, s: int, t: int, m: int) -> int:
+        v = ctypes.c_int64()
+        _check(self._lib.rkr_sharded_opt(self._h, s, t, m, ctypes.byref(v)))
+        return v.value
+
+    def row(self, s: int, t: int):
+        W = self.M + 1
+        o = np.empty(W, np.int64)
+        k = np.empty(W, np.int8)
+        v = np.empty(W, np.int32)
+        _check(self._lib.rkr_sharded_row(self._h, s, t, o.ctypes.data, k.ctypes.data,
+                                         v.ctypes.data))
+        return o, k, v
+
+    def download(self):
+        L = self.L
+        rows = [self.row(s, t) for s in range(L) for t in range(s, L)]
+        return tuple(np.stack([r[i] for r in rows]) for i in range(3))
+
+    def backtrack(self, s: int, t: int, m: int) -> List[Tuple[int, int, int]]:
+        cap = 4096
+        while True:
+            buf = (RkrOp * cap)()
+            n = ctypes.c_int64()
+            st = self._lib.rkr_sharded_backtrack(self._h, s, t, m, buf, cap, ctypes.byref(n))
+            if st == RKR_ERR_CAPACITY:
+                cap = n.value
+                continue
+            _check(st)
+            return [(buf[i].kind, buf[i].block, buf[i].option) for i in range(n.value)]
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.rkr_sharded_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

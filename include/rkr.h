@@ -247,6 +247,28 @@ rkr_status rkr_sharded_backtrack(rkr_sharded* sharded, int32_t s, int32_t t, int
                                  rkr_op* ops, int64_t cap, int64_t* n_ops);
 void rkr_sharded_destroy(rkr_sharded* sharded);
 
+/* Multi-process budget sharding (one process per GPU, e.g. torchrun):
+ * rank r calls rkr_shard_create(..., n_shards, r, ...) (same menu/unit/m_max on
+ * every rank), exchanges rkr_shard_export's 64-byte CUDA IPC handle and 8
+ * int64 info words with its neighbours (any host channel: torch.distributed,
+ * MPI, files), links to shard r+1 with rkr_shard_link, then every fill is
+ * rkr_shard_zero on all ranks -> a host barrier -> rkr_shard_launch on all
+ * ranks.  The halo exchange happens inside the kernels over NVLink peer
+ * memory.  rkr_shard_backtrack walks the whole table from shard 0's process
+ * (handles/infos of all n shards, index 0 ignored); m is a global slot.
+ * Shard tables are ordinary rkr_table handles for accessors (local slots,
+ * rkr_shard_range gives [m_lo, m_hi)); destroy with rkr_table_destroy. */
+rkr_status rkr_shard_create(const rkr_menu* menu, int64_t unit, int32_t m_max, int32_t n_shards,
+                            int32_t shard, const rkr_exec* exec, rkr_table** out);
+rkr_status rkr_shard_range(const rkr_table* shard, int32_t* m_lo, int32_t* m_hi);
+rkr_status rkr_shard_export(const rkr_table* shard, void* ipc_handle, int64_t* info);
+rkr_status rkr_shard_link(rkr_table* shard, const void* next_ipc_handle, const int64_t* next_info);
+rkr_status rkr_shard_zero(rkr_table* shard);
+rkr_status rkr_shard_launch(rkr_table* shard);
+rkr_status rkr_shard_backtrack(rkr_table* shard0, int32_t n_shards, const void* const* ipc_handles,
+                               const int64_t* infos, int32_t s, int32_t t, int32_t m, rkr_op* ops,
+                               int64_t cap, int64_t* n_ops);
+
 /* Diagnostics (persistent kernel only): 6 globaltimer stamps per item of the
  * next fills {dequeued, diagonal k-2 met, bulk cuts done, diagonal k-1 met,
  * tail done, published}; item_k/item_j (nullable) receive each item's

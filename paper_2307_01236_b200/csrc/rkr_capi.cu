@@ -248,6 +248,9 @@ struct rkr_table {
     unsigned long long* trace = nullptr;
     int32_t bt_s = 0, bt_t = 0, bt_m = 0;
     InstDesc hdesc{};             // this table as the persistent kernel sees it
+    bool ipc = false;             // block from cudaMalloc (multi-process shard)
+    int32_t shard_lo = 0, shard_hi = 0;
+    std::vector<void*> ipc_open;  // peer blocks opened with cudaIpcOpenMemHandle
     InstDesc* ddesc = nullptr;    // device copy (single-table fills)
     LaunchPlan lplan{};           // single-table launch order (device pointers)
 
@@ -274,6 +277,15 @@ void free_table(rkr_table* t) {
     if (!t) return;
     DeviceGuard dg(t->device);
     if (t->trace) cudaFreeAsync(t->trace, t->stream);
+    for (void* p : t->ipc_open) {
+        cudaStreamSynchronize(t->stream);
+        cudaIpcCloseMemHandle(p);
+    }
+    if (t->block && t->ipc) {
+        cudaStreamSynchronize(t->stream);
+        cudaFree(t->block);
+        t->block = nullptr;
+    }
     if (t->block) cudaFreeAsync(t->block, t->stream);
     if (t->dops) cudaFreeAsync(t->dops, t->stream);
     delete t;
@@ -329,7 +341,11 @@ rkr_status alloc_and_upload(rkr_table* t) {
     t->menu_bytes = menu_bytes;
     t->block_bytes = bytes;
 
-    CK(cudaMallocAsync(&t->block, bytes, t->stream));
+    if (t->ipc) {  // exportable to other processes (cudaIpcGetMemHandle needs cudaMalloc)
+        CK(cudaMalloc(&t->block, bytes));
+    } else {
+        CK(cudaMallocAsync(&t->block, bytes, t->stream));
+    }
     unsigned char* b = static_cast<unsigned char*>(t->block);
     t->dm.blk_off = reinterpret_cast<const int32_t*>(b + off[0]);
     t->dm.fwd_req = reinterpret_cast<const int64_t*>(b + off[1]);
@@ -368,6 +384,7 @@ rkr_status alloc_and_upload(rkr_table* t) {
     pd.counter = reinterpret_cast<unsigned long long*>(b + off[21]);
     pd.done = reinterpret_cast<int32_t*>(b + off[21] + 8);
     pd.trace = nullptr;
+    t->hdesc.halo = pd.done + (size_t)t->g.L * t->plan.J;
     t->prog.ptr = b + off[22];
     t->prog.sweep = b + off[23];
     t->prog.gate = reinterpret_cast<int32_t*>(b + off[24]);
@@ -431,6 +448,7 @@ rkr_status enqueue_fill(rkr_table* t) {
 // common to all shards; j_offset = global tile index of local tile 0.
 struct ShardSpec {
     int32_t m_base, pad, j_offset;
+    bool ipc = false;
 };
 
 // Everything rkr_table_create does except the fill: validation and unit
@@ -479,6 +497,7 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
     if (spec) {
         t->g.pad = spec->pad;
         t->g.m_base = spec->m_base;
+        t->ipc = spec->ipc;
     }
     t->g.sr = round_up((int64_t)t->g.pad + m_max + 1, 32);
     t->g.sa = round_up((int64_t)m_max + 1, 64);
@@ -1601,5 +1620,200 @@ rkr_status rkr_sharded_backtrack(rkr_sharded* sh, int32_t s, int32_t t, int32_t 
 }
 
 void rkr_sharded_destroy(rkr_sharded* sh) { free_sharded(sh); }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Multi-process budget sharding: one process per GPU (torchrun), shard r on
+// rank r; the halo link to the next shard goes through CUDA IPC.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct ShardGeom {
+    int32_t pad, W, R, TM;
+    std::vector<int32_t> lo, hi, J, jo;
+};
+
+rkr_status shard_geometry(const rkr_menu* menu, int64_t unit, int32_t m_max, int32_t n,
+                          ShardGeom& sg) {
+    HostMenu h;
+    rkr_status st = build_host_menu(menu, unit, h);
+    if (st) return st;
+    int64_t maxshift = 0;
+    for (int64_t p : h.pack_chg) maxshift = std::max(maxshift, p);
+    for (int32_t c = 1; c < h.L; ++c) maxshift = std::max(maxshift, h.act_u[c]);
+    sg.pad = (int32_t)round_up(std::min<int64_t>(maxshift, (int64_t)m_max + 1), 8);
+    sg.W = (m_max + 1) / n;
+    if (n > 1 && sg.W < std::max(sg.pad, 1))
+        return fail(RKR_ERR_INVALID,
+                    "too many shards: each must own at least the halo of %d budget slots", sg.pad);
+    sg.R = persistent_choose_r(sg.W - 1);
+    sg.TM = 256 * sg.R;
+    int32_t jo = 0;
+    for (int r = 0; r < n; ++r) {
+        const int32_t lo = r * sg.W, hi = (r == n - 1) ? m_max + 1 : (r + 1) * sg.W;
+        sg.lo.push_back(lo);
+        sg.hi.push_back(hi);
+        sg.J.push_back((hi - lo + sg.TM - 1) / sg.TM);
+        sg.jo.push_back(jo);
+        jo += sg.J.back();
+    }
+    return RKR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rkr_status rkr_shard_create(const rkr_menu* menu, int64_t unit, int32_t m_max, int32_t n_shards,
+                            int32_t shard, const rkr_exec* exec, rkr_table** out) {
+    if (!out) return fail(RKR_ERR_ARGUMENT, "null output handle");
+    *out = nullptr;
+    if (n_shards < 1 || shard < 0 || shard >= n_shards)
+        return fail(RKR_ERR_ARGUMENT, "shard %d of %d", shard, n_shards);
+    if (m_max < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
+    ShardGeom sg;
+    rkr_status st = shard_geometry(menu, unit, m_max, n_shards, sg);
+    if (st) return st;
+    rkr_exec ex{};
+    if (exec) ex = *exec;
+    ex.kernel = RKR_KERNEL_PERSISTENT;
+    ShardSpec spec{sg.lo[shard], sg.pad, sg.jo[shard]};
+    spec.ipc = true;
+    rkr_table* t = nullptr;
+    st = prepare_table(menu, unit, sg.hi[shard] - sg.lo[shard] - 1, &ex, sg.R, &t, &spec);
+    if (st) return st;
+    t->shard_lo = sg.lo[shard];
+    t->shard_hi = sg.hi[shard];
+    if (shard > 0) {  // tiles of the previous shard that meet this shard's halo
+        const int32_t Wp = sg.hi[shard - 1] - sg.lo[shard - 1];
+        t->hdesc.halo_need = sg.J[shard - 1] - std::max(0, (Wp - sg.pad) / sg.TM);
+    }
+    DeviceGuard dg(t->device);
+    CK(cudaMemcpyAsync(t->ddesc, &t->hdesc, sizeof(InstDesc), cudaMemcpyHostToDevice, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    *out = t;
+    return RKR_OK;
+}
+
+rkr_status rkr_shard_range(const rkr_table* t, int32_t* m_lo, int32_t* m_hi) {
+    if (!t || !m_lo || !m_hi) return fail(RKR_ERR_ARGUMENT, "null argument");
+    *m_lo = t->shard_lo;
+    *m_hi = t->shard_hi;
+    return RKR_OK;
+}
+
+rkr_status rkr_shard_export(const rkr_table* t, void* ipc_handle, int64_t* info) {
+    if (!t || !ipc_handle || !info) return fail(RKR_ERR_ARGUMENT, "null argument");
+    if (!t->ipc) return fail(RKR_ERR_ARGUMENT, "table was not created by rkr_shard_create");
+    DeviceGuard dg(t->device);
+    cudaIpcMemHandle_t hnd;
+    CK(cudaIpcGetMemHandle(&hnd, t->block));
+    std::memcpy(ipc_handle, &hnd, sizeof hnd);
+    const unsigned char* b = static_cast<const unsigned char*>(t->block);
+    info[0] = static_cast<const unsigned char*>(t->opt) - b;
+    info[1] = t->g.sr;
+    info[2] = reinterpret_cast<const unsigned char*>(t->hdesc.halo) - b;
+    info[3] = reinterpret_cast<const unsigned char*>(t->arg) - b;
+    info[4] = t->g.sa;
+    info[5] = t->g.pad;
+    info[6] = t->shard_lo;
+    info[7] = t->shard_hi;
+    return RKR_OK;
+}
+
+rkr_status rkr_shard_link(rkr_table* t, const void* next_ipc_handle, const int64_t* next_info) {
+    if (!t || !next_ipc_handle || !next_info) return fail(RKR_ERR_ARGUMENT, "null argument");
+    DeviceGuard dg(t->device);
+    cudaIpcMemHandle_t hnd;
+    std::memcpy(&hnd, next_ipc_handle, sizeof hnd);
+    void* base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, hnd, cudaIpcMemLazyEnablePeerAccess));
+    t->ipc_open.push_back(base);
+    unsigned char* b = static_cast<unsigned char*>(base);
+    t->hdesc.next_opt = b + next_info[0];
+    t->hdesc.next_sr = next_info[1];
+    t->hdesc.next_halo = reinterpret_cast<int32_t*>(b + next_info[2]);
+    t->hdesc.next_peer = 1;  // another process: system-scope fences
+    CK(cudaMemcpyAsync(t->ddesc, &t->hdesc, sizeof(InstDesc), cudaMemcpyHostToDevice, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    return RKR_OK;
+}
+
+rkr_status rkr_shard_zero(rkr_table* t) {
+    if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
+    DeviceGuard dg(t->device);
+    CK(cudaMemsetAsync(t->pdev.counter, 0, t->state_bytes, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    return RKR_OK;
+}
+
+rkr_status rkr_shard_launch(rkr_table* t) {
+    if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
+    DeviceGuard dg(t->device);
+    if (launch_fill_batch(t->ddesc, &t->hdesc, t->lplan, t->width, t->plan.R,
+                          std::max(t->g.L - 1, 1), std::max(t->hm.max_opts, 1), t->pdev.counter,
+                          t->stream))
+        return cuda_fail(cudaGetLastError(), "shard launch");
+    return RKR_OK;
+}
+
+rkr_status rkr_shard_backtrack(rkr_table* t0, int32_t n, const void* const* ipc_handles,
+                               const int64_t* infos, int32_t s, int32_t t, int32_t m, rkr_op* ops,
+                               int64_t cap, int64_t* n_ops) {
+    if (!t0 || n < 1 || !n_ops || (n > 1 && (!ipc_handles || !infos)))
+        return fail(RKR_ERR_ARGUMENT, "null argument");
+    DeviceGuard dg(t0->device);
+    std::vector<ShardView> v(n);
+    const int32_t m_glob = (int32_t)(n > 1 ? infos[8 * (n - 1) + 7] : t0->shard_hi) - 1;
+    for (int r = 0; r < n; ++r) {
+        const int64_t* in = infos + 8 * r;
+        if (r == 0) {
+            v[0] = ShardView{t0->opt, t0->arg, t0->g.sr, t0->g.sa, t0->g.pad, t0->shard_lo};
+            continue;
+        }
+        cudaIpcMemHandle_t hnd;
+        std::memcpy(&hnd, ipc_handles[r], sizeof hnd);
+        void* base = nullptr;
+        CK(cudaIpcOpenMemHandle(&base, hnd, cudaIpcMemLazyEnablePeerAccess));
+        t0->ipc_open.push_back(base);
+        unsigned char* b = static_cast<unsigned char*>(base);
+        v[r] = ShardView{b + in[0], reinterpret_cast<const uint16_t*>(b + in[3]), in[1], in[4],
+                         (int32_t)in[5], (int32_t)in[6]};
+    }
+    ShardView* dv = nullptr;
+    int64_t* dout = nullptr;
+    int32_t* dops = nullptr;
+    int4* dstk = nullptr;
+    const int64_t dcap = std::max<int64_t>(cap, 16);
+    CK(cudaMalloc(reinterpret_cast<void**>(&dv), sizeof(ShardView) * n));
+    CK(cudaMalloc(reinterpret_cast<void**>(&dout), 64));
+    CK(cudaMalloc(reinterpret_cast<void**>(&dops), (size_t)dcap * 12));
+    CK(cudaMalloc(reinterpret_cast<void**>(&dstk), sizeof(int4) * (2 * (size_t)t0->g.L + 16)));
+    CK(cudaMemcpy(dv, v.data(), sizeof(ShardView) * n, cudaMemcpyHostToDevice));
+    rkr_status st = RKR_OK;
+    if (launch_walk_sharded(dv, n, t0->dm, t0->g.L, m_glob, t0->width, s, t, m,
+                            dops, dcap, reinterpret_cast<int32_t*>(dstk), dout, t0->stream))
+        st = cuda_fail(cudaGetLastError(), "shard walk launch");
+    int64_t res[4] = {0, 0, -1, -1};
+    if (st == RKR_OK) {
+        cudaError_t e = cudaMemcpyAsync(res, dout, sizeof res, cudaMemcpyDeviceToHost, t0->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(t0->stream);
+        if (e == cudaSuccess && std::min(res[0], cap) > 0)
+            e = cudaMemcpy(ops, dops, (size_t)std::min(res[0], cap) * 12, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) st = cuda_fail(e, "shard walk copy");
+    }
+    cudaFree(dv);
+    cudaFree(dout);
+    cudaFree(dops);
+    cudaFree(dstk);
+    if (st) return st;
+    *n_ops = res[0];
+    if (res[1] == 2)
+        return fail(RKR_ERR_INFEASIBLE, "no feasible schedule for blocks %lld..%lld",
+                    (long long)res[2], (long long)res[3]);
+    if (res[0] > cap) return fail(RKR_ERR_CAPACITY, "schedule needs %lld ops", (long long)res[0]);
+    return RKR_OK;
+}
 
 }  // extern "C"

@@ -618,7 +618,8 @@ void persistent_plan(const Geometry& g, int width, int R, PersistPlan& p) {
 }
 
 size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p) {
-    return 8 + (size_t)g.L * p.J * sizeof(int);
+    // counter | done flags [L x J] | halo counters [L] (budget shards)
+    return 8 + (size_t)g.L * p.J * sizeof(int) + (size_t)g.L * sizeof(int);
 }
 
 int64_t program_cut_entries(const Geometry& g) { return diag_cut_off(g.L, g.L); }

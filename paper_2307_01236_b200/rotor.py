@@ -136,6 +136,13 @@ def lib() -> ctypes.CDLL:
     L.rkr_sharded_backtrack.argtypes = [p, i32, i32, i32, P(RkrOp), i64, P(i64)]
     L.rkr_sharded_destroy.argtypes = [p]
     L.rkr_sharded_destroy.restype = None
+    L.rkr_shard_create.argtypes = [P(RkrMenu), i64, i32, i32, i32, P(RkrExec), P(p)]
+    L.rkr_shard_range.argtypes = [p, P(i32), P(i32)]
+    L.rkr_shard_export.argtypes = [p, p, P(i64)]
+    L.rkr_shard_link.argtypes = [p, p, P(i64)]
+    L.rkr_shard_zero.argtypes = [p]
+    L.rkr_shard_launch.argtypes = [p]
+    L.rkr_shard_backtrack.argtypes = [p, i32, P(p), P(i64), i32, i32, i32, P(RkrOp), i64, P(i64)]
     L.rkr_backtrack_async.argtypes = [p, i32, i32, i32]
     L.rkr_backtrack_fetch.argtypes = [p, P(RkrOp), i64, P(i64)]
     _lib = L
@@ -634,3 +641,84 @@ class ShardedTable:
 
     def __exit__(self, *a):
         self.close()
+
+
+class ProcessShard:
+    """Shard `rank` of a budget-sharded table built by one process per GPU
+    (rkr_shard_*); neighbours exchange CUDA IPC handles through any host
+    channel (bench.py and the tests use torch.distributed)."""
+
+    def __init__(self, menu: Menu, unit: int, m_max: int, n_shards: int, rank: int,
+                 device: int = 0, width: str = "auto"):
+        self._lib = lib()
+        self._ms = menu.struct()
+        ex = _exec(device, width)
+        self._h = ctypes.c_void_p()
+        _check(self._lib.rkr_shard_create(ctypes.byref(self._ms), unit, m_max, n_shards, rank,
+                                          ctypes.byref(ex), ctypes.byref(self._h)))
+        self.menu, self.n, self.rank, self.M = menu, n_shards, rank, m_max
+        self.table = DpTable._borrow(self._h.value, menu, self)
+
+    def range(self) -> Tuple[int, int]:
+        lo, hi = ctypes.c_int32(), ctypes.c_int32()
+        _check(self._lib.rkr_shard_range(self._h, ctypes.byref(lo), ctypes.byref(hi)))
+        return lo.value, hi.value
+
+    def export(self) -> Tuple[bytes, List[int]]:
+        hnd = ctypes.create_string_buffer(64)
+        info = (ctypes.c_int64 * 8)()
+        _check(self._lib.rkr_shard_export(self._h, hnd, info))
+        return hnd.raw, list(info)
+
+    def link(self, next_handle: bytes, next_info: Sequence[int]) -> None:
+        hnd = ctypes.create_string_buffer(next_handle, 64)
+        info = (ctypes.c_int64 * 8)(*next_info)
+        _check(self._lib.rkr_shard_link(self._h, hnd, info))
+
+    def zero(self) -> None:
+        _check(self._lib.rkr_shard_zero(self._h))
+
+    def launch(self) -> None:
+        _check(self._lib.rkr_shard_launch(self._h))
+
+    def sync(self) -> None:
+        self.table.sync()
+
+    def backtrack(self, handles: Sequence[bytes], infos: Sequence[Sequence[int]], s: int, t: int,
+                  m: int) -> List[Tuple[int, int, int]]:
+        n = len(handles)
+        bufs = [ctypes.create_string_buffer(h, 64) for h in handles]
+        hp = (ctypes.c_void_p * n)(*[ctypes.cast(b, ctypes.c_void_p) for b in bufs])
+        flat = (ctypes.c_int64 * (8 * n))(*[x for inf in infos for x in inf])
+        cap = 4096
+        while True:
+            buf = (RkrOp * cap)()
+            nn = ctypes.c_int64()
+            st = self._lib.rkr_shard_backtrack(self._h, n, hp, flat, s, t, m, buf, cap,
+                                               ctypes.byref(nn))
+            if st == RKR_ERR_CAPACITY:
+                cap = nn.value
+                continue
+            _check(st)
+            return [(buf[i].kind, buf[i].block, buf[i].option) for i in range(nn.value)]
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.rkr_table_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def link_process_shards(shard: "ProcessShard", all_gather) -> Tuple[List[bytes], List[List[int]]]:
+    """Exchange IPC handles with every rank (all_gather: obj -> list of objs)
+    and link this shard to the next one.  Returns all handles and infos."""
+    mine = shard.export()
+    everyone = all_gather(mine)
+    if shard.rank + 1 < shard.n:
+        shard.link(*everyone[shard.rank + 1])
+    return [e[0] for e in everyone], [e[1] for e in everyone]

@@ -759,7 +759,7 @@ rkr_status rkr_backtrack_fetch(rkr_table* t, rkr_op* ops, int64_t cap, int64_t* 
     if (!t->bt_pending) return fail(RKR_ERR_ARGUMENT, "no backtrack enqueued on this table");
     DeviceGuard dg(t->device);
     *n_ops = 0;
-    CK(cudaMemcpyAsync(t->hout, t->dout, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaMemcpyAsync(t->hout, t->dout, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, t->stream));
     CK(cudaStreamSynchronize(t->stream));
     int64_t n = t->hout[0];
     if (n > t->dops_cap) {  // grow the device op buffer and walk again (rare)
@@ -895,12 +895,17 @@ rkr_status rkr_solve_chain(const rkr_menu* menu, int64_t budget_bytes, int32_t u
     st = rkr_table_create(menu, unit, (int32_t)m_top, exec, &t);           // :262
     if (st) return st;
     const int L = t->g.L;
-    int64_t best;
-    st = rkr_table_opt(t, 0, L - 1, (int32_t)m_top, &best);                // :264
-    if (st) {
+    // one device walk from the top cell: its first read is opt(0, L-1, m_top)
+    // (chain_dp.hpp:264), returned with the ops, so a feasible solve needs a
+    // single host synchronisation
+    st = rkr_backtrack_async(t, 0, L - 1, (int32_t)m_top);
+    if (st == RKR_OK) st = rkr_backtrack_fetch(t, ops, cap, n_ops);
+    const int64_t best = t->hout[4];
+    if (st != RKR_OK && best < RKR_INF_TIME) {
         rkr_table_destroy(t);
         return st;
     }
+    if (best >= RKR_INF_TIME) *n_ops = 0;
     if (best >= RKR_INF_TIME) {                                            // :265-288
         int64_t capu = 0;
         for (int i = 0; i < L; ++i) {
@@ -928,7 +933,6 @@ rkr_status rkr_solve_chain(const rkr_menu* menu, int64_t budget_bytes, int32_t u
     *opt_time = best;
     *unit_out = unit;
     *m_top_out = (int32_t)m_top;
-    st = rkr_backtrack(t, 0, L - 1, (int32_t)m_top, ops, cap, n_ops);     // :293
     rkr_table_destroy(t);
     return st;
 }
@@ -1177,7 +1181,7 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
     }
     const int nb = (int)idx.size();
     std::vector<int64_t> top(nb, kInf64);
-    std::vector<int64_t> walk_out(4 * (size_t)nb, 0);
+    std::vector<int64_t> walk_out(8 * (size_t)nb, 0);
     int64_t cap_each = 0;
     std::vector<int32_t> walk_ops;
     std::vector<std::vector<rkr_op>> big(nb);  // schedules that overflowed the batch slots
@@ -1195,7 +1199,7 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
         DeviceGuard dg(b->device);
         // scratch: m_at[nb] | active[nb] | tops[nb] | walk out[4 nb] | ops[nb * cap]
         cap_each = std::max<int64_t>(256, 16 * (int64_t)L);
-        const size_t bytes = (size_t)nb * (4 + 1 + 8 + 32) + 64 + (size_t)nb * cap_each * 12;
+        const size_t bytes = (size_t)nb * (4 + 1 + 8 + 64) + 64 + (size_t)nb * cap_each * 12;
         void* scr = nullptr;
         cudaError_t e = cudaMallocAsync(&scr, bytes, b->stream);
         if (e != cudaSuccess) {
@@ -1205,7 +1209,7 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
         unsigned char* p = static_cast<unsigned char*>(scr);
         int64_t* d_tops = reinterpret_cast<int64_t*>(p);
         int64_t* d_wout = d_tops + nb;
-        int32_t* d_ops = reinterpret_cast<int32_t*>(d_wout + 4 * (size_t)nb);
+        int32_t* d_ops = reinterpret_cast<int32_t*>(d_wout + 8 * (size_t)nb);
         int32_t* d_mat = d_ops + (size_t)nb * cap_each * 3;
         uint8_t* d_act = reinterpret_cast<uint8_t*>(d_mat + nb);
         std::vector<uint8_t> act(nb, 1);
@@ -1220,7 +1224,7 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
             if (launch_batch_walk(b->ddesc, d_mat, d_act, nb, b->width, d_ops, cap_each, d_wout,
                                   b->stream))
                 return cuda_fail(cudaGetLastError(), "walk launch");
-            CK(cudaMemcpyAsync(walk_out.data(), d_wout, 32 * (size_t)nb, cudaMemcpyDeviceToHost,
+            CK(cudaMemcpyAsync(walk_out.data(), d_wout, 64 * (size_t)nb, cudaMemcpyDeviceToHost,
                                b->stream));
             walk_ops.resize((size_t)nb * cap_each * 3);
             CK(cudaMemcpyAsync(walk_ops.data(), d_ops, walk_ops.size() * 4, cudaMemcpyDeviceToHost,
@@ -1232,8 +1236,8 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
         cudaFreeAsync(scr, b->stream);
         // schedules longer than cap_each: walk those tables again on their own
         for (int q = 0; q < nb && st == RKR_OK; ++q) {
-            if (!act[q] || walk_out[4 * q] <= cap_each) continue;
-            big[q].resize((size_t)walk_out[4 * q]);
+            if (!act[q] || walk_out[8 * q] <= cap_each) continue;
+            big[q].resize((size_t)walk_out[8 * q]);
             int64_t nn = 0;
             st = rkr_backtrack(b->tables[q], 0, L - 1, mm[q], big[q].data(),
                                (int64_t)big[q].size(), &nn);
@@ -1299,8 +1303,8 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
             status[i] = RKR_OK;
             opt_time[i] = top[q];
             m_top_out[i] = mtop[i];
-            cnt = walk_out[4 * q];
-            if (walk_out[4 * q + 1] != 0) {
+            cnt = walk_out[8 * q];
+            if (walk_out[8 * q + 1] != 0) {
                 result = fail(RKR_ERR_INFEASIBLE, "schedule walk failed for budget %d", i);
                 cnt = 0;
             }

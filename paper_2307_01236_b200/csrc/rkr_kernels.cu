@@ -235,6 +235,14 @@ __device__ void walk(const Geometry& g, const DevMenu& dm, const V* __restrict__
         }
         ++n;
     };
+    {  // the root cell's value (solve_chain's opt_time / feasibility test)
+        int64_t top = kInf64;
+        if (m0 >= 0) {
+            const V v = opt[row_id(L, s0, t0) * g.sr + g.pad + (m0 > M ? M : m0)];
+            top = v >= Cost<V>::inf ? kInf64 : (int64_t)v;
+        }
+        out[4] = top;
+    }
     stack[sp++] = make_int4(0, s0, t0, m0);
     while (sp > 0) {
         const int4 e = stack[--sp];
@@ -286,17 +294,21 @@ __device__ void walk(const Geometry& g, const DevMenu& dm, const V* __restrict__
     out[3] = bad_t;
 }
 
+// The walk is a chain of dependent loads (code -> next cell); keeping the
+// stack in shared memory takes the stack's global round trips off that chain.
 template <typename V>
 __global__ void backtrack(Geometry g, DevMenu dm, const V* __restrict__ opt,
                           const uint16_t* __restrict__ arg, int s0, int t0, int m0,
                           int32_t* __restrict__ ops, int64_t cap, int4* __restrict__ stack,
-                          int64_t* __restrict__ out) {
+                          int64_t* __restrict__ out, int smem_stack) {
+    extern __shared__ int4 sstack[];
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    walk<V>(g, dm, opt, arg, s0, t0, m0, ops, cap, stack, out);
+    walk<V>(g, dm, opt, arg, s0, t0, m0, ops, cap, smem_stack ? sstack : stack, out);
 }
 
 // Batched K2: thread i walks table i from (0, L-1, m_at[i]) when active[i];
-// ops of table i go to ops + 3 * cap * i (at most cap of them).
+// ops of table i go to ops + 3 * cap * i (at most cap of them); its 8-word
+// result record to out + 8 * i.
 template <typename V>
 __global__ void batch_walk(const InstDesc* __restrict__ d, const int32_t* __restrict__ m_at,
                            const uint8_t* __restrict__ active, int n, int32_t* __restrict__ ops,
@@ -304,13 +316,13 @@ __global__ void batch_walk(const InstDesc* __restrict__ d, const int32_t* __rest
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     if (!active[i]) {
-        out[4 * i] = 0;
-        out[4 * i + 1] = -1;
+        out[8 * i] = 0;
+        out[8 * i + 1] = -1;
         return;
     }
     const InstDesc& D = d[i];
     walk<V>(D.g, D.dm, static_cast<const V*>(D.opt), D.arg, 0, D.g.L - 1, m_at[i],
-            ops + 3 * cap * (int64_t)i, cap, static_cast<int4*>(D.stack), out + 4 * i);
+            ops + 3 * cap * (int64_t)i, cap, static_cast<int4*>(D.stack), out + 8 * i);
 }
 
 // K2 across budget shards (config 5): identical walk, each cell read from the
@@ -509,12 +521,17 @@ int launch_backtrack(const LaunchCtx& c, int32_t s, int32_t t, int32_t m, int32_
                      int64_t cap, int32_t* dev_stack, int64_t* dev_out) {
     cudaStream_t st = static_cast<cudaStream_t>(c.stream);
     int4* stk = reinterpret_cast<int4*>(dev_stack);
+    const size_t sbytes = sizeof(int4) * (2 * (size_t)c.g.L + 16);
+    const int use_smem = sbytes <= 48 * 1024 ? 1 : 0;
+    const size_t dyn = use_smem ? sbytes : 0;
     if (c.width == 32)
-        backtrack<uint32_t><<<1, 32, 0, st>>>(c.g, c.dm, static_cast<const uint32_t*>(c.opt),
-                                              c.arg, s, t, m, dev_ops, cap, stk, dev_out);
+        backtrack<uint32_t><<<1, 32, dyn, st>>>(c.g, c.dm, static_cast<const uint32_t*>(c.opt),
+                                                c.arg, s, t, m, dev_ops, cap, stk, dev_out,
+                                                use_smem);
     else
-        backtrack<int64_t><<<1, 32, 0, st>>>(c.g, c.dm, static_cast<const int64_t*>(c.opt),
-                                             c.arg, s, t, m, dev_ops, cap, stk, dev_out);
+        backtrack<int64_t><<<1, 32, dyn, st>>>(c.g, c.dm, static_cast<const int64_t*>(c.opt),
+                                               c.arg, s, t, m, dev_ops, cap, stk, dev_out,
+                                               use_smem);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

@@ -238,8 +238,8 @@ __device__ inline Programs<V> programs_of(const ProgDev& q) {
 // SINGLE: one table whose descriptor travels as a kernel parameter (constant
 // bank); batches read their descriptors from global memory (measured 22%
 // slower per item on config 3, so the single-table path keeps the param).
-template <typename V, int NT, int R, int U, bool SINGLE>
-__global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict__ inst,
+template <typename V, int NT, int R, int U, bool SINGLE, int MINB>
+__global__ void __launch_bounds__(NT, MINB) fill_persistent(const InstDesc* __restrict__ inst,
                                                       const __grid_constant__ InstDesc d0,
                                                       LaunchPlan lp,
                                                       unsigned long long* __restrict__ counter,
@@ -273,10 +273,13 @@ __global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict
         const int j = __ldg(lp.j + ea);
         const int s = (int)(gidx - __ldg(lp.start + ea));
         const InstDesc& D = SINGLE ? d0 : inst[__ldg(lp.inst + ea)];
-        const Geometry g = D.g;
-        const DevMenu dm = D.dm;
-        const PlanDev pl = D.plan;
-        const Programs<V> pr = programs_of<V>(D.prog);
+        // references, not copies: fields are re-read from the parameter bank
+        // (single table) or L1 (batch) where used, instead of pinning ~40
+        // registers for the whole item
+        const Geometry& g = D.g;
+        const DevMenu& dm = D.dm;
+        const PlanDev& pl = D.plan;
+        const ProgDev& pq = D.prog;
         V* __restrict__ opt = static_cast<V*>(D.opt);
         uint16_t* __restrict__ arg = D.arg;
         int* __restrict__ done = pl.done;
@@ -291,16 +294,16 @@ __global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict
         const int o0 = __ldg(dm.blk_off + s);
         const int nopt = __ldg(dm.blk_off + s + 1) - o0;
         for (int i = tid; i < nopt; i += NT) {
-            sm.thr[i] = pr.thr[rid * pr.ocap + i];
-            sm.pc[i] = pr.pc[o0 + i];
-            sm.otot[i] = pr.otot[o0 + i];
+            sm.thr[i] = pq.thr[rid * pq.ocap + i];
+            sm.pc[i] = pq.pc[o0 + i];
+            sm.otot[i] = static_cast<const V*>(pq.otot)[o0 + i];
         }
         if (k > 0) {
             const int64_t base = diag_cut_off(L, k) + (int64_t)s * k;
             for (int i = tid; i < k; i += NT) {
-                sm.ptr[i] = pr.ptr[base + i];
-                sm.sweep[i] = pr.sweep[base + i];
-                sm.gate[i] = pr.gate[base + i];
+                sm.ptr[i] = static_cast<const longlong2*>(pq.ptr)[base + i];
+                sm.sweep[i] = static_cast<const V*>(pq.sweep)[base + i];
+                sm.gate[i] = pq.gate[base + i];
             }
         }
 
@@ -519,17 +522,22 @@ __global__ void __launch_bounds__(NT) fill_persistent(const InstDesc* __restrict
     }
 }
 
-template <typename V, int R, bool SINGLE>
+// Occupancy floor per R (registers: R=1 -> <=40, R=2 -> <=64, no spills);
+// measured on config 3 (profiles/r01_persist/variants.txt).
+template <int R>
+constexpr int kMinBlocks = R == 1 ? 6 : 4;
+
+template <typename V, int R, bool SINGLE, int U = 4, int MINB = kMinBlocks<R>>
 int launch_t(const InstDesc* dev_desc, const InstDesc& d0, const LaunchPlan& lp, int kcap, int ocap,
              unsigned long long* counter, cudaStream_t st) {
-    constexpr int NT = 256, U = 4;
+    constexpr int NT = 256;
     Caps c;
     c.TM = NT * R;
     c.seg_cap = 0;
     c.kcap = kcap > 0 ? kcap : 1;
     c.ocap = ocap > 0 ? ocap : 1;
     const size_t smem = psmem_bytes<V>(c);
-    auto kern = fill_persistent<V, NT, R, U, SINGLE>;
+    auto kern = fill_persistent<V, NT, R, U, SINGLE, MINB>;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
@@ -634,6 +642,21 @@ int launch_fill_batch(const InstDesc* dev_desc, const InstDesc* single, const La
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     InstDesc d0{};
     if (single) d0 = *single;
+    static const int variant = [] {
+        const char* e = getenv("RKR_VARIANT");  // tuning knob for measurements
+        return e ? atoi(e) : 0;
+    }();
+    if (single && width == 32 && variant) {
+        switch (variant * 10 + R) {
+            case 11: return launch_t<uint32_t, 1, true, 8, 6>(dev_desc, d0, lp, kcap, ocap, counter, st);
+            case 12: return launch_t<uint32_t, 2, true, 8, 4>(dev_desc, d0, lp, kcap, ocap, counter, st);
+            case 21: return launch_t<uint32_t, 1, true, 4, 1>(dev_desc, d0, lp, kcap, ocap, counter, st);
+            case 22: return launch_t<uint32_t, 2, true, 4, 5>(dev_desc, d0, lp, kcap, ocap, counter, st);
+            case 31: return launch_t<uint32_t, 1, true, 2, 8>(dev_desc, d0, lp, kcap, ocap, counter, st);
+            case 32: return launch_t<uint32_t, 2, true, 2, 5>(dev_desc, d0, lp, kcap, ocap, counter, st);
+            default: break;
+        }
+    }
     if (single) {
         if (width == 32)
             return R == 2 ? launch_t<uint32_t, 2, true>(dev_desc, d0, lp, kcap, ocap, counter, st)

@@ -269,6 +269,13 @@ rkr_status rkr_shard_backtrack(rkr_table* shard0, int32_t n_shards, const void* 
                                const int64_t* infos, int32_t s, int32_t t, int32_t m, rkr_op* ops,
                                int64_t cap, int64_t* n_ops);
 
+/* Schedule validation gate (host, exact): replays ops in the chain-level
+ * block-atomic memory model the DP optimises (the model of the reference's
+ * tests/test_helpers.hpp:249-322) and returns the makespan and the peak in
+ * bytes.  A malformed schedule gives RKR_ERR_INVALID and *bad_op = index. */
+rkr_status rkr_replay(const rkr_menu* menu, const rkr_op* ops, int64_t n_ops, int64_t* peak,
+                      int64_t* makespan, int64_t* bad_op);
+
 /* Diagnostics (persistent kernel only): 6 globaltimer stamps per item of the
  * next fills {dequeued, diagonal k-2 met, bulk cuts done, diagonal k-1 met,
  * tail done, published}; item_k/item_j (nullable) receive each item's

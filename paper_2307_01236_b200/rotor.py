@@ -143,6 +143,7 @@ def lib() -> ctypes.CDLL:
     L.rkr_shard_zero.argtypes = [p]
     L.rkr_shard_launch.argtypes = [p]
     L.rkr_shard_backtrack.argtypes = [p, i32, P(p), P(i64), i32, i32, i32, P(RkrOp), i64, P(i64)]
+    L.rkr_replay.argtypes = [P(RkrMenu), P(RkrOp), i64, P(i64), P(i64), P(i64)]
     L.rkr_backtrack_async.argtypes = [p, i32, i32, i32]
     L.rkr_backtrack_fetch.argtypes = [p, P(RkrOp), i64, P(i64)]
     _lib = L
@@ -509,6 +510,7 @@ class SweepRow:
     m_top: int = 0
     min_feasible: int = -1
     ops: List[Tuple[int, int, int]] = field(default_factory=list)
+    peak: int = -1        # replayed peak bytes (sweep() fills it)
 
 
 def sweep_raw(menu: Menu, budgets: Sequence[int], units: int, device: int = 0,
@@ -554,6 +556,13 @@ def sweep(menu: Menu, budgets: Sequence[int], units: int, device: int = 0,
     for r in rows:
         if not r.feasible:
             continue
+        # the validation gate of schedule_with_menu (pipeline.hpp:200-203):
+        # replay the schedule; it must reproduce the DP optimum and fit
+        r.peak, makespan = replay(menu, r.ops)
+        if makespan != r.opt_time:
+            raise RuntimeError(f"replayed makespan {makespan} != DP optimum {r.opt_time}")
+        if r.peak > r.budget:
+            raise RuntimeError(f"BudgetExceeded: peak {r.peak} > budget {r.budget}")
         if r.opt_time > prev:
             raise RuntimeError("sweep makespan increased with budget")
         prev = r.opt_time
@@ -722,3 +731,16 @@ def link_process_shards(shard: "ProcessShard", all_gather) -> Tuple[List[bytes],
     if shard.rank + 1 < shard.n:
         shard.link(*everyone[shard.rank + 1])
     return [e[0] for e in everyone], [e[1] for e in everyone]
+
+
+def replay(menu: Menu, ops: Sequence[Tuple[int, int, int]]) -> Tuple[int, int]:
+    """Schedule validation gate (rkr_replay): (peak bytes, makespan) of a
+    schedule in the DP's block-atomic memory model; raises ValidationError
+    on a malformed schedule."""
+    n = len(ops)
+    arr = (RkrOp * max(n, 1))(*[RkrOp(*o) for o in ops])
+    ms = menu.struct()
+    pk, tm, bad = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().rkr_replay(ctypes.byref(ms), arr, n, ctypes.byref(pk), ctypes.byref(tm),
+                            ctypes.byref(bad)))
+    return pk.value, tm.value

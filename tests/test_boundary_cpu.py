@@ -82,3 +82,20 @@ def test_cpp_test_binary_links():
     path = build_cpp_tests()
     out = subprocess.run(["ldd", path], capture_output=True, text=True).stdout
     assert "librkr.so" in out and "not found" not in out.split("librkr.so")[1].split("\n")[0]
+
+
+def test_replay_gate_matches_reference_model(orc, synthetic):
+    """rkr_replay (product, host) == the oracle's replay of the reference model."""
+    from paper_2307_01236_b200.menu import synthetic_menu
+
+    for e in synthetic["solves"]:
+        if e["status"] != 0:
+            continue
+        menu = synthetic_menu(e["L"], e["B"], e["M"], e["seed"], byte_scale=e["byte_scale"])
+        st, ops, *_ = orc.solve_chain(menu, e["budget"], e["units"])
+        assert rotor.replay(menu, ops) == (e["replay_peak"], e["replay_time"])
+    m = tiny_chain_menu()
+    good = [(2, 0, 1), (2, 1, 1), (0, 1, -1), (3, 1, 1), (3, 0, 1)]
+    assert rotor.replay(m, good) == orc.atomic_replay(m, good)
+    with pytest.raises(rotor.ValidationError, match="op 1"):
+        rotor.replay(m, [(2, 0, 1), (3, 0, 1)])

@@ -281,23 +281,36 @@ def b200_arm(args, world, rank, local):
     h2d = table.h2d_bytes()
     e2e_times = []
     n_ops = 0
-    # one C-ABI call per step: rkr_solve_chain with budget = M + a_0 bytes and
-    # units = budget gives unit 1 and m_top = M, i.e. exactly this table
-    chain = rotor.Chain.skeleton(L)
+    # one C-ABI call per step: rkr_solve_chain(host menu arrays) with
+    # budget = M + a_0 bytes and units = budget (unit 1, m_top = M, i.e.
+    # exactly this table); output buffers preallocated on the host, as a C
+    # caller would
+    import ctypes
+
+    lib = rotor.lib()
     budget = M + int(menu.act_sizes[0])
+    ms = menu.struct()
+    ex = rotor._exec(local, "auto")
+    cap = 1 << 16
+    obuf = (rotor.RkrOp * cap)()
+    n_, ot_, un_, mf_ = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    mt_ = ctypes.c_int32()
     for i in range(args.warmup + args.steps):
         with torch.cuda.stream(stream):
             flush.zero_()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        sol = rotor.solve_chain(chain, menu, budget, budget, device=local)
+        st = lib.rkr_solve_chain(ctypes.byref(ms), budget, budget, ctypes.byref(ex), obuf, cap,
+                                 ctypes.byref(n_), ctypes.byref(ot_), ctypes.byref(un_),
+                                 ctypes.byref(mt_), ctypes.byref(mf_))
         dt = time.perf_counter() - t0
-        topv, sched = sol.opt_time, sol.raw_ops
+        assert st == 0, lib.rkr_last_error()
         if i >= args.warmup:
             e2e_times.append(dt)
-        n_ops = len(sched)
-        assert topv == top and sched == ops
+    n_ops = n_.value
+    sched = [(obuf[q].kind, obuf[q].block, obuf[q].option) for q in range(n_ops)]
+    assert ot_.value == top and sched == ops
     e2e_s = max_over_ranks(sum(e2e_times))
     d2h = 8 + 2 + 32 + 12 * n_ops
 

@@ -262,6 +262,7 @@ struct rkr_table {
         c.arg = arg;
         c.width = width;
         c.max_opts = hm.max_opts;
+        c.nq = (int32_t)hm.ids.size();
         c.stream = stream;
         c.kernel = kernel;
         c.plan = pdev;

@@ -172,6 +172,7 @@ struct LaunchCtx {
     int32_t max_opts;   // max saved options per block
     void* stream;       // cudaStream_t
     int32_t kernel;     // 0 = persistent dataflow fill (K1p), 1 = one launch per diagonal (K1)
+    int32_t nq;         // saved options in the menu (walk staging)
     PlanDev plan;       // K1p schedule + state (device pointers)
     ProgDev prog;       // K1p cell programs
     size_t state_bytes; // bytes of counter + flags to zero before each fill

@@ -215,11 +215,30 @@ __global__ void init_pads(Geometry g, V* opt) {
     }
 }
 
+// Menu lookups the walk needs, straight from the device menu or from a
+// shared-memory copy (the walk is a chain of dependent loads, so every hop
+// it takes off global memory shortens it).  chg/act are cast to int exactly
+// as build_schedule_rec does (chain_dp.hpp:229, :240).
+struct GlobalMenuView {
+    const DevMenu* dm;
+    __device__ int blk(int s) const { return dm->blk_off[s]; }
+    __device__ int id(int q) const { return dm->ids[q]; }
+    __device__ int chg(int q) const { return (int)dm->chg_bt[q]; }
+    __device__ int act(int c) const { return (int)dm->act_u[c]; }
+};
+struct SharedMenuView {
+    const int32_t *b, *i, *g, *a;
+    __device__ int blk(int s) const { return b[s]; }
+    __device__ int id(int q) const { return i[q]; }
+    __device__ int chg(int q) const { return g[q]; }
+    __device__ int act(int c) const { return a[c]; }
+};
+
 // K2: build_schedule_rec as an explicit stack walk on one thread.  Stack
 // entries are int4 {type, s, t, m}: type 0 = cell to expand, type 1 =
-// pending BlockBwd(s, t = option).  Returns {n_ops, status, bad_s, bad_t}.
-template <typename V>
-__device__ void walk(const Geometry& g, const DevMenu& dm, const V* __restrict__ opt,
+// pending BlockBwd(s, t = option).  out = {n_ops, status, bad_s, bad_t, top}.
+template <typename V, typename MV>
+__device__ void walk(const Geometry& g, const MV& mv, const V* __restrict__ opt,
                      const uint16_t* __restrict__ arg, int s0, int t0, int m0,
                      int32_t* __restrict__ ops, int64_t cap, int4* __restrict__ stack,
                      int64_t* __restrict__ out) {
@@ -254,12 +273,10 @@ __device__ void walk(const Geometry& g, const DevMenu& dm, const V* __restrict__
         // table.opt(s,t,m) >= kInfTime -> InfeasibleBudget (chain_dp.hpp:213-215)
         const int64_t rid = row_id(L, s, t);
         bool inf = m < 0;
-        int mm = m > M ? M : m;
-        uint16_t code = 0;
-        if (!inf) {
-            inf = opt[rid * g.sr + g.pad + mm] >= Cost<V>::inf;
-            code = arg[rid * g.sa + mm];
-        }
+        const int mm = m > M ? M : (m < 0 ? 0 : m);
+        const V v = __ldcg(opt + rid * g.sr + g.pad + mm);   // both loads in flight together
+        const uint16_t code = __ldcg(arg + rid * g.sa + mm);
+        inf = inf || v >= Cost<V>::inf;
         if (inf || code == 0) {  // code 0 on a finite cell = "cell without a decision"
             status = 2;
             bad_s = s;
@@ -267,15 +284,15 @@ __device__ void walk(const Geometry& g, const DevMenu& dm, const V* __restrict__
             break;
         }
         if (!(code & kCutBit)) {  // Option (chain_dp.hpp:217-232)
-            const int q = dm.blk_off[s] + code - 1;
-            const int val = dm.ids[q];
+            const int q = mv.blk(s) + code - 1;
+            const int val = mv.id(q);
             emit(2, s, val);
             if (s == t) {
                 if (t == L - 1) emit(0, t, -1);
                 emit(3, s, val);
             } else {
                 stack[sp++] = make_int4(1, s, val, 0);
-                stack[sp++] = make_int4(0, s + 1, t, m - (int)dm.chg_bt[q]);
+                stack[sp++] = make_int4(0, s + 1, t, m - mv.chg(q));
             }
         } else {  // Cut (chain_dp.hpp:233-244)
             const int c = code & 0x7fff;
@@ -284,8 +301,8 @@ __device__ void walk(const Geometry& g, const DevMenu& dm, const V* __restrict__
                 emit(2, j, 0);
                 emit(1, j, -1);
             }
-            stack[sp++] = make_int4(0, s, c - 1, m);                  // left, after
-            stack[sp++] = make_int4(0, c, t, m - (int)dm.act_u[c]);   // right, first
+            stack[sp++] = make_int4(0, s, c - 1, m);             // left, after
+            stack[sp++] = make_int4(0, c, t, m - mv.act(c));     // right, first
         }
     }
     out[0] = n;
@@ -294,16 +311,38 @@ __device__ void walk(const Geometry& g, const DevMenu& dm, const V* __restrict__
     out[3] = bad_t;
 }
 
-// The walk is a chain of dependent loads (code -> next cell); keeping the
-// stack in shared memory takes the stack's global round trips off that chain.
+// The walk is a chain of dependent loads (code -> next cell); one warp stages
+// the stack and the menu lookups in shared memory when they fit, so each hop
+// costs one table read.
 template <typename V>
 __global__ void backtrack(Geometry g, DevMenu dm, const V* __restrict__ opt,
                           const uint16_t* __restrict__ arg, int s0, int t0, int m0,
                           int32_t* __restrict__ ops, int64_t cap, int4* __restrict__ stack,
-                          int64_t* __restrict__ out, int smem_stack) {
-    extern __shared__ int4 sstack[];
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    walk<V>(g, dm, opt, arg, s0, t0, m0, ops, cap, smem_stack ? sstack : stack, out);
+                          int64_t* __restrict__ out, int smem_mode, int nq) {
+    extern __shared__ int4 sbuf[];
+    if (blockIdx.x != 0) return;
+    const int L = g.L;
+    if (smem_mode) {
+        int4* sstack = sbuf;
+        int32_t* b = reinterpret_cast<int32_t*>(sstack + 2 * L + 16);
+        int32_t* a = b + L + 1;
+        int32_t* i = a + L + 1;
+        int32_t* gq = i + nq;
+        for (int x = threadIdx.x; x <= L; x += blockDim.x) {
+            b[x] = dm.blk_off[x];
+            a[x] = (int)dm.act_u[x];
+        }
+        for (int x = threadIdx.x; x < nq; x += blockDim.x) {
+            i[x] = dm.ids[x];
+            gq[x] = (int)dm.chg_bt[x];
+        }
+        __syncthreads();
+        if (threadIdx.x != 0) return;
+        walk<V>(g, SharedMenuView{b, i, gq, a}, opt, arg, s0, t0, m0, ops, cap, sstack, out);
+    } else {
+        if (threadIdx.x != 0) return;
+        walk<V>(g, GlobalMenuView{&dm}, opt, arg, s0, t0, m0, ops, cap, stack, out);
+    }
 }
 
 // Batched K2: thread i walks table i from (0, L-1, m_at[i]) when active[i];
@@ -321,8 +360,8 @@ __global__ void batch_walk(const InstDesc* __restrict__ d, const int32_t* __rest
         return;
     }
     const InstDesc& D = d[i];
-    walk<V>(D.g, D.dm, static_cast<const V*>(D.opt), D.arg, 0, D.g.L - 1, m_at[i],
-            ops + 3 * cap * (int64_t)i, cap, static_cast<int4*>(D.stack), out + 8 * i);
+    walk<V>(D.g, GlobalMenuView{&D.dm}, static_cast<const V*>(D.opt), D.arg, 0, D.g.L - 1,
+            m_at[i], ops + 3 * cap * (int64_t)i, cap, static_cast<int4*>(D.stack), out + 8 * i);
 }
 
 // K2 across budget shards (config 5): identical walk, each cell read from the
@@ -521,17 +560,19 @@ int launch_backtrack(const LaunchCtx& c, int32_t s, int32_t t, int32_t m, int32_
                      int64_t cap, int32_t* dev_stack, int64_t* dev_out) {
     cudaStream_t st = static_cast<cudaStream_t>(c.stream);
     int4* stk = reinterpret_cast<int4*>(dev_stack);
-    const size_t sbytes = sizeof(int4) * (2 * (size_t)c.g.L + 16);
+    const int nq = c.nq;
+    const size_t sbytes = sizeof(int4) * (2 * (size_t)c.g.L + 16) +
+                          4 * (2 * ((size_t)c.g.L + 1) + 2 * (size_t)nq);
     const int use_smem = sbytes <= 48 * 1024 ? 1 : 0;
     const size_t dyn = use_smem ? sbytes : 0;
     if (c.width == 32)
-        backtrack<uint32_t><<<1, 32, dyn, st>>>(c.g, c.dm, static_cast<const uint32_t*>(c.opt),
-                                                c.arg, s, t, m, dev_ops, cap, stk, dev_out,
-                                                use_smem);
+        backtrack<uint32_t><<<1, 128, dyn, st>>>(c.g, c.dm, static_cast<const uint32_t*>(c.opt),
+                                                 c.arg, s, t, m, dev_ops, cap, stk, dev_out,
+                                                 use_smem, nq);
     else
-        backtrack<int64_t><<<1, 32, dyn, st>>>(c.g, c.dm, static_cast<const int64_t*>(c.opt),
-                                               c.arg, s, t, m, dev_ops, cap, stk, dev_out,
-                                               use_smem);
+        backtrack<int64_t><<<1, 128, dyn, st>>>(c.g, c.dm, static_cast<const int64_t*>(c.opt),
+                                                c.arg, s, t, m, dev_ops, cap, stk, dev_out,
+                                                use_smem, nq);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

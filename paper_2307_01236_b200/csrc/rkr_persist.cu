@@ -99,14 +99,18 @@ __host__ __device__ inline int64_t diag_cut_off(int64_t L, int64_t k) {
 }
 
 // ---------------------------------------------------------------------------
-// prep_programs: one thread per cell (s, t).
+// prep_programs: one warp per cell (s, t); the option-0 sweep (:162) and the
+// `break` gate (:164) are prefix sum / prefix max over the cuts, done 32 cuts
+// at a time with warp shuffles.
 // ---------------------------------------------------------------------------
 template <typename V>
 __global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> pr) {
     const int ocap = pr.ocap;
     const int L = g.L, M = g.M;
-    for (int64_t rid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; rid < g.rows;
-         rid += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t rid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); rid < g.rows;
+         rid += warps) {
         int lo = 0, hi = L - 1;  // rid -> (k, s): rows are diagonal-major
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -121,7 +125,7 @@ __global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> 
         const bool seeded = t < L - 1;                              // chain_dp.hpp:126
         const int64_t seed = seeded ? 2 * dm.act_u[t + 1] : 0;      // chain_dp.hpp:127
         const int o0 = dm.blk_off[s], nopt = dm.blk_off[s + 1] - o0;
-        for (int i = 0; i < nopt; ++i) {
+        for (int i = lane; i < nopt; i += 32) {
             const int q = o0 + i;
             const int64_t need = (k == 0 && seeded) ? dm.fwd_req_pre[q] + dm.act_u[t + 1]
                                                     : dm.fwd_req[q] + seed;  // :141-143
@@ -131,24 +135,40 @@ __global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> 
         }
         if (k == 0) continue;
         const int64_t base = diag_cut_off(L, k) + (int64_t)s * k;
-        const int64_t gate0 = dm.fwd0_own[s] + seed;                          // :159
-        V sweep = 0;
-        int64_t gmax = gate0;
-        for (int i = 0; i < k; ++i) {
+        V carry_sum = 0;
+        long long carry_max = dm.fwd0_own[s] + seed;                          // :159
+        for (int i0 = 0; i0 < k; i0 += 32) {
+            const int i = i0 + lane;
             const int c = s + 1 + i;
-            sweep += (V)dm.tf0[c - 1];                                        // :162
-            if (c - 1 > s) {                                                  // :164
-                const int64_t gv = dm.fwd0_full[c - 1] + seed;
-                gmax = gv > gmax ? gv : gmax;
+            V inc = 0;
+            long long gv = LLONG_MIN;
+            if (i < k) {
+                inc = (V)dm.tf0[c - 1];
+                if (c - 1 > s) gv = dm.fwd0_full[c - 1] + seed;
             }
-            const int64_t a = dm.act_u[c];
-            const int sh = a > g.pad ? g.pad : (int)a;
-            longlong2 p;
-            p.x = (long long)(opt + row_id(L, s, c - 1) * g.sr + g.pad);
-            p.y = (long long)(opt + row_id(L, c, t) * g.sr + g.pad - sh);
-            pr.ptr[base + i] = p;
-            pr.sweep[base + i] = sweep;
-            pr.gate[base + i] = clampm(gmax - g.m_base, M);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {  // inclusive scans
+                const V y = __shfl_up_sync(0xffffffffu, inc, off);
+                const long long ym = __shfl_up_sync(0xffffffffu, gv, off);
+                if (lane >= off) {
+                    inc += y;
+                    gv = ym > gv ? ym : gv;
+                }
+            }
+            const V sweep = carry_sum + inc;
+            const long long gmax = gv > carry_max ? gv : carry_max;
+            if (i < k) {
+                const int64_t a = dm.act_u[c];
+                const int sh = a > g.pad ? g.pad : (int)a;
+                longlong2 p;
+                p.x = (long long)(opt + row_id(L, s, c - 1) * g.sr + g.pad);
+                p.y = (long long)(opt + row_id(L, c, t) * g.sr + g.pad - sh);
+                pr.ptr[base + i] = p;
+                pr.sweep[base + i] = sweep;
+                pr.gate[base + i] = clampm(gmax - g.m_base, M);
+            }
+            carry_sum = __shfl_sync(0xffffffffu, sweep, 31);
+            carry_max = __shfl_sync(0xffffffffu, gmax, 31);
         }
     }
     // per saved option: clamped pack shift and pass time
@@ -573,9 +593,10 @@ Programs<V> host_programs_of(const LaunchCtx& cx) {
 template <typename V>
 int prep_t(const LaunchCtx& cx) {
     cudaStream_t st = static_cast<cudaStream_t>(cx.stream);
-    int64_t n = cx.g.rows > cx.prog.nq ? cx.g.rows : cx.prog.nq;
+    // one warp per cell; the option pass strides over threads
+    const int64_t n = cx.g.rows * 32 > cx.prog.nq ? cx.g.rows * 32 : cx.prog.nq;
     int blocks = (int)((n + 127) / 128);
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
     prep_programs<V><<<blocks, 128, 0, st>>>(cx.g, cx.dm, static_cast<const V*>(cx.opt),
                                              host_programs_of<V>(cx));

@@ -65,6 +65,16 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ int ld_relaxed_sys(const int* p) {
     int v;
     asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -258,6 +268,8 @@ __device__ inline Programs<V> programs_of(const ProgDev& q) {
 // SINGLE: one table whose descriptor travels as a kernel parameter (constant
 // bank); batches read their descriptors from global memory (measured 22%
 // slower per item on config 3, so the single-table path keeps the param).
+__constant__ int pl_sleep_ns = 32;  // poll back-off (tuning knob, RKR_SLEEP_NS)
+
 template <typename V, int NT, int R, int U, bool SINGLE, int MINB>
 __global__ void __launch_bounds__(NT, MINB) fill_persistent(const InstDesc* __restrict__ inst,
                                                       const __grid_constant__ InstDesc d0,
@@ -342,7 +354,9 @@ __global__ void __launch_bounds__(NT, MINB) fill_persistent(const InstDesc* __re
                 const int need = L - kk;
                 const int* row = done + (int64_t)kk * pl.J;
                 for (int jj = (j - pl.dj > 0 ? j - pl.dj : 0); jj <= j; ++jj)
-                    while (ld_relaxed(row + jj) < need) __nanosleep(32);
+                    while (ld_relaxed(row + jj) < need) {
+                        if (pl_sleep_ns) __nanosleep(pl_sleep_ns);
+                    }
                 if (need_halo) {  // slots below 0 come from the previous shard
                     const int* h = D.halo + kk;
                     while (ld_relaxed_sys(h) < need * D.halo_need) __nanosleep(64);
@@ -527,8 +541,9 @@ __global__ void __launch_bounds__(NT, MINB) fill_persistent(const InstDesc* __re
                     __threadfence();
                 atomicAdd(D.next_halo + k, 1);
             }
-            __threadfence();
-            atomicAdd(done + (int64_t)k * pl.J + j, 1);
+            // release-add: orders this CTA's stores (made visible to thread 0
+            // by the barrier) before the count, without a separate fence
+            red_release_add(done + (int64_t)k * pl.J + j, 1);
         }
         if (pl.trace && tid == 0) {
             unsigned long long* tr = pl.trace + 6 * idx;  // per-table item index
@@ -663,6 +678,14 @@ int launch_fill_batch(const InstDesc* dev_desc, const InstDesc* single, const La
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     InstDesc d0{};
     if (single) d0 = *single;
+    static const bool sleep_set = [] {
+        if (const char* e = getenv("RKR_SLEEP_NS")) {
+            const int v = atoi(e);
+            cudaMemcpyToSymbol(pl_sleep_ns, &v, sizeof v);
+        }
+        return true;
+    }();
+    (void)sleep_set;
     static const int variant = [] {
         const char* e = getenv("RKR_VARIANT");  // tuning knob for measurements
         return e ? atoi(e) : 0;

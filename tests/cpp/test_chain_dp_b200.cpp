@@ -205,6 +205,34 @@ static void validation() {
     CHECK(threw);
 }
 
+static void b200_extensions() {
+    OptionMenu menu = tiny_menu();
+    Chain chain = tiny_chain();
+    // batched tables agree with single tables
+    b200::Batch batch({menu, menu}, {1, 1}, {64, 10});
+    CHECK(batch.size() == 2);
+    CHECK(batch.table(0).opt(0, 1, 64) == 39);
+    CHECK(batch.table(1).opt(0, 1, 10) == 49);
+    // the sweep: per-budget solve_chain results, sorted, monotone
+    auto rows = b200::sweep(chain, menu, {16, 14, 12, 16, 40}, 16);
+    CHECK(rows.size() == 4);
+    CHECK(rows[0].budget == 12 && !rows[0].feasible && rows[0].min_feasible > 0);
+    CHECK(rows[1].budget == 14 && rows[1].feasible);
+    CHECK(rows[3].feasible && rows[3].opt_time == 39);
+    ChainSolution one = solve_chain(chain, menu, 16, 16);
+    CHECK(rows[2].schedule.ops == one.schedule.ops);
+    // a 2-shard table equals the unsharded one
+    b200::ShardedTable sh(menu, 1, 64, 2);
+    DpTable whole(menu, 1, 64);
+    bool same = true;
+    for (int m = 0; m <= 64; ++m) same = same && sh.opt(0, 1, m) == whole.opt(0, 1, m);
+    CHECK(same);
+    std::vector<ScheduleOp> a, b;
+    sh.build_schedule(chain, 0, 1, 10, a);
+    build_schedule_rec(whole, menu, chain, 0, 1, 10, b);
+    CHECK(a == b);
+}
+
 int main() {
     quantization();
     single_block();
@@ -213,6 +241,7 @@ int main() {
     tiny_schedules();
     solve_and_min_feasible();
     validation();
+    b200_extensions();
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }

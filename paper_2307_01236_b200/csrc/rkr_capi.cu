@@ -376,7 +376,6 @@ rkr_status alloc_and_upload(rkr_table* t) {
     pd.TM = t->plan.TM;
     pd.J = t->plan.J;
     pd.dj = t->plan.dj;
-    pd.seg_cap = t->plan.seg_cap;
     pd.n_plan = (int32_t)np;
     pd.total = t->plan.total;
     pd.start = reinterpret_cast<const int64_t*>(b + off[12]);

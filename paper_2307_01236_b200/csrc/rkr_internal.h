@@ -64,14 +64,14 @@ __host__ __device__ inline int64_t row_id(int32_t L, int32_t s, int32_t t) {
 // tau = lambda * g + k), so about L / lambda groups are in flight: enough
 // items to fill the GPU, few enough that their rows stay in L2.
 struct PersistPlan {
-    int32_t R = 1, TM = 256, J = 1, dj = 0, seg_cap = 0, lambda = 1;
+    int32_t R = 1, TM = 256, J = 1, dj = 0, lambda = 1;
     int32_t j_offset = 0;        // global tile index of local tile 0 (sharded tables)
     int64_t total = 0;
     std::vector<int64_t> start;  // first item index of each (g, k) plan entry, in key order
     std::vector<int32_t> g, k;   // the entry's group and diagonal
 };
 struct PlanDev {
-    int32_t R, TM, J, dj, seg_cap, n_plan;
+    int32_t R, TM, J, dj, n_plan;
     int64_t total;
     const int64_t* start;
     const int32_t* g;

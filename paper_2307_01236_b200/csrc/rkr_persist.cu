@@ -16,16 +16,19 @@
 // table -- the option thresholds of chain_dp.hpp:141-147, the row addresses
 // of every cut, the option-0 sweep prefix sums (:162) and the `break` gate
 // (:164) as a prefix maximum -- is computed once per table by prep_programs
-// and copied into shared memory by each item before it waits on its
-// dependencies, so the critical path of an item is: wait -> option window ->
-// candidate loop -> store -> publish.
+// and copied into shared memory by each item before it waits.
 //
-// Candidate loop.  Each lane first counts the cuts its budget slot admits
-// (binary search on the monotone gate), then runs the cut loop in batches of
-// U iterations whose 2*U*R loads are issued before any is consumed.  The
-// option window (row (s+1, t) at shifts m - pack_chg) is staged in shared
-// memory.  Tie-break: options in menu order, then cuts ascending, strict '<'
-// -- the reference's first minimum (chain_dp.hpp:139-174).
+// Two phases per item.  Only the options (row (s+1, t)), cut c = s+1 (right
+// operand (s+1, t)) and cut c = t (left operand (s, t-1)) read diagonal k-1.
+// The item first waits for diagonal k-2 and runs the other cuts ("bulk":
+// each lane counts the cuts its slot admits by binary search on the
+// monotone gate, then loads them in batches of U iterations so 2*U*R loads
+// are in flight), then waits for k-1 and runs the short "tail": options
+// through L1 (ld.ca; the acquire fence invalidated L1) and the two remaining
+// cuts, merged with a lexicographic (value, code) minimum.  Completion is
+// published with a release reduction (red.release.gpu).
+// Tie-break: options in menu order, then cuts ascending -- the reference's
+// first minimum (chain_dp.hpp:139-174).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -201,12 +204,11 @@ struct PSmem {
     V* otot;          // [ocap]
     int32_t* thr;     // [ocap]
     int32_t* pc;      // [ocap]
-    V* seg;           // [seg_cap + TM]
     long long* item;  // [1]
 };
 
 struct Caps {
-    int32_t kcap, ocap, seg_cap, TM;
+    int32_t kcap, ocap, TM;
 };
 
 template <typename V>
@@ -219,8 +221,6 @@ __host__ __device__ inline size_t psmem_bytes(const Caps& c) {
     b += (size_t)c.ocap * sizeof(V);
     b = (b + 15) & ~size_t(15);
     b += (size_t)c.ocap * 8;
-    b = (b + 15) & ~size_t(15);
-    b += (size_t)(c.seg_cap > 0 ? c.seg_cap + c.TM : 0) * sizeof(V);
     b = (b + 15) & ~size_t(15);
     return b + 16;
 }
@@ -243,9 +243,6 @@ __device__ inline PSmem<V> pcarve(unsigned char* p, const Caps& c) {
     s.thr = reinterpret_cast<int32_t*>(p + b);
     s.pc = s.thr + c.ocap;
     b += (size_t)c.ocap * 8;
-    b = (b + 15) & ~size_t(15);
-    s.seg = reinterpret_cast<V*>(p + b);
-    b += (size_t)(c.seg_cap > 0 ? c.seg_cap + c.TM : 0) * sizeof(V);
     b = (b + 15) & ~size_t(15);
     s.item = reinterpret_cast<long long*>(p + b);
     return s;
@@ -568,7 +565,6 @@ int launch_t(const InstDesc* dev_desc, const InstDesc& d0, const LaunchPlan& lp,
     constexpr int NT = 256;
     Caps c;
     c.TM = NT * R;
-    c.seg_cap = 0;
     c.kcap = kcap > 0 ? kcap : 1;
     c.ocap = ocap > 0 ? ocap : 1;
     const size_t smem = psmem_bytes<V>(c);
@@ -633,7 +629,6 @@ void persistent_plan(const Geometry& g, int width, int R, PersistPlan& p) {
     p.TM = 256 * p.R;
     p.J = (g.M + 1 + p.TM - 1) / p.TM;
     p.dj = (g.pad + p.TM - 1) / p.TM;
-    p.seg_cap = 0;  // option window read through L1 (ld.ca) after the acquire fence
     // Order key lambda*j + k.  lambda = 1 is the 2D (tile, diagonal)
     // wavefront: critical path L + J - 1 item steps, every tile in flight.
     // lambda = 0 is diagonal-major (critical path L steps) and wins when the

@@ -64,14 +64,23 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfg_idx):
+def ncu_traffic(cfg_idx, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one fill launch of
+    `kernel` (profiles/ncu_traffic.json, from an ncu capture of this bench)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(f"config{cfg_idx}", {}).get("dram_bytes_per_fill")
+        return d.get(f"config{cfg_idx}", {}).get(kernel, {}).get("dram_bytes_per_fill")
     except Exception:
         return None
+
+
+FILL_KERNELS = {
+    "tiles": "fill_tiles (K1t: one co-resident launch, one CTA per budget tile)",
+    "queue": "fill_persistent (K1p: one persistent launch, dataflow work queue)",
+    "diagonal": "fill_diag (K1: one launch per anti-diagonal)",
+}
 
 
 class ClockSampler:
@@ -320,7 +329,8 @@ def b200_arm(args, world, rank, local):
     peak, peak_src = measured_peak()
     ab = alg_bytes(L, M)
     achieved = ab / fill_mean_s / 1e9
-    traffic = ncu_traffic(args.config)
+    kern = table.kernel()
+    traffic = ncu_traffic(args.config, kern)
     line = {
         "metric": "DP cell-updates/sec (rk-Rotor chain DP, full table fill + backtrack)",
         "value": world * cells * args.steps / tot_s,
@@ -349,10 +359,11 @@ def b200_arm(args, world, rank, local):
                 "ms_per_step": 1e3 * e2e_s / args.steps,
                 "path": "rkr_solve_chain(host menu arrays): quantize, H2D, fill, top cell, "
                         "device backtrack, D2H of the schedule"},
-        "gpu_launches": args.steps * (L + 2),
+        # per step: the fill (one launch, or L for the per-diagonal kernel) + the walk
+        "gpu_launches": args.steps * ((L if kern == "diagonal" else 1) + 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "fill_diag (all L diagonal launches of one fill)",
+                     "kernel": FILL_KERNELS[kern],
                      "alg_bytes_per_fill": ab, "fill_ms": 1e3 * fill_mean_s,
                      "peak_source": peak_src},
         "clocks": sampler.summary(),

@@ -85,8 +85,12 @@ typedef enum {
 } rkr_width;
 
 typedef enum {
-    RKR_KERNEL_PERSISTENT = 0, /* one persistent, dataflow-scheduled launch per fill (default) */
-    RKR_KERNEL_DIAGONAL = 1    /* one launch per anti-diagonal (the simple wavefront) */
+    RKR_KERNEL_PERSISTENT = 0, /* one persistent launch per fill (default): budget tiles
+                                  when they fit one CTA per SM, else the work queue */
+    RKR_KERNEL_DIAGONAL = 1,   /* one launch per anti-diagonal (the simple wavefront) */
+    RKR_KERNEL_QUEUE = 2,      /* persistent, dataflow-queue scheduled (row-segment items) */
+    RKR_KERNEL_TILES = 3       /* persistent, one CTA per budget tile (RKR_ERR_INVALID if
+                                  the table does not fit) */
 } rkr_kernel;
 
 /* Execution settings; pass NULL for defaults (device 0, the library's shared
@@ -127,6 +131,9 @@ int64_t rkr_table_act_units(const rkr_table* table, int32_t i);
 /* 32 or 64: the cost width the fill ran in (bookkeeping only; every value
  * leaving the library is int64 and bit-exact). */
 int32_t rkr_table_width(const rkr_table* table);
+/* The fill kernel the table runs: RKR_KERNEL_TILES, RKR_KERNEL_QUEUE or
+ * RKR_KERNEL_DIAGONAL (RKR_KERNEL_PERSISTENT resolves to one of the first two). */
+int32_t rkr_table_kernel(const rkr_table* table);
 /* DpTable::max_candidates_per_cell / worst_cell_allowance (:118-120),
  * computed in closed form from the menu (the device fill visits exactly the
  * reference's candidate sequence). */

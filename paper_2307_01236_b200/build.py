@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librkr.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("rkr_kernels.cu", "rkr_persist.cu", "rkr_capi.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("rkr_kernels.cu", "rkr_persist.cu", "rkr_tiles.cu", "rkr_capi.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "rkr_internal.h"), os.path.join(ROOT, "include", "rkr.h")]
 
 NVCC_FLAGS = [

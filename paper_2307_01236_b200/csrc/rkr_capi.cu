@@ -240,7 +240,10 @@ struct rkr_table {
     int32_t* dops = nullptr;      // device op buffer (separate, grows on demand)
     int64_t dops_cap = 0;
     bool bt_pending = false;
-    int kernel = 0;
+    int kernel = 0;               // RKR_KERNEL_PERSISTENT or RKR_KERNEL_DIAGONAL
+    bool tiles = false;           // persistent fill by budget tiles (K1t) instead of the queue (K1p)
+    TilePlan tplan;
+    int32_t flag_cols = 0;        // done-flag columns: max(K1p tiles J, K1t tiles T)
     PersistPlan plan;
     PlanDev pdev{};
     ProgDev prog{};
@@ -328,11 +331,15 @@ rkr_status alloc_and_upload(rkr_table* t) {
     const size_t vbytes = t->width == 32 ? 4 : 8;
     take(((size_t)t->g.rows * t->g.sr + kOptSlack) * vbytes);  // 19 opt
     take((size_t)t->g.rows * t->g.sa * 2);       // 20 arg
-    t->state_bytes = persistent_state_bytes(t->g, t->plan);
+    // counter | done flags [L x flag_cols] (K1p tiles or K1t tiles) | halo [L]
+    t->flag_cols = std::max<int32_t>(t->plan.J, t->tplan.T);
+    t->state_bytes = 8 + ((size_t)t->g.L * t->flag_cols + t->g.L) * sizeof(int);
     take(t->state_bytes);                        // 21 K1p counter + done flags
     const bool progs = t->kernel == RKR_KERNEL_PERSISTENT;
     const size_t nc = progs ? (size_t)program_cut_entries(t->g) : 0;
-    const size_t ocap = std::max<int32_t>(h.max_opts, 1);
+    // thr row stride; K1t copies thr rows with bulk copies and reads whole batches of 8
+    const size_t ocap = t->tiles ? round_up(std::max<int32_t>(h.max_opts, 1), 8)
+                                 : std::max<int32_t>(h.max_opts, 1);
     take(nc * 16);                               // 22 program ptr
     take(nc * vbytes);                           // 23 program sweep
     take(nc * 4);                                // 24 program gate
@@ -384,7 +391,8 @@ rkr_status alloc_and_upload(rkr_table* t) {
     pd.counter = reinterpret_cast<unsigned long long*>(b + off[21]);
     pd.done = reinterpret_cast<int32_t*>(b + off[21] + 8);
     pd.trace = nullptr;
-    t->hdesc.halo = pd.done + (size_t)t->g.L * t->plan.J;
+    t->hdesc.halo = pd.done + (size_t)t->g.L * t->flag_cols;
+    t->tplan.done = pd.done;
     t->prog.ptr = b + off[22];
     t->prog.sweep = b + off[23];
     t->prog.gate = reinterpret_cast<int32_t*>(b + off[24]);
@@ -393,6 +401,7 @@ rkr_status alloc_and_upload(rkr_table* t) {
     t->prog.otot = b + off[27];
     t->prog.nq = (int64_t)h.ids.size();
     t->prog.ocap = (int32_t)ocap;
+    t->prog.tiles = t->tiles ? 1 : 0;
     t->hdesc.g = t->g;
     t->hdesc.dm = t->dm;
     t->hdesc.opt = t->opt;
@@ -437,6 +446,11 @@ rkr_status enqueue_fill(rkr_table* t) {
         return RKR_OK;
     }
     CK(cudaMemsetAsync(t->pdev.counter, 0, t->state_bytes, t->stream));
+    if (t->tiles) {
+        if (launch_fill_tiles(t->hdesc, t->tplan, t->width, t->stream))
+            return cuda_fail(cudaGetLastError(), "tile fill launch");
+        return RKR_OK;
+    }
     if (launch_fill_batch(t->ddesc, &t->hdesc, t->lplan, t->width, t->plan.R,
                           std::max(t->g.L - 1, 1), std::max(t->hm.max_opts, 1), t->pdev.counter,
                           t->stream))
@@ -468,7 +482,12 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
     t->unit = unit;
     t->device = exec ? exec->device : 0;
     const int want = exec ? exec->width : RKR_WIDTH_AUTO;
-    t->kernel = exec ? exec->kernel : RKR_KERNEL_PERSISTENT;
+    const int kreq = exec ? exec->kernel : RKR_KERNEL_PERSISTENT;
+    if (kreq < RKR_KERNEL_PERSISTENT || kreq > RKR_KERNEL_TILES) {
+        delete t;
+        return fail(RKR_ERR_ARGUMENT, "unknown kernel %d", kreq);
+    }
+    t->kernel = kreq == RKR_KERNEL_DIAGONAL ? RKR_KERNEL_DIAGONAL : RKR_KERNEL_PERSISTENT;
     t->width = (want != RKR_WIDTH_64 && t->hm.bounded32) ? 32 : 64;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= t->device || t->device < 0) {
@@ -505,6 +524,20 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
     if (t->kernel == RKR_KERNEL_PERSISTENT) {
         persistent_plan(t->g, t->width, R > 0 ? R : persistent_choose_r(m_max), t->plan);
         if (spec) t->plan.j_offset = spec->j_offset;
+        // budget tiles (K1t) for single, unsharded tables that fit one CTA
+        // per tile on the device; the queue (K1p) otherwise or on request
+        if (!spec && kreq != RKR_KERNEL_QUEUE) {
+            int sms = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
+            t->tiles = tile_plan(t->g, t->width, sms, (int64_t)h.ids.size(),
+                                 (int)round_up(std::max<int32_t>(h.max_opts, 1), 8), t->tplan) == 1;
+        }
+        if (kreq == RKR_KERNEL_TILES && !t->tiles) {
+            delete t;
+            return fail(RKR_ERR_INVALID, "kernel TILES: %d budget slots x %d rows do not fit "
+                        "one co-resident tile per SM", m_max + 1, (int)t->g.L);
+        }
+        if (!t->tiles) t->tplan = TilePlan{};
     }
     st = alloc_and_upload(t);
     if (st == RKR_OK && launch_init_pads(t->ctx())) st = cuda_fail(cudaGetLastError(), "pad launch");
@@ -612,6 +645,11 @@ int32_t rkr_table_length(const rkr_table* t) { return t ? t->g.L : 0; }
 int64_t rkr_table_unit(const rkr_table* t) { return t ? t->unit : 0; }
 int32_t rkr_table_m_max(const rkr_table* t) { return t ? t->g.M : -1; }
 int32_t rkr_table_width(const rkr_table* t) { return t ? t->width : 0; }
+int32_t rkr_table_kernel(const rkr_table* t) {
+    if (!t) return -1;
+    if (t->kernel == RKR_KERNEL_DIAGONAL) return RKR_KERNEL_DIAGONAL;
+    return t->tiles ? RKR_KERNEL_TILES : RKR_KERNEL_QUEUE;
+}
 int64_t rkr_table_act_units(const rkr_table* t, int32_t i) {
     return (t && i >= 0 && i <= t->g.L) ? t->hm.act_u[i] : 0;
 }
@@ -804,26 +842,31 @@ rkr_status rkr_table_refill(rkr_table* t) {
     return enqueue_fill(t);
 }
 
+static int64_t rkr_trace_slots(const rkr_table* t) {
+    return t->tiles ? (int64_t)t->g.L * t->tplan.T : t->plan.total;
+}
+
 rkr_status rkr_debug_trace(rkr_table* t, int32_t enable) {
     if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
     DeviceGuard dg(t->device);
     if (enable && !t->trace && t->kernel == RKR_KERNEL_PERSISTENT) {
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->trace), (size_t)t->plan.total * 48,
-                           t->stream));
-        CK(cudaMemsetAsync(t->trace, 0, (size_t)t->plan.total * 48, t->stream));
+        const size_t n = (size_t)rkr_trace_slots(t) * 48;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->trace), n, t->stream));
+        CK(cudaMemsetAsync(t->trace, 0, n, t->stream));
     } else if (!enable && t->trace) {
         CK(cudaFreeAsync(t->trace, t->stream));
         t->trace = nullptr;
     }
     t->pdev.trace = t->trace;
     t->hdesc.plan.trace = t->trace;
+    t->tplan.trace = t->trace;
     CK(cudaMemcpyAsync(t->ddesc, &t->hdesc, sizeof(InstDesc), cudaMemcpyHostToDevice, t->stream));
     CK(cudaStreamSynchronize(t->stream));
     return RKR_OK;
 }
 
 int64_t rkr_debug_trace_items(const rkr_table* t) {
-    return (t && t->trace) ? t->plan.total : 0;
+    return (t && t->trace) ? rkr_trace_slots(t) : 0;
 }
 
 rkr_status rkr_debug_trace_read(const rkr_table* t, uint64_t* out, int32_t* item_k,
@@ -831,7 +874,14 @@ rkr_status rkr_debug_trace_read(const rkr_table* t, uint64_t* out, int32_t* item
     if (!t || !t->trace) return fail(RKR_ERR_ARGUMENT, "tracing not enabled");
     DeviceGuard dg(t->device);
     CK(cudaStreamSynchronize(t->stream));
-    CK(cudaMemcpy(out, t->trace, (size_t)t->plan.total * 48, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, t->trace, (size_t)rkr_trace_slots(t) * 48, cudaMemcpyDeviceToHost));
+    if (t->tiles) {  // one slot per (diagonal k, tile j), k-major
+        for (int64_t q = 0; q < rkr_trace_slots(t); ++q) {
+            if (item_k) item_k[q] = (int32_t)(q / t->tplan.T);
+            if (item_j) item_j[q] = (int32_t)(q % t->tplan.T);
+        }
+        return RKR_OK;
+    }
     // item -> (k, j) from the host copy of the plan
     const PersistPlan& p = t->plan;
     for (size_t e = 0; e < p.start.size(); ++e) {
@@ -1087,7 +1137,7 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
     rkr_exec ex{};
     if (exec) ex = *exec;
     ex.width = all32 ? RKR_WIDTH_AUTO : RKR_WIDTH_64;
-    ex.kernel = RKR_KERNEL_PERSISTENT;
+    ex.kernel = RKR_KERNEL_QUEUE;  // batched and sharded tables run K1p
     rkr_batch* b = new rkr_batch();
     b->device = ex.device;
     b->R = persistent_choose_r(min_m);
@@ -1409,7 +1459,7 @@ rkr_status sharded_create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max
         const int32_t lo = r * W, hi = (r == n - 1) ? m_max + 1 : (r + 1) * W;
         rkr_exec ex{};
         if (exec) ex = *exec;
-        ex.kernel = RKR_KERNEL_PERSISTENT;
+        ex.kernel = RKR_KERNEL_QUEUE;  // batched and sharded tables run K1p
         if (devices) ex.device = devices[r];
         if (devices && exec && exec->stream) ex.stream = nullptr;  // per-device library streams
         ShardSpec spec{lo, pad, jo};
@@ -1681,7 +1731,7 @@ rkr_status rkr_shard_create(const rkr_menu* menu, int64_t unit, int32_t m_max, i
     if (st) return st;
     rkr_exec ex{};
     if (exec) ex = *exec;
-    ex.kernel = RKR_KERNEL_PERSISTENT;
+    ex.kernel = RKR_KERNEL_QUEUE;  // batched and sharded tables run K1p
     ShardSpec spec{sg.lo[shard], sg.pad, sg.jo[shard]};
     spec.ipc = true;
     rkr_table* t = nullptr;

@@ -57,6 +57,11 @@ __host__ __device__ inline int64_t diag_off(int32_t L, int32_t k) {
 __host__ __device__ inline int64_t row_id(int32_t L, int32_t s, int32_t t) {
     return diag_off(L, t - s) + s;
 }
+// First cell-program cut entry of diagonal k: sum_{k' < k} (L - k') k'.
+// Cell (s, s + k) owns entries [diag_cut_off(L, k) + s * k, + k).
+__host__ __device__ inline int64_t diag_cut_off(int64_t L, int64_t k) {
+    return L * k * (k - 1) / 2 - (k - 1) * k * (2 * k - 1) / 6;
+}
 
 // K1p schedule (rkr_persist.cu).  Work items are (column group g, diagonal k,
 // tile j in the group, s).  Groups are GW = 1 tile wide; their diagonal
@@ -89,7 +94,8 @@ struct ProgDev {
     int32_t* pc;      // [saved options]
     void* otot;       // V [saved options]
     int64_t nq;
-    int32_t ocap;     // row stride of thr (the table's max saved options, >= 1)
+    int32_t ocap;     // row stride of thr (the table's max saved options, >= 1; K1t: rounded to 4)
+    int32_t tiles;    // 1: ptr holds K1t cut programs, int4 {off_l, off_r, sweep, gate}
 };
 int64_t program_cut_entries(const Geometry& g);
 
@@ -161,6 +167,23 @@ int launch_fill_batch(const InstDesc* dev_desc, const InstDesc* single, const La
 void persistent_plan(const Geometry& g, int width, int R, PersistPlan& p);
 int persistent_choose_r(int32_t M);
 size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p);  // counter + flags
+
+// K1t schedule (rkr_tiles.cu): CTA j owns budget slots [jW, (j+1)W) of every
+// row; done[k * T + j] != 0 once diagonal k of tile j is stored.
+struct TileSmem {  // shared-memory carve-up of K1t (byte offsets)
+    uint32_t best, code, blk, opd, prog, thr, bar, total;
+    uint32_t prog_bytes, thr_bytes;  // one buffer of each (two of each are kept)
+};
+struct TilePlan {
+    int32_t WC = 0, W = 0, T = 0, d = 0;  // W = 32 WC; d = lower tiles read (ceil(pad / W))
+    int32_t cap = 0;                      // bulk partials (values + codes) in shared memory
+    int32_t L = 0, nq = 0, ocap = 0;      // blocks, saved options, thr row stride
+    TileSmem sm{};
+    int32_t* done = nullptr;              // [L * T]
+    unsigned long long* trace = nullptr;  // optional: 6 stamps per (k, j)
+};
+int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp);  // 1 = eligible
+int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream);
 
 // Launch entry points (rkr_kernels.cu).
 struct LaunchCtx {

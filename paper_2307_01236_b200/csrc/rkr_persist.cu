@@ -104,12 +104,9 @@ struct Programs {
     V* otot;          // per saved option: time_fwd + time_bwd
     int64_t nq;
     int32_t ocap;     // thr row stride
+    int32_t tiles;    // 1: ptr holds K1t programs (int4 {off_l, off_r, sweep, gate}; width 32)
 };
 
-// first cut-program entry of diagonal k: sum_{k' < k} (L - k') k'
-__host__ __device__ inline int64_t diag_cut_off(int64_t L, int64_t k) {
-    return L * k * (k - 1) / 2 - (k - 1) * k * (2 * k - 1) / 6;
-}
 
 // ---------------------------------------------------------------------------
 // prep_programs: one warp per cell (s, t); the option-0 sweep (:162) and the
@@ -173,12 +170,23 @@ __global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> 
             if (i < k) {
                 const int64_t a = dm.act_u[c];
                 const int sh = a > g.pad ? g.pad : (int)a;
-                longlong2 p;
-                p.x = (long long)(opt + row_id(L, s, c - 1) * g.sr + g.pad);
-                p.y = (long long)(opt + row_id(L, c, t) * g.sr + g.pad - sh);
-                pr.ptr[base + i] = p;
-                pr.sweep[base + i] = sweep;
-                pr.gate[base + i] = clampm(gmax - g.m_base, M);
+                if (pr.tiles) {
+                    // K1t: element offsets of slot 0 (32-bit, tile_plan checks
+                    // rows * sr < 2^31) and the sweep and gate in one entry
+                    int4 q;
+                    q.x = (int)(row_id(L, s, c - 1) * g.sr + g.pad);
+                    q.y = (int)(row_id(L, c, t) * g.sr + g.pad - sh);
+                    q.z = (int)sweep;
+                    q.w = clampm(gmax - g.m_base, M);
+                    reinterpret_cast<int4*>(pr.ptr)[base + i] = q;
+                } else {
+                    longlong2 p;
+                    p.x = (long long)(opt + row_id(L, s, c - 1) * g.sr + g.pad);
+                    p.y = (long long)(opt + row_id(L, c, t) * g.sr + g.pad - sh);
+                    pr.ptr[base + i] = p;
+                    pr.sweep[base + i] = sweep;
+                    pr.gate[base + i] = clampm(gmax - g.m_base, M);
+                }
             }
             carry_sum = __shfl_sync(0xffffffffu, sweep, 31);
             carry_max = __shfl_sync(0xffffffffu, gmax, 31);
@@ -259,6 +267,7 @@ __device__ inline Programs<V> programs_of(const ProgDev& q) {
     p.otot = static_cast<V*>(q.otot);
     p.nq = q.nq;
     p.ocap = q.ocap;
+    p.tiles = q.tiles;
     return p;
 }
 
@@ -475,25 +484,44 @@ __global__ void __launch_bounds__(NT, MINB) fill_persistent(const InstDesc* __re
                 code[r] = cd;
             }
         };
-        // Case 1 (chain_dp.hpp:139-156)
-        for (int i = 0; i < nopt; ++i) {
-            const V tt = sm.otot[i];
-            const int th = sm.thr[i];
-            const int p = sm.pc[i];
+        // Case 1 (chain_dp.hpp:139-156).  The option windows of row (s+1, t)
+        // are loaded OB options at a time (OB*R loads in flight) before any
+        // is consumed: this loop is on the diagonal's critical path, and a
+        // load-use per option would serialise nopt L2 round trips.
+        constexpr int OB = 8;
+        for (int i0 = 0; i0 < nopt; i0 += OB) {
+            V sub[OB][R];
+            if (k > 0) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int m = mb + NT * r;
-                V tot = tt;
-                bool ok = m >= th;
-                if (k > 0) {
-                    // option window: L1-cached (the acquire fence above
-                    // invalidated L1, so every line is fetched after publish)
-                    const V sub = __ldca(nxt + (m - p));
-                    if constexpr (CostP<V>::checked) ok = ok && sub < INF;
-                    tot = tt + sub;
+                for (int u = 0; u < OB; ++u) {
+                    const int i = i0 + u < nopt ? i0 + u : i0;
+                    const int p = sm.pc[i];
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        // L1-cached: the acquire fence above invalidated L1,
+                        // so every line is fetched after the publish
+                        sub[u][r] = __ldca(nxt + (mb + NT * r - p));
                 }
-                if constexpr (!CostP<V>::checked) ok = ok && tot < INF;
-                offer(r, tot, (uint16_t)(i + 1), ok);
+            }
+#pragma unroll
+            for (int u = 0; u < OB; ++u) {
+                const int i = i0 + u;
+                if (i < nopt) {
+                    const V tt = sm.otot[i];
+                    const int th = sm.thr[i];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int m = mb + NT * r;
+                        V tot = tt;
+                        bool ok = m >= th;
+                        if (k > 0) {
+                            if constexpr (CostP<V>::checked) ok = ok && sub[u][r] < INF;
+                            tot = tt + sub[u][r];
+                        }
+                        if constexpr (!CostP<V>::checked) ok = ok && tot < INF;
+                        offer(r, tot, (uint16_t)(i + 1), ok);
+                    }
+                }
             }
         }
         // Case 2 tail cuts (chain_dp.hpp:158-174)
@@ -598,6 +626,7 @@ Programs<V> host_programs_of(const LaunchCtx& cx) {
     p.otot = static_cast<V*>(cx.prog.otot);
     p.nq = cx.prog.nq;
     p.ocap = cx.prog.ocap;
+    p.tiles = cx.prog.tiles;
     return p;
 }
 

@@ -1,0 +1,448 @@
+// rkr_tiles.cu -- K1t: the whole table fill as ONE co-resident launch in
+// which every CTA owns a budget tile (sm_100a).
+//
+// Why budget tiles.  Every read of the fill goes to a strictly smaller span
+// at a budget slot m' <= m (chain_dp.hpp:148, :166-167: shifts pack_chg,
+// act_u >= 0; the left operand of a cut is unshifted).  So if CTA j owns the
+// slots [jW, (j+1)W) of EVERY row, then diagonal k of its tile depends only
+// on (a) its own tile's earlier diagonals -- a __syncthreads away -- and (b)
+// the lower tiles j-d .. j-1 (d = ceil(pad / W)) up to diagonal k-1.  There
+// is no work queue and no item holds an SM while it waits: each CTA walks
+// the L diagonals of its tile in order, and the only cross-SM traffic is one
+// done flag per (diagonal, tile).
+//
+// One step k of CTA j:
+//   bulk(k)   cuts c in [s+2, t-1] of every row (s, t = s+k) of the tile.
+//             They read diagonals <= k-2 only, which the previous step's
+//             wait already acquired, so the bulk overlaps the lower tiles'
+//             progress on diagonal k-1.  When a diagonal has fewer (row,
+//             warp slice) units than warps, the cut range is split into P
+//             parts (late diagonals: few rows, many cuts).
+//   wait(k-1) lanes of warp 0 poll the flags of tiles j-d .. j-1 (relaxed),
+//             one gpu-scope acq_rel fence, CTA barrier.
+//   tail(k)   merge the bulk parts, then the options (row (s+1, t)) and the
+//             cuts c = s+1 and c = t -- the only candidates reading diagonal
+//             k-1 -- store opt/arg, barrier, release-add the flag (k, j).
+// Tie-break: the bulk scans its cuts ascending with a strict '<'; parts and
+// the tail merge with a lexicographic (value, code) minimum, and codes order
+// exactly like the reference's scan (options in menu order, then cuts
+// ascending), so every cell keeps the reference's first minimum
+// (chain_dp.hpp:139-174).
+//
+// Eligibility: T = ceil((M+1) / W) tiles must be co-resident (one 1024-thread
+// CTA per SM, cooperative launch), and the bulk partials (max(L W, 1024)
+// values + codes) must fit in shared memory.  Otherwise the queue-scheduled
+// K1p (rkr_persist.cu) runs.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "rkr_internal.h"
+
+namespace rkr {
+
+namespace {
+
+constexpr uint32_t INF = kInf32;  // K1t runs the 32-bit cost path only
+
+__device__ __forceinline__ int t_ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void t_fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void t_red_release_add(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long t_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+
+constexpr int kNW = 32;        // warps per CTA
+constexpr int kNT = kNW * 32;  // threads per CTA
+constexpr int kU = 8;          // cuts per load batch (2 kU loads in flight per lane)
+constexpr int kOB = 8;         // options per load batch
+
+inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~15ull); }
+inline TileSmem tile_smem(const TilePlan& tp) {
+    TileSmem m;
+    const uint64_t L = tp.L;
+    uint64_t pmax = 0;  // max over k of (L - k) k cut entries
+    for (uint64_t k = 0; k < L; ++k) pmax = (L - k) * k > pmax ? (L - k) * k : pmax;
+    m.prog_bytes = al16(pmax * 16);
+    m.thr_bytes = al16(L * tp.ocap * 4);
+    uint64_t b = 0;
+    m.best = 0;
+    b = al16(b + (uint64_t)tp.cap * 4);
+    m.code = (uint32_t)b;
+    b = al16(b + (uint64_t)tp.cap * 2);
+    m.blk = (uint32_t)b;
+    b = al16(b + (L + 1) * 4);
+    m.opd = (uint32_t)b;
+    b = al16(b + L * tp.ocap * 8);  // [block][ocap] {pack shift, pass time}, padded
+    m.prog = (uint32_t)b;
+    b += 2ull * m.prog_bytes;
+    m.thr = (uint32_t)b;
+    b += 2ull * m.thr_bytes;
+    m.bar = (uint32_t)b;
+    b += 16;
+    m.total = (uint32_t)b;
+    return m;
+}
+
+// One step's programs -> shared buffer (k & 1): the cut programs of diagonal
+// k (contiguous, (L-k) k int4 entries) and its rows' option thresholds.
+__device__ __forceinline__ void stage_step(const TilePlan& tp, const ProgDev& pq, const TileSmem& sm,
+                                           unsigned char* smem, uint64_t* bars, int L, int k) {
+    const int b = k & 1;
+    const uint32_t pb = (uint32_t)(L - k) * (uint32_t)k * 16u;
+    const uint32_t tb = (uint32_t)(L - k) * (uint32_t)tp.ocap * 4u;
+    mbar_expect_tx(bars + b, pb + tb);
+    if (pb)
+        bulk_g2s(smem + sm.prog + b * sm.prog_bytes,
+                 static_cast<const int4*>(pq.ptr) + diag_cut_off(L, k), pb, bars + b);
+    bulk_g2s(smem + sm.thr + b * sm.thr_bytes, pq.thr + diag_off(L, k) * tp.ocap, tb, bars + b);
+}
+
+template <int WC>
+__global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ InstDesc D,
+                                                    const __grid_constant__ TilePlan tp) {
+    constexpr int W = 32 * WC;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const TileSmem& sm = tp.sm;
+    uint32_t* pbest = reinterpret_cast<uint32_t*>(smem_raw + sm.best);
+    uint16_t* pcode = reinterpret_cast<uint16_t*>(smem_raw + sm.code);
+    int32_t* s_blk = reinterpret_cast<int32_t*>(smem_raw + sm.blk);
+    int2* s_opd = reinterpret_cast<int2*>(smem_raw + sm.opd);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sm.bar);
+
+    const Geometry& g = D.g;
+    const DevMenu& dm = D.dm;
+    const ProgDev& pq = D.prog;
+    uint32_t* __restrict__ opt = static_cast<uint32_t*>(D.opt);
+    uint16_t* __restrict__ arg = D.arg;
+    const int L = g.L, M = g.M;
+    const int sr = (int)g.sr;  // rows * sr < 2^31 (tile_plan)
+    const int ocap = tp.ocap;
+    const int j = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int m_lo = j * W;
+    const int d_eff = tp.d < j ? tp.d : j;  // lower tiles this one reads
+    int* __restrict__ done = tp.done;
+
+    // Table-independent data in shared memory: block option ranges, and per
+    // saved option the pack shift clamped to pad (:148) and time_fwd +
+    // time_bwd (:150).  Cut programs and thresholds arrive per step by bulk
+    // copy, one step ahead (double buffer, one mbarrier per buffer).
+    if (tid == 0) {
+        mbar_init(bars + 0, 1);
+        mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int c = tid; c <= L; c += kNT) s_blk[c] = __ldg(dm.blk_off + c);
+    // options of block s at [s * ocap, s * ocap + nopt_s); padding never wins
+    // (pass time INF, shift 0)
+    for (int q = tid; q < L * ocap; q += kNT) {
+        const int b = q / ocap, i = q - b * ocap;
+        const int o = __ldg(dm.blk_off + b) + i;
+        s_opd[q] = o < __ldg(dm.blk_off + b + 1)
+                       ? make_int2(__ldg(pq.pc + o), (int)__ldg(static_cast<const uint32_t*>(pq.otot) + o))
+                       : make_int2(0, (int)INF);
+    }
+    __syncthreads();
+    if (tid == 0) stage_step(tp, pq, sm, smem_raw, bars, L, 0);
+
+    for (int k = 0; k < L; ++k) {
+        unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+        if (tp.trace && tid == 0) t0 = t_gtimer();
+        // prefetch step k+1 into the other buffer (freed by the previous
+        // step's closing barrier); order the generic reads of that buffer
+        // before the async-proxy writes
+        if (tid == 0 && k + 1 < L) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            stage_step(tp, pq, sm, smem_raw, bars, L, k + 1);
+        }
+        mbar_wait(bars + (k & 1), (uint32_t)(k >> 1) & 1u);
+        const int4* prog = reinterpret_cast<const int4*>(smem_raw + sm.prog + (k & 1) * sm.prog_bytes);
+        const int32_t* thrs = reinterpret_cast<const int32_t*>(smem_raw + sm.thr + (k & 1) * sm.thr_bytes);
+
+        const int rows = L - k;
+        const int units = rows * WC;
+        const int nb = k >= 3 ? k - 2 : 0;  // bulk cuts i = 1 .. k-2
+        int P = 1, chunk = nb;
+        if (nb > 0 && units < kNW) {  // late diagonals: split the cut range
+            P = kNW / units;
+            const int pmax = (nb + 7) >> 3;  // keep >= 8 cuts per part
+            if (P > pmax) P = pmax;
+            chunk = (nb + P - 1) / P;
+        }
+
+        // ---- bulk: cuts i in [1, k-2], ascending, strict '<' ------------------
+        // program entry i of cell (s, s+k): element offsets of slot 0 of the
+        // left row (s, c-1) and of the right row (c, t) shifted by act_u[c]
+        // (:166-167), the option-0 sweep (:162) and the gate (:159, :164)
+        if (nb > 0) {
+            for (int it = warp; it < units * P; it += kNW) {
+                const int p = P == 1 ? 0 : it / units;
+                const int u = it - p * units;
+                const int s = u / WC;
+                const int m = m_lo + (u - s * WC) * 32 + lane;
+                const int4* pe = prog + s * k;
+                const uint16_t cb = (uint16_t)(kCutBit | (s + 1));
+                const int ib = 1 + p * chunk;
+                const int ie = ib + chunk < k - 1 ? ib + chunk : k - 1;
+                uint32_t best = INF;
+                uint16_t code = 0;
+                int i0 = ib;
+                for (; i0 + kU <= ie; i0 += kU) {
+                    uint32_t lv[kU], rv[kU];
+                    int4 e[kU];
+#pragma unroll
+                    for (int q = 0; q < kU; ++q) {
+                        e[q] = pe[i0 + q];
+                        // unconditional loads (every offset is inside the
+                        // table); the gate masks the candidate afterwards
+                        lv[q] = __ldcg(opt + (uint32_t)(e[q].x + m));
+                        rv[q] = __ldcg(opt + (uint32_t)(e[q].y + m));
+                    }
+#pragma unroll
+                    for (int q = 0; q < kU; ++q) {
+                        const uint32_t tot = (uint32_t)e[q].z + lv[q] + rv[q];
+                        if (e[q].w <= m && tot < best) {
+                            best = tot;
+                            code = (uint16_t)(cb + i0 + q);
+                        }
+                    }
+                    // the gate only grows with i: stop once no lane admits
+                    // the batch's last cut (the `break` of :164)
+                    if (!__any_sync(0xffffffffu, e[kU - 1].w <= m)) {
+                        i0 = ie;
+                        break;
+                    }
+                }
+                for (; i0 < ie; ++i0) {
+                    const int4 e = pe[i0];
+                    const uint32_t tot = (uint32_t)e.z + __ldcg(opt + (uint32_t)(e.x + m)) +
+                                         __ldcg(opt + (uint32_t)(e.y + m));
+                    if (e.w <= m && tot < best) {
+                        best = tot;
+                        code = (uint16_t)(cb + i0);
+                    }
+                }
+                pbest[it * 32 + lane] = best;
+                pcode[it * 32 + lane] = code;
+            }
+        }
+        if (tp.trace && tid == 0) t1 = t_gtimer();
+
+        // ---- wait for diagonal k-1 on the lower tiles ----------------------------
+        if (k >= 1 && warp == 0) {
+            const int* row = done + (int64_t)(k - 1) * tp.T;
+            for (int q = lane; q < d_eff; q += 32)
+                while (t_ld_relaxed(row + j - 1 - q) == 0) __nanosleep(20);
+            __syncwarp();
+            if (lane == 0) t_fence_acq_rel();
+        }
+        __syncthreads();
+        if (tp.trace && tid == 0) t2 = t_gtimer();
+
+        // ---- tail -------------------------------------------------------------------
+        // Candidates are merged in the reference's scan order -- options (menu
+        // order), cut i = 0, the bulk parts (i = 1 .. k-2, part by part), cut
+        // i = k-1 -- each with a strict '<', so the first minimum wins.
+        const int rbase = (int)diag_off(L, k);
+        for (int u = warp; u < units; u += kNW) {
+            const int s = u / WC;
+            const int m = m_lo + (u - s * WC) * 32 + lane;
+            const int rid = rbase + s;
+            // tail cut operands: i = 0 (c = s+1) and i = k-1 (c = t); their
+            // loads go out first
+            uint32_t tl0 = INF, tr0 = INF, tl1 = INF, tr1 = INF;
+            int4 e0 = make_int4(0, 0, 0, M + 2), e1 = e0;
+            if (k > 0) {
+                e0 = prog[s * k];
+                tl0 = __ldcg(opt + (uint32_t)(e0.x + m));
+                tr0 = __ldcg(opt + (uint32_t)(e0.y + m));
+                if (k > 1) {
+                    e1 = prog[s * k + k - 1];
+                    tl1 = __ldcg(opt + (uint32_t)(e1.x + m));
+                    tr1 = __ldcg(opt + (uint32_t)(e1.y + m));
+                }
+            }
+            uint32_t best = INF;
+            int code = 0;
+            // Case 1 (chain_dp.hpp:139-156): options of block s in menu order;
+            // windows of row (s+1, t) at m - pack_chg (row (s+1, t) is the next
+            // row of diagonal k-1: id rid - (L - k + 1) + 1)
+            const int nopt = s_blk[s + 1] - s_blk[s];
+            const int4* od4 = reinterpret_cast<const int4*>(s_opd + s * ocap);  // 2 options each
+            const int4* th4 = reinterpret_cast<const int4*>(thrs + s * ocap);   // 4 options each
+            const int widx = k > 0 ? (rid - (L - k)) * sr + g.pad + m : 0;
+            // whole batches: the padding options (ocap is a multiple of kOB) never win
+            for (int i0 = 0; i0 < nopt; i0 += kOB) {
+                uint32_t sub[kOB], ot[kOB];
+                int32_t th[kOB];
+#pragma unroll
+                for (int q = 0; q < kOB; q += 2) {
+                    const int4 o2 = od4[(i0 + q) >> 1];
+                    ot[q] = (uint32_t)o2.y;
+                    ot[q + 1] = (uint32_t)o2.w;
+                    sub[q] = k > 0 ? __ldcg(opt + (uint32_t)(widx - o2.x)) : 0u;
+                    sub[q + 1] = k > 0 ? __ldcg(opt + (uint32_t)(widx - o2.z)) : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < kOB; q += 4) {
+                    const int4 t4 = th4[(i0 + q) >> 2];
+                    th[q] = t4.x;
+                    th[q + 1] = t4.y;
+                    th[q + 2] = t4.z;
+                    th[q + 3] = t4.w;
+                }
+#pragma unroll
+                for (int q = 0; q < kOB; ++q) {
+                    const uint32_t tot = ot[q] + sub[q];
+                    if (m >= th[q] && tot < best) {
+                        best = tot;
+                        code = i0 + q + 1;
+                    }
+                }
+            }
+            // Case 2 (chain_dp.hpp:158-174): cut i = 0, bulk parts, cut i = k-1
+            const uint16_t cb = (uint16_t)(kCutBit | (s + 1));
+            {
+                const uint32_t tot = (uint32_t)e0.z + tl0 + tr0;
+                if (e0.w <= m && tot < best) {
+                    best = tot;
+                    code = cb;
+                }
+            }
+            if (nb > 0) {
+                for (int p = 0; p < P; ++p) {
+                    const int idx = (p * units + u) * 32 + lane;
+                    const uint32_t v = pbest[idx];
+                    if (v < best) {
+                        best = v;
+                        code = pcode[idx];
+                    }
+                }
+            }
+            {
+                const uint32_t tot = (uint32_t)e1.z + tl1 + tr1;
+                if (e1.w <= m && tot < best) {
+                    best = tot;
+                    code = (uint16_t)(cb + k - 1);
+                }
+            }
+            // store (chain_dp.hpp:176-177)
+            if (m <= M) {
+                opt[(int64_t)rid * sr + g.pad + m] = best;
+                arg[(int64_t)rid * g.sa + m] = (uint16_t)code;
+            }
+        }
+        if (tp.trace && tid == 0) t3 = t_gtimer();
+        __syncthreads();  // frees the partials and this step's program buffer
+        if (tid == 0) {
+            // release-add: orders the CTA's stores (made visible to thread 0
+            // by the barrier) before the flag
+            t_red_release_add(done + (int64_t)k * tp.T + j, 1);
+            if (tp.trace) {  // the K1p stamp layout (no k-2 wait: stamps 0 = 1)
+                unsigned long long* tr = tp.trace + 6 * ((int64_t)k * tp.T + j);
+                tr[0] = t0;
+                tr[1] = t0;
+                tr[2] = t1;
+                tr[3] = t2;
+                tr[4] = t3;
+                tr[5] = t_gtimer();
+            }
+        }
+    }
+}
+
+template <int WC>
+int launch_tiles_t(const InstDesc& d, const TilePlan& tp, cudaStream_t st) {
+    auto kern = fill_tiles<WC>;
+    const size_t smem = tp.sm.total;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+        return 3;
+    InstDesc dd = d;
+    TilePlan pp = tp;
+    void* args[] = {&dd, &pp};
+    // cooperative: the CTAs wait on each other, so all T must be co-resident
+    if (cudaLaunchCooperativeKernel((const void*)kern, dim3(tp.T), dim3(kNT), args, smem, st) !=
+        cudaSuccess)
+        return 3;
+    return 0;
+}
+
+}  // namespace
+
+// Narrowest tile (W = 32 WC) whose T tiles fit one CTA per SM; 0 = not
+// eligible (the queue-scheduled K1p runs instead).
+int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp) {
+    if (const char* e = getenv("RKR_TILES"))  // tuning knob: 0 disables K1t
+        if (atoi(e) == 0) return 0;
+    if (width != 32) return 0;
+    // 32-bit element offsets inside the table (plus the tile over-read)
+    if ((double)g.rows * g.sr + 64.0 * 32 + g.pad >= 2147483647.0) return 0;
+    for (int wc = 1; wc <= 8; wc *= 2) {
+        const int W = 32 * wc;
+        const int64_t T = ((int64_t)g.M + 1 + W - 1) / W;
+        if (T > sms) continue;
+        tp.WC = wc;
+        tp.W = W;
+        tp.T = (int32_t)T;
+        tp.d = (g.pad + W - 1) / W;
+        tp.cap = (int32_t)((int64_t)g.L * W > kNT ? (int64_t)g.L * W : kNT);
+        tp.L = g.L;
+        tp.nq = (int32_t)nq;
+        tp.ocap = ocap;
+        tp.sm = tile_smem(tp);
+        return tp.sm.total <= 220 * 1024 ? 1 : 0;
+    }
+    return 0;
+}
+
+int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (width != 32) return 3;
+    switch (tp.WC) {
+        case 1: return launch_tiles_t<1>(d, tp, st);
+        case 2: return launch_tiles_t<2>(d, tp, st);
+        case 4: return launch_tiles_t<4>(d, tp, st);
+        case 8: return launch_tiles_t<8>(d, tp, st);
+    }
+    return 3;
+}
+
+}  // namespace rkr

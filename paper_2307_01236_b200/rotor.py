@@ -29,7 +29,7 @@ from .menu import Menu, RkrMenu
 K_INF_TIME = (2**63 - 1) // 4  # remat::kInfTime, chain_dp.hpp:23
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librkr.so")
+LIB_PATH = os.environ.get("RKR_LIB") or os.path.join(_HERE, "librkr.so")  # RKR_LIB: A/B tuning
 
 RKR_OK, RKR_ERR_INVALID, RKR_ERR_INFEASIBLE, RKR_ERR_CUDA, RKR_ERR_OOM, RKR_ERR_CAPACITY, \
     RKR_ERR_ARGUMENT = range(7)
@@ -84,7 +84,7 @@ def lib() -> ctypes.CDLL:
     L.rkr_table_destroy.argtypes = [p]
     L.rkr_table_destroy.restype = None
     for name, rt in (("rkr_table_length", i32), ("rkr_table_unit", i64), ("rkr_table_m_max", i32),
-                     ("rkr_table_width", i32)):
+                     ("rkr_table_width", i32), ("rkr_table_kernel", i32)):
         getattr(L, name).argtypes = [p]
         getattr(L, name).restype = rt
     L.rkr_table_act_units.argtypes = [p, i32]
@@ -163,7 +163,7 @@ def _check(st: int, min_feasible: int = -1) -> None:
     raise DeviceError(f"librkr status {st}: {msg}")
 
 
-KERNELS = {"persistent": 0, "diagonal": 1}
+KERNELS = {"persistent": 0, "diagonal": 1, "queue": 2, "tiles": 3}
 
 
 def _exec(device: int, width: str, stream: Optional[int] = None,
@@ -288,6 +288,11 @@ class DpTable:
 
     def width(self) -> int:
         return self._lib.rkr_table_width(self._h)
+
+    def kernel(self) -> str:
+        """The fill kernel this table runs: "tiles", "queue" or "diagonal"."""
+        k = self._lib.rkr_table_kernel(self._h)
+        return {v: n for n, v in KERNELS.items()}[k]
 
     def sync(self) -> None:
         _check(self._lib.rkr_table_sync(self._h))

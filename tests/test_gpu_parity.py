@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 INF = rotor.K_INF_TIME
 WIDTHS = ["auto", "64"]
-KERNELS = ["persistent", "diagonal"]
+KERNELS = ["tiles", "queue", "diagonal"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -23,6 +23,8 @@ def _device():
 
 
 def dev_tables(menu, unit, M, width="auto", kernel="persistent"):
+    if kernel == "tiles" and width == "64":
+        pytest.skip("the budget-tile fill (K1t) runs the 32-bit cost path only")
     with rotor.DpTable(menu, unit, M, width=width, kernel=kernel) as t:
         o, k, v = t.download()
         return o, k, v, t.width()
@@ -321,6 +323,8 @@ def test_edge_menus_vs_oracle(orc, idx, M, unit):
     st, *ref = orc.fill(menu, unit, M)
     assert st == 0
     for width, kernel in ((w_, k_) for w_ in WIDTHS for k_ in KERNELS):
+        if kernel == "tiles" and (width == "64" or idx in (2, 3)):
+            continue  # K1t is 32-bit only (idx 2, 3 fail the overflow proof)
         o, k, v, w = dev_tables(menu, unit, M, width, kernel)
         if idx in (2, 3):
             assert w == 64

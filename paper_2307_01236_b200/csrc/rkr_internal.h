@@ -179,6 +179,7 @@ struct TilePlan {
     int32_t cap = 0;                      // bulk partials (values + codes) in shared memory
     int32_t L = 0, nq = 0, ocap = 0;      // blocks, saved options, thr row stride
     TileSmem sm{};
+    int32_t comm = 0;                     // 1: a dedicated communication warp (latency-bound tables)
     int32_t* done = nullptr;              // [L * T]
     unsigned long long* trace = nullptr;  // optional: 6 stamps per (k, j)
 };

@@ -135,6 +135,7 @@ __global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> 
         const bool seeded = t < L - 1;                              // chain_dp.hpp:126
         const int64_t seed = seeded ? 2 * dm.act_u[t + 1] : 0;      // chain_dp.hpp:127
         const int o0 = dm.blk_off[s], nopt = dm.blk_off[s + 1] - o0;
+        for (int i = nopt + lane; i < ocap; i += 32) pr.thr[rid * ocap + i] = M + 1;  // padding: never valid
         for (int i = lane; i < nopt; i += 32) {
             const int q = o0 + i;
             const int64_t need = (k == 0 && seeded) ? dm.fwd_req_pre[q] + dm.act_u[t + 1]

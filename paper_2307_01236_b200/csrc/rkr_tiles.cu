@@ -5,34 +5,34 @@
 // at a budget slot m' <= m (chain_dp.hpp:148, :166-167: shifts pack_chg,
 // act_u >= 0; the left operand of a cut is unshifted).  So if CTA j owns the
 // slots [jW, (j+1)W) of EVERY row, then diagonal k of its tile depends only
-// on (a) its own tile's earlier diagonals -- a __syncthreads away -- and (b)
+// on (a) its own tile's earlier diagonals -- a CTA barrier away -- and (b)
 // the lower tiles j-d .. j-1 (d = ceil(pad / W)) up to diagonal k-1.  There
 // is no work queue and no item holds an SM while it waits: each CTA walks
 // the L diagonals of its tile in order, and the only cross-SM traffic is one
 // done flag per (diagonal, tile).
 //
-// One step k of CTA j:
-//   bulk(k)   cuts c in [s+2, t-1] of every row (s, t = s+k) of the tile.
-//             They read diagonals <= k-2 only, which the previous step's
-//             wait already acquired, so the bulk overlaps the lower tiles'
-//             progress on diagonal k-1.  When a diagonal has fewer (row,
-//             warp slice) units than warps, the cut range is split into P
-//             parts (late diagonals: few rows, many cuts).
-//   wait(k-1) lanes of warp 0 poll the flags of tiles j-d .. j-1 (relaxed),
-//             one gpu-scope acq_rel fence, CTA barrier.
-//   tail(k)   merge the bulk parts, then the options (row (s+1, t)) and the
-//             cuts c = s+1 and c = t -- the only candidates reading diagonal
-//             k-1 -- store opt/arg, barrier, release-add the flag (k, j).
-// Tie-break: the bulk scans its cuts ascending with a strict '<'; parts and
-// the tail merge with a lexicographic (value, code) minimum, and codes order
-// exactly like the reference's scan (options in menu order, then cuts
-// ascending), so every cell keeps the reference's first minimum
-// (chain_dp.hpp:139-174).
+// Warp roles.  Warps 0..30 compute; warp 31 communicates, so that no fence,
+// flag poll or release ever stalls a compute warp:
+//   compute, step k:  bulk(k) -> sync READY(k) -> tail(k) -> arrive DONE(k)
+//   comm,    step k:  poll flags (k-1) of tiles j-d..j-1, acquire ->
+//                     arrive READY(k) -> sync DONE(k) -> release flag (k, j)
+//                     -> bulk-copy the programs of step k+2
+// bulk(k)  cuts c in [s+2, t-1] of every row (s, t = s+k): they read
+//          diagonals <= k-2 only (acquired before tail(k-1)), so they overlap
+//          the lower tiles' progress on diagonal k-1.  When a diagonal has
+//          fewer (row, warp slice) units than compute warps, the cut range is
+//          split into P parts (late diagonals: few rows, many cuts).
+// tail(k)  the options (row (s+1, t)) and cuts c = s+1 and c = t -- the only
+//          candidates reading diagonal k-1 -- merged with the bulk parts in
+//          the reference's scan order, then stored.
+// Tie-break: options in menu order, then cuts ascending, each merged with a
+// strict '<' in that order, so every cell keeps the reference's first
+// minimum (chain_dp.hpp:139-174).
 //
-// Eligibility: T = ceil((M+1) / W) tiles must be co-resident (one 1024-thread
-// CTA per SM, cooperative launch), and the bulk partials (max(L W, 1024)
-// values + codes) must fit in shared memory.  Otherwise the queue-scheduled
-// K1p (rkr_persist.cu) runs.
+// Eligibility: 32-bit costs; T = ceil((M+1) / W) tiles co-resident (one
+// 1024-thread CTA per SM, cooperative launch); shared memory for the bulk
+// partials and two steps of programs.  Otherwise the queue-scheduled K1p
+// (rkr_persist.cu) runs.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -87,10 +87,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
 }
 
+__device__ __forceinline__ int t_ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// named barriers (0 is __syncthreads): compute warps arrive / sync, the
+// communication warp syncs / arrives
+constexpr int kBarReady = 1, kBarDone = 2;
+__device__ __forceinline__ void nb_sync(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(1024) : "memory");
+}
+__device__ __forceinline__ void nb_arrive(int id) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(1024) : "memory");
+}
+
 constexpr int kNW = 32;        // warps per CTA
 constexpr int kNT = kNW * 32;  // threads per CTA
 constexpr int kU = 8;          // cuts per load batch (2 kU loads in flight per lane)
-constexpr int kOB = 8;         // options per load batch
+constexpr int kOB = 8;         // options per load batch (ocap is a multiple of kOB)
 
 inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~15ull); }
 inline TileSmem tile_smem(const TilePlan& tp) {
@@ -102,9 +117,16 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     m.thr_bytes = al16(L * tp.ocap * 4);
     uint64_t b = 0;
     m.best = 0;
-    b = al16(b + (uint64_t)tp.cap * 4);
+    // bulk partials: [L W] for unsplit steps (a unit's parts are written and
+    // read by the same warp), then two [kNT] buffers by step parity for split
+    // steps (parts cross warps; a warp may run one step ahead)
+    // [L W] (>= kNT); with the communication warp also two [kNT] parity
+    // buffers for split steps.  (Config 3 sits at the edge: 12 KB more shared
+    // memory measured 30% slower -- less L1 left for loads in flight.)
+    const uint64_t np = (uint64_t)tp.cap + (tp.comm ? 2 * kNT : 0);
+    b = al16(b + np * 4);
     m.code = (uint32_t)b;
-    b = al16(b + (uint64_t)tp.cap * 2);
+    b = al16(b + np * 2);
     m.blk = (uint32_t)b;
     b = al16(b + (L + 1) * 4);
     m.opd = (uint32_t)b;
@@ -133,14 +155,58 @@ __device__ __forceinline__ void stage_step(const TilePlan& tp, const ProgDev& pq
     bulk_g2s(smem + sm.thr + b * sm.thr_bytes, pq.thr + diag_off(L, k) * tp.ocap, tb, bars + b);
 }
 
-template <int WC>
+// Cuts i in [ib, ie) of one cell slice, ascending, strict '<' into (best,
+// code).  Program entry i of cell (s, s+k): element offsets of slot 0 of the
+// left row (s, c-1) and of the right row (c, t) shifted by act_u[c]
+// (:166-167), the option-0 sweep (:162) and the gate (:159, :164).
+__device__ __forceinline__ void scan_cuts(const uint32_t* __restrict__ opt, const int4* pe, int ib,
+                                          int ie, int m, int cb, uint32_t& best, int& code) {
+    int i0 = ib;
+    for (; i0 + kU <= ie; i0 += kU) {
+        uint32_t lv[kU], rv[kU];
+        int4 e[kU];
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            e[q] = pe[i0 + q];
+            // unconditional loads (every offset is inside the table); the
+            // gate masks the candidate afterwards
+            lv[q] = __ldcg(opt + (uint32_t)(e[q].x + m));
+            rv[q] = __ldcg(opt + (uint32_t)(e[q].y + m));
+        }
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const uint32_t tot = (uint32_t)e[q].z + lv[q] + rv[q];
+            if (e[q].w <= m && tot < best) {
+                best = tot;
+                code = cb + i0 + q;
+            }
+        }
+        // the gate only grows with i: stop once no lane admits the batch's
+        // last cut (the `break` of :164)
+        if (!__any_sync(0xffffffffu, e[kU - 1].w <= m)) return;
+    }
+    for (; i0 < ie; ++i0) {
+        const int4 e = pe[i0];
+        const uint32_t tot =
+            (uint32_t)e.z + __ldcg(opt + (uint32_t)(e.x + m)) + __ldcg(opt + (uint32_t)(e.y + m));
+        if (e.w <= m && tot < best) {
+            best = tot;
+            code = cb + i0;
+        }
+    }
+}
+
+// COMM: warp 31 is the communication warp (latency-bound tables); otherwise
+// all 32 warps compute and warp 0 polls / thread 0 publishes inline, behind
+// CTA barriers (throughput-bound tables, where the 32nd compute warp and
+// barrier-aligned phases measured faster).
+template <int WC, bool COMM>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ InstDesc D,
                                                     const __grid_constant__ TilePlan tp) {
     constexpr int W = 32 * WC;
+    constexpr int kNC = COMM ? kNW - 1 : kNW;  // compute warps
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const TileSmem& sm = tp.sm;
-    uint32_t* pbest = reinterpret_cast<uint32_t*>(smem_raw + sm.best);
-    uint16_t* pcode = reinterpret_cast<uint16_t*>(smem_raw + sm.code);
     int32_t* s_blk = reinterpret_cast<int32_t*>(smem_raw + sm.blk);
     int2* s_opd = reinterpret_cast<int2*>(smem_raw + sm.opd);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sm.bar);
@@ -156,21 +222,18 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
     const int j = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int m_lo = j * W;
-    const int d_eff = tp.d < j ? tp.d : j;  // lower tiles this one reads
-    int* __restrict__ done = tp.done;
 
     // Table-independent data in shared memory: block option ranges, and per
-    // saved option the pack shift clamped to pad (:148) and time_fwd +
-    // time_bwd (:150).  Cut programs and thresholds arrive per step by bulk
-    // copy, one step ahead (double buffer, one mbarrier per buffer).
+    // (block, option slot) the pack shift clamped to pad (:148) and time_fwd
+    // + time_bwd (:150), padded to ocap with options that never win (pass
+    // time INF).  Cut programs and thresholds arrive per step by bulk copy,
+    // two steps ahead (double buffer, one mbarrier per buffer).
     if (tid == 0) {
         mbar_init(bars + 0, 1);
         mbar_init(bars + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int c = tid; c <= L; c += kNT) s_blk[c] = __ldg(dm.blk_off + c);
-    // options of block s at [s * ocap, s * ocap + nopt_s); padding never wins
-    // (pass time INF, shift 0)
     for (int q = tid; q < L * ocap; q += kNT) {
         const int b = q / ocap, i = q - b * ocap;
         const int o = __ldg(dm.blk_off + b) + i;
@@ -178,19 +241,47 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
                        ? make_int2(__ldg(pq.pc + o), (int)__ldg(static_cast<const uint32_t*>(pq.otot) + o))
                        : make_int2(0, (int)INF);
     }
+    const int d_eff = tp.d < j ? tp.d : j;  // lower tiles this one reads
+    int* __restrict__ done = tp.done;
     __syncthreads();
-    if (tid == 0) stage_step(tp, pq, sm, smem_raw, bars, L, 0);
 
+    if (COMM && warp == kNC) {
+        // ================= communication warp =================
+        if (lane == 0) {
+            stage_step(tp, pq, sm, smem_raw, bars, L, 0);
+            if (L > 1) stage_step(tp, pq, sm, smem_raw, bars, L, 1);
+        }
+        for (int k = 0; k < L; ++k) {
+            if (k >= 1) {  // diagonal k-1 of the lower tiles, acquired
+                const int* row = done + (int64_t)(k - 1) * tp.T;
+                for (int q = lane; q < d_eff; q += 32)
+                    while (t_ld_acquire(row + j - 1 - q) == 0) __nanosleep(20);
+                __syncwarp();
+            }
+            nb_arrive(kBarReady);
+            nb_sync(kBarDone);  // the compute warps stored diagonal k
+            if (lane == 0) {
+                // release-add: orders the CTA's stores (made visible to this
+                // thread by the barrier) before the flag
+                t_red_release_add(done + (int64_t)k * tp.T + j, 1);
+                // buffer (k & 1) is free: every compute warp finished tail(k)
+                if (k + 2 < L) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    stage_step(tp, pq, sm, smem_raw, bars, L, k + 2);
+                }
+            }
+        }
+        return;
+    }
+
+    // ================= compute warps =================
+    if (!COMM && tid == 0) {
+        stage_step(tp, pq, sm, smem_raw, bars, L, 0);
+        if (L > 1) stage_step(tp, pq, sm, smem_raw, bars, L, 1);
+    }
     for (int k = 0; k < L; ++k) {
         unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
         if (tp.trace && tid == 0) t0 = t_gtimer();
-        // prefetch step k+1 into the other buffer (freed by the previous
-        // step's closing barrier); order the generic reads of that buffer
-        // before the async-proxy writes
-        if (tid == 0 && k + 1 < L) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            stage_step(tp, pq, sm, smem_raw, bars, L, k + 1);
-        }
         mbar_wait(bars + (k & 1), (uint32_t)(k >> 1) & 1u);
         const int4* prog = reinterpret_cast<const int4*>(smem_raw + sm.prog + (k & 1) * sm.prog_bytes);
         const int32_t* thrs = reinterpret_cast<const int32_t*>(smem_raw + sm.thr + (k & 1) * sm.thr_bytes);
@@ -199,80 +290,50 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
         const int units = rows * WC;
         const int nb = k >= 3 ? k - 2 : 0;  // bulk cuts i = 1 .. k-2
         int P = 1, chunk = nb;
-        if (nb > 0 && units < kNW) {  // late diagonals: split the cut range
-            P = kNW / units;
+        if (nb > 0 && units < kNC) {  // late diagonals: split the cut range
+            P = kNC / units;
             const int pmax = (nb + 7) >> 3;  // keep >= 8 cuts per part
             if (P > pmax) P = pmax;
             chunk = (nb + P - 1) / P;
         }
+        // bulk partials (see tile_smem)
+        const int poff = (!COMM || P == 1) ? 0 : tp.cap + (k & 1) * kNT;
+        uint32_t* pbest = reinterpret_cast<uint32_t*>(smem_raw + sm.best) + poff;
+        uint16_t* pcode = reinterpret_cast<uint16_t*>(smem_raw + sm.code) + poff;
 
-        // ---- bulk: cuts i in [1, k-2], ascending, strict '<' ------------------
-        // program entry i of cell (s, s+k): element offsets of slot 0 of the
-        // left row (s, c-1) and of the right row (c, t) shifted by act_u[c]
-        // (:166-167), the option-0 sweep (:162) and the gate (:159, :164)
+        // ---- bulk: cuts i in [1, k-2] ahead of the wait -----------------------
+        // (scanning them inside the tail instead, which frees the [L W]
+        // partials, measured 3% slower on config 3)
         if (nb > 0) {
-            for (int it = warp; it < units * P; it += kNW) {
+            for (int it = warp; it < units * P; it += kNC) {
                 const int p = P == 1 ? 0 : it / units;
                 const int u = it - p * units;
                 const int s = u / WC;
                 const int m = m_lo + (u - s * WC) * 32 + lane;
-                const int4* pe = prog + s * k;
-                const uint16_t cb = (uint16_t)(kCutBit | (s + 1));
                 const int ib = 1 + p * chunk;
                 const int ie = ib + chunk < k - 1 ? ib + chunk : k - 1;
                 uint32_t best = INF;
-                uint16_t code = 0;
-                int i0 = ib;
-                for (; i0 + kU <= ie; i0 += kU) {
-                    uint32_t lv[kU], rv[kU];
-                    int4 e[kU];
-#pragma unroll
-                    for (int q = 0; q < kU; ++q) {
-                        e[q] = pe[i0 + q];
-                        // unconditional loads (every offset is inside the
-                        // table); the gate masks the candidate afterwards
-                        lv[q] = __ldcg(opt + (uint32_t)(e[q].x + m));
-                        rv[q] = __ldcg(opt + (uint32_t)(e[q].y + m));
-                    }
-#pragma unroll
-                    for (int q = 0; q < kU; ++q) {
-                        const uint32_t tot = (uint32_t)e[q].z + lv[q] + rv[q];
-                        if (e[q].w <= m && tot < best) {
-                            best = tot;
-                            code = (uint16_t)(cb + i0 + q);
-                        }
-                    }
-                    // the gate only grows with i: stop once no lane admits
-                    // the batch's last cut (the `break` of :164)
-                    if (!__any_sync(0xffffffffu, e[kU - 1].w <= m)) {
-                        i0 = ie;
-                        break;
-                    }
-                }
-                for (; i0 < ie; ++i0) {
-                    const int4 e = pe[i0];
-                    const uint32_t tot = (uint32_t)e.z + __ldcg(opt + (uint32_t)(e.x + m)) +
-                                         __ldcg(opt + (uint32_t)(e.y + m));
-                    if (e.w <= m && tot < best) {
-                        best = tot;
-                        code = (uint16_t)(cb + i0);
-                    }
-                }
+                int code = 0;
+                scan_cuts(opt, prog + s * k, ib, ie, m, kCutBit | (s + 1), best, code);
                 pbest[it * 32 + lane] = best;
-                pcode[it * 32 + lane] = code;
+                pcode[it * 32 + lane] = (uint16_t)code;
             }
         }
         if (tp.trace && tid == 0) t1 = t_gtimer();
-
-        // ---- wait for diagonal k-1 on the lower tiles ----------------------------
-        if (k >= 1 && warp == 0) {
-            const int* row = done + (int64_t)(k - 1) * tp.T;
-            for (int q = lane; q < d_eff; q += 32)
-                while (t_ld_relaxed(row + j - 1 - q) == 0) __nanosleep(20);
-            __syncwarp();
-            if (lane == 0) t_fence_acq_rel();
+        // diagonal k-1 of the lower tiles acquired (and, with P > 1, every
+        // bulk part of this step written)
+        if constexpr (COMM) {
+            nb_sync(kBarReady);
+        } else {
+            if (k >= 1 && warp == 0) {
+                const int* row = done + (int64_t)(k - 1) * tp.T;
+                for (int q = lane; q < d_eff; q += 32)
+                    while (t_ld_relaxed(row + j - 1 - q) == 0) __nanosleep(20);
+                __syncwarp();
+                if (lane == 0) t_fence_acq_rel();
+            }
+            __syncthreads();
         }
-        __syncthreads();
         if (tp.trace && tid == 0) t2 = t_gtimer();
 
         // ---- tail -------------------------------------------------------------------
@@ -280,7 +341,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
         // order), cut i = 0, the bulk parts (i = 1 .. k-2, part by part), cut
         // i = k-1 -- each with a strict '<', so the first minimum wins.
         const int rbase = (int)diag_off(L, k);
-        for (int u = warp; u < units; u += kNW) {
+        for (int u = warp; u < units; u += kNC) {
             const int s = u / WC;
             const int m = m_lo + (u - s * WC) * 32 + lane;
             const int rid = rbase + s;
@@ -302,12 +363,12 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
             int code = 0;
             // Case 1 (chain_dp.hpp:139-156): options of block s in menu order;
             // windows of row (s+1, t) at m - pack_chg (row (s+1, t) is the next
-            // row of diagonal k-1: id rid - (L - k + 1) + 1)
+            // row of diagonal k-1: id rid - (L - k))
             const int nopt = s_blk[s + 1] - s_blk[s];
             const int4* od4 = reinterpret_cast<const int4*>(s_opd + s * ocap);  // 2 options each
             const int4* th4 = reinterpret_cast<const int4*>(thrs + s * ocap);   // 4 options each
             const int widx = k > 0 ? (rid - (L - k)) * sr + g.pad + m : 0;
-            // whole batches: the padding options (ocap is a multiple of kOB) never win
+            // whole batches: the padding options never win
             for (int i0 = 0; i0 < nopt; i0 += kOB) {
                 uint32_t sub[kOB], ot[kOB];
                 int32_t th[kOB];
@@ -337,7 +398,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
                 }
             }
             // Case 2 (chain_dp.hpp:158-174): cut i = 0, bulk parts, cut i = k-1
-            const uint16_t cb = (uint16_t)(kCutBit | (s + 1));
+            const int cb = kCutBit | (s + 1);
             {
                 const uint32_t tot = (uint32_t)e0.z + tl0 + tr0;
                 if (e0.w <= m && tot < best) {
@@ -359,7 +420,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
                 const uint32_t tot = (uint32_t)e1.z + tl1 + tr1;
                 if (e1.w <= m && tot < best) {
                     best = tot;
-                    code = (uint16_t)(cb + k - 1);
+                    code = cb + k - 1;
                 }
             }
             // store (chain_dp.hpp:176-177)
@@ -368,28 +429,34 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
                 arg[(int64_t)rid * g.sa + m] = (uint16_t)code;
             }
         }
-        if (tp.trace && tid == 0) t3 = t_gtimer();
-        __syncthreads();  // frees the partials and this step's program buffer
-        if (tid == 0) {
-            // release-add: orders the CTA's stores (made visible to thread 0
-            // by the barrier) before the flag
-            t_red_release_add(done + (int64_t)k * tp.T + j, 1);
-            if (tp.trace) {  // the K1p stamp layout (no k-2 wait: stamps 0 = 1)
-                unsigned long long* tr = tp.trace + 6 * ((int64_t)k * tp.T + j);
-                tr[0] = t0;
-                tr[1] = t0;
-                tr[2] = t1;
-                tr[3] = t2;
-                tr[4] = t3;
-                tr[5] = t_gtimer();
+        if (tp.trace && tid == 0) {
+            t3 = t_gtimer();
+            unsigned long long* tr = tp.trace + 6 * ((int64_t)k * tp.T + j);
+            tr[0] = t0;  // the K1p stamp layout: no k-2 wait (stamp 1 = 0),
+            tr[1] = t0;  // publish happens on the communication warp (5 = 4)
+            tr[2] = t1;
+            tr[3] = t2;
+            tr[4] = t3;
+            tr[5] = t3;
+        }
+        if constexpr (COMM) {
+            nb_arrive(kBarDone);  // stores of diagonal k issued; go on to bulk(k+1)
+        } else {
+            __syncthreads();
+            if (tid == 0) {
+                t_red_release_add(done + (int64_t)k * tp.T + j, 1);
+                if (k + 2 < L) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    stage_step(tp, pq, sm, smem_raw, bars, L, k + 2);
+                }
             }
         }
     }
 }
 
-template <int WC>
+template <int WC, bool COMM>
 int launch_tiles_t(const InstDesc& d, const TilePlan& tp, cudaStream_t st) {
-    auto kern = fill_tiles<WC>;
+    auto kern = fill_tiles<WC, COMM>;
     const size_t smem = tp.sm.total;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -427,6 +494,11 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
         tp.L = g.L;
         tp.nq = (int32_t)nq;
         tp.ocap = ocap;
+        // the communication warp pays off where the fill is latency-bound
+        // (per-step work of a few microseconds: configs 1-2), not where it is
+        // throughput-bound (config 3: measured 5.36 ms without, 6.56 with)
+        tp.comm = (double)g.rows * (g.M + 1) <= 16.0e6 ? 1 : 0;
+        if (const char* e = getenv("RKR_COMM")) tp.comm = atoi(e) ? 1 : 0;  // tuning knob
         tp.sm = tile_smem(tp);
         return tp.sm.total <= 220 * 1024 ? 1 : 0;
     }
@@ -436,11 +508,19 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
 int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (width != 32) return 3;
+    if (tp.comm) {
+        switch (tp.WC) {
+            case 1: return launch_tiles_t<1, true>(d, tp, st);
+            case 2: return launch_tiles_t<2, true>(d, tp, st);
+            case 4: return launch_tiles_t<4, true>(d, tp, st);
+            case 8: return launch_tiles_t<8, true>(d, tp, st);
+        }
+    }
     switch (tp.WC) {
-        case 1: return launch_tiles_t<1>(d, tp, st);
-        case 2: return launch_tiles_t<2>(d, tp, st);
-        case 4: return launch_tiles_t<4>(d, tp, st);
-        case 8: return launch_tiles_t<8>(d, tp, st);
+        case 1: return launch_tiles_t<1, false>(d, tp, st);
+        case 2: return launch_tiles_t<2, false>(d, tp, st);
+        case 4: return launch_tiles_t<4, false>(d, tp, st);
+        case 8: return launch_tiles_t<8, false>(d, tp, st);
     }
     return 3;
 }

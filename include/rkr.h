@@ -187,6 +187,10 @@ rkr_status rkr_table_sync(const rkr_table* table);
 /* Re-run the whole fill from the device-resident menu (no host work, async):
  * the device-only step bench.py times. */
 rkr_status rkr_table_refill(rkr_table* table);
+/* Refill, then walk build_schedule_rec from (s, t, m) on the device (async;
+ * collect with rkr_backtrack_fetch).  With the budget-tile fill the walk is
+ * fused into the fill launch: the last CTA to finish walks. */
+rkr_status rkr_table_refill_walk(rkr_table* table, int32_t s, int32_t t, int32_t m);
 /* The cudaStream_t every kernel of this table is launched on. */
 void* rkr_table_stream(const rkr_table* table);
 /* Bytes copied host->device by rkr_table_create (the staged menu precompute). */

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librkr.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("rkr_kernels.cu", "rkr_persist.cu", "rkr_tiles.cu", "rkr_capi.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "rkr_internal.h"), os.path.join(ROOT, "include", "rkr.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "rkr_internal.h"), os.path.join(CSRC, "rkr_walk.cuh"), os.path.join(ROOT, "include", "rkr.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -218,6 +218,7 @@ struct Staging {
     }
 };
 thread_local Staging t_stage;
+thread_local Staging t_back;  // pinned D2H staging (walk results)
 
 }  // namespace
 
@@ -332,8 +333,9 @@ rkr_status alloc_and_upload(rkr_table* t) {
     take(((size_t)t->g.rows * t->g.sr + kOptSlack) * vbytes);  // 19 opt
     take((size_t)t->g.rows * t->g.sa * 2);       // 20 arg
     // counter | done flags [L x flag_cols] (K1p tiles or K1t tiles) | halo [L]
+    // | CTAs finished (K1t fused walk)
     t->flag_cols = std::max<int32_t>(t->plan.J, t->tplan.T);
-    t->state_bytes = 8 + ((size_t)t->g.L * t->flag_cols + t->g.L) * sizeof(int);
+    t->state_bytes = 8 + ((size_t)t->g.L * t->flag_cols + t->g.L + 1) * sizeof(int);
     take(t->state_bytes);                        // 21 K1p counter + done flags
     const bool progs = t->kernel == RKR_KERNEL_PERSISTENT;
     const size_t nc = progs ? (size_t)program_cut_entries(t->g) : 0;
@@ -393,6 +395,7 @@ rkr_status alloc_and_upload(rkr_table* t) {
     pd.trace = nullptr;
     t->hdesc.halo = pd.done + (size_t)t->g.L * t->flag_cols;
     t->tplan.done = pd.done;
+    t->tplan.fin = t->hdesc.halo + t->g.L;
     t->prog.ptr = b + off[22];
     t->prog.sweep = b + off[23];
     t->prog.gate = reinterpret_cast<int32_t*>(b + off[24]);
@@ -439,7 +442,31 @@ rkr_status alloc_and_upload(rkr_table* t) {
     return RKR_OK;
 }
 
-rkr_status enqueue_fill(rkr_table* t) {
+rkr_status ensure_ops(rkr_table* t) {
+    if (t->dops_cap == 0) {
+        const int64_t cap = std::max<int64_t>(4096, 8 * (int64_t)t->g.L + 64);
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->dops), (size_t)cap * 12, t->stream));
+        t->dops_cap = cap;
+    }
+    return RKR_OK;
+}
+
+// Fill, then (walk) the schedule walk from (s, tt, m): fused into the K1t
+// launch (its last CTA walks), or as the K2 launch after the fill.
+rkr_status enqueue_fill(rkr_table* t, bool walk = false, int32_t s = 0, int32_t tt = 0,
+                        int32_t m = 0) {
+    if (walk) {
+        rkr_status st = ensure_ops(t);
+        if (st) return st;
+    }
+    if (walk && !t->tiles) {
+        rkr_status st = enqueue_fill(t);
+        if (st) return st;
+        if (launch_backtrack(t->ctx(), s, tt, m, t->dops, t->dops_cap,
+                             reinterpret_cast<int32_t*>(t->stack), t->dout))
+            return cuda_fail(cudaGetLastError(), "backtrack launch");
+        return RKR_OK;
+    }
     if (t->kernel != RKR_KERNEL_PERSISTENT) {
         if (launch_init_pads(t->ctx())) return cuda_fail(cudaGetLastError(), "pad launch");
         if (launch_fill_all(t->ctx())) return cuda_fail(cudaGetLastError(), "fill launch");
@@ -447,7 +474,16 @@ rkr_status enqueue_fill(rkr_table* t) {
     }
     CK(cudaMemsetAsync(t->pdev.counter, 0, t->state_bytes, t->stream));
     if (t->tiles) {
-        if (launch_fill_tiles(t->hdesc, t->tplan, t->width, t->stream))
+        TilePlan tp = t->tplan;
+        tp.walk = walk ? 1 : 0;
+        tp.ws = s;
+        tp.wt = tt;
+        tp.wm = m;
+        tp.wops = t->dops;
+        tp.wcap = t->dops_cap;
+        tp.wout = t->dout;
+        tp.wstack = reinterpret_cast<int4*>(t->stack);
+        if (launch_fill_tiles(t->hdesc, tp, t->width, t->stream))
             return cuda_fail(cudaGetLastError(), "tile fill launch");
         return RKR_OK;
     }
@@ -540,7 +576,9 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
         if (!t->tiles) t->tplan = TilePlan{};
     }
     st = alloc_and_upload(t);
-    if (st == RKR_OK && launch_init_pads(t->ctx())) st = cuda_fail(cudaGetLastError(), "pad launch");
+    // (the persistent kernels' program launch also writes the pads)
+    if (st == RKR_OK && t->kernel != RKR_KERNEL_PERSISTENT && launch_init_pads(t->ctx()))
+        st = cuda_fail(cudaGetLastError(), "pad launch");
     if (st == RKR_OK && t->kernel == RKR_KERNEL_PERSISTENT && launch_prep_programs(t->ctx()))
         st = cuda_fail(cudaGetLastError(), "program launch");
     if (st != RKR_OK) {
@@ -776,11 +814,8 @@ rkr_status rkr_backtrack_async(rkr_table* t, int32_t s, int32_t tt, int32_t m) {
     rkr_status st = check_cell(t, s, tt);
     if (st) return st;
     DeviceGuard dg(t->device);
-    if (t->dops_cap == 0) {
-        const int64_t cap = std::max<int64_t>(4096, 8 * (int64_t)t->g.L + 64);
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->dops), (size_t)cap * 12, t->stream));
-        t->dops_cap = cap;
-    }
+    st = ensure_ops(t);
+    if (st) return st;
     if (launch_backtrack(t->ctx(), s, tt, m, t->dops, t->dops_cap,
                          reinterpret_cast<int32_t*>(t->stack), t->dout))
         return cuda_fail(cudaGetLastError(), "backtrack launch");
@@ -797,9 +832,19 @@ rkr_status rkr_backtrack_fetch(rkr_table* t, rkr_op* ops, int64_t cap, int64_t* 
     if (!t->bt_pending) return fail(RKR_ERR_ARGUMENT, "no backtrack enqueued on this table");
     DeviceGuard dg(t->device);
     *n_ops = 0;
-    CK(cudaMemcpyAsync(t->hout, t->dout, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, t->stream));
+    // one round trip for the usual case: the walk record and the first `est`
+    // ops come back together through pinned memory
+    const int64_t est = std::min<int64_t>({cap, t->dops_cap, 16 * (int64_t)t->g.L + 64});
+    void* pin = nullptr;
+    CK(t_back.get(64 + (size_t)std::max<int64_t>(est, 0) * 12, &pin));
+    CK(cudaMemcpyAsync(pin, t->dout, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, t->stream));
+    if (est > 0)
+        CK(cudaMemcpyAsync(static_cast<char*>(pin) + 64, t->dops, (size_t)est * 12,
+                           cudaMemcpyDeviceToHost, t->stream));
     CK(cudaStreamSynchronize(t->stream));
+    std::memcpy(t->hout, pin, 5 * sizeof(int64_t));
     int64_t n = t->hout[0];
+    const bool have = n <= est;  // ops already on the host
     if (n > t->dops_cap) {  // grow the device op buffer and walk again (rare)
         CK(cudaFreeAsync(t->dops, t->stream));
         CK(cudaMallocAsync(reinterpret_cast<void**>(&t->dops), (size_t)n * 12, t->stream));
@@ -815,7 +860,9 @@ rkr_status rkr_backtrack_fetch(rkr_table* t, rkr_op* ops, int64_t cap, int64_t* 
     t->bt_pending = false;
     const int64_t status = t->hout[1];
     const int64_t ncopy = std::min(n, cap);
-    if (ncopy > 0) {
+    if (ncopy > 0 && have) {
+        std::memcpy(ops, static_cast<char*>(pin) + 64, (size_t)ncopy * 12);
+    } else if (ncopy > 0) {
         CK(cudaMemcpyAsync(ops, t->dops, (size_t)ncopy * 12, cudaMemcpyDeviceToHost, t->stream));
         CK(cudaStreamSynchronize(t->stream));
     }
@@ -840,6 +887,19 @@ rkr_status rkr_table_refill(rkr_table* t) {
     if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
     DeviceGuard dg(t->device);
     return enqueue_fill(t);
+}
+
+rkr_status rkr_table_refill_walk(rkr_table* t, int32_t s, int32_t tt, int32_t m) {
+    rkr_status st = check_cell(t, s, tt);
+    if (st) return st;
+    DeviceGuard dg(t->device);
+    st = enqueue_fill(t, true, s, tt, m);
+    if (st) return st;
+    t->bt_s = s;
+    t->bt_t = tt;
+    t->bt_m = m;
+    t->bt_pending = true;
+    return RKR_OK;
 }
 
 static int64_t rkr_trace_slots(const rkr_table* t) {
@@ -942,13 +1002,13 @@ rkr_status rkr_solve_chain(const rkr_menu* menu, int64_t budget_bytes, int32_t u
     if (m_top < 0) return fail(RKR_ERR_INFEASIBLE, "budget cannot hold the chain input");
     if (m_top > 0x7ffffffe) return fail(RKR_ERR_INVALID, "budget slots exceed int range");
     rkr_table* t = nullptr;
-    st = rkr_table_create(menu, unit, (int32_t)m_top, exec, &t);           // :262
+    st = prepare_table(menu, unit, (int32_t)m_top, exec, 0, &t);          // :262
     if (st) return st;
     const int L = t->g.L;
-    // one device walk from the top cell: its first read is opt(0, L-1, m_top)
-    // (chain_dp.hpp:264), returned with the ops, so a feasible solve needs a
-    // single host synchronisation
-    st = rkr_backtrack_async(t, 0, L - 1, (int32_t)m_top);
+    // fill + one device walk from the top cell (fused into the K1t launch):
+    // its first read is opt(0, L-1, m_top) (chain_dp.hpp:264), returned with
+    // the ops, so a feasible solve needs a single host synchronisation
+    st = rkr_table_refill_walk(t, 0, L - 1, (int32_t)m_top);
     if (st == RKR_OK) st = rkr_backtrack_fetch(t, ops, cap, n_ops);
     const int64_t best = t->hout[4];
     if (st != RKR_OK && best < RKR_INF_TIME) {

@@ -180,6 +180,14 @@ struct TilePlan {
     int32_t L = 0, nq = 0, ocap = 0;      // blocks, saved options, thr row stride
     TileSmem sm{};
     int32_t comm = 0;                     // 1: a dedicated communication warp (latency-bound tables)
+    // fused K2 (per launch): the last CTA walks from (ws, wt, wm) into wops /
+    // wout = {n_ops, status, bad_s, bad_t, top} (rkr_walk.cuh)
+    int32_t walk = 0, ws = 0, wt = 0, wm = 0;
+    int32_t* wops = nullptr;
+    int64_t wcap = 0;
+    int64_t* wout = nullptr;
+    int4* wstack = nullptr;
+    int* fin = nullptr;                   // CTAs finished (zeroed with the flags)
     int32_t* done = nullptr;              // [L * T]
     unsigned long long* trace = nullptr;  // optional: 6 stamps per (k, j)
 };

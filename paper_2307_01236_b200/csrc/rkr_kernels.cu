@@ -17,23 +17,11 @@
 #include <cstdint>
 
 #include "rkr_internal.h"
+#include "rkr_walk.cuh"
 
 namespace rkr {
 
 namespace {
-
-template <typename V>
-struct Cost;
-template <>
-struct Cost<uint32_t> {
-    static constexpr uint32_t inf = kInf32;
-    static constexpr bool checked = false;  // bounded by the host overflow proof
-};
-template <>
-struct Cost<int64_t> {
-    static constexpr int64_t inf = kInf64;
-    static constexpr bool checked = true;   // arbitrary int64: explicit inf tests
-};
 
 __device__ __forceinline__ int32_t clamp_thr(int64_t x, int32_t M) {
     return x < -1 ? -1 : (x > (int64_t)M + 1 ? M + 1 : (int32_t)x);
@@ -215,105 +203,6 @@ __global__ void init_pads(Geometry g, V* opt) {
     }
 }
 
-// Menu lookups the walk needs, straight from the device menu or from a
-// shared-memory copy (the walk is a chain of dependent loads, so every hop
-// it takes off global memory shortens it).  chg/act are cast to int exactly
-// as build_schedule_rec does (chain_dp.hpp:229, :240).
-struct GlobalMenuView {
-    const DevMenu* dm;
-    __device__ int blk(int s) const { return dm->blk_off[s]; }
-    __device__ int id(int q) const { return dm->ids[q]; }
-    __device__ int chg(int q) const { return (int)dm->chg_bt[q]; }
-    __device__ int act(int c) const { return (int)dm->act_u[c]; }
-};
-struct SharedMenuView {
-    const int32_t *b, *i, *g, *a;
-    __device__ int blk(int s) const { return b[s]; }
-    __device__ int id(int q) const { return i[q]; }
-    __device__ int chg(int q) const { return g[q]; }
-    __device__ int act(int c) const { return a[c]; }
-};
-
-// K2: build_schedule_rec as an explicit stack walk on one thread.  Stack
-// entries are int4 {type, s, t, m}: type 0 = cell to expand, type 1 =
-// pending BlockBwd(s, t = option).  out = {n_ops, status, bad_s, bad_t, top}.
-template <typename V, typename MV>
-__device__ void walk(const Geometry& g, const MV& mv, const V* __restrict__ opt,
-                     const uint16_t* __restrict__ arg, int s0, int t0, int m0,
-                     int32_t* __restrict__ ops, int64_t cap, int4* __restrict__ stack,
-                     int64_t* __restrict__ out) {
-    const int L = g.L, M = g.M;
-    int64_t n = 0;
-    int sp = 0;
-    int64_t status = 0, bad_s = -1, bad_t = -1;
-    auto emit = [&](int kd, int b, int x) {
-        if (n < cap) {
-            ops[3 * n] = kd;
-            ops[3 * n + 1] = b;
-            ops[3 * n + 2] = x;
-        }
-        ++n;
-    };
-    {  // the root cell's value (solve_chain's opt_time / feasibility test)
-        int64_t top = kInf64;
-        if (m0 >= 0) {
-            const V v = opt[row_id(L, s0, t0) * g.sr + g.pad + (m0 > M ? M : m0)];
-            top = v >= Cost<V>::inf ? kInf64 : (int64_t)v;
-        }
-        out[4] = top;
-    }
-    stack[sp++] = make_int4(0, s0, t0, m0);
-    while (sp > 0) {
-        const int4 e = stack[--sp];
-        if (e.x == 1) {  // deferred BlockBwd of an option turn (chain_dp.hpp:230)
-            emit(3, e.y, e.z);
-            continue;
-        }
-        const int s = e.y, t = e.z, m = e.w;
-        // table.opt(s,t,m) >= kInfTime -> InfeasibleBudget (chain_dp.hpp:213-215)
-        const int64_t rid = row_id(L, s, t);
-        bool inf = m < 0;
-        const int mm = m > M ? M : (m < 0 ? 0 : m);
-        const V v = __ldcg(opt + rid * g.sr + g.pad + mm);   // both loads in flight together
-        const uint16_t code = __ldcg(arg + rid * g.sa + mm);
-        inf = inf || v >= Cost<V>::inf;
-        if (inf || code == 0) {  // code 0 on a finite cell = "cell without a decision"
-            status = 2;
-            bad_s = s;
-            bad_t = t;
-            break;
-        }
-        if (!(code & kCutBit)) {  // Option (chain_dp.hpp:217-232)
-            const int q = mv.blk(s) + code - 1;
-            const int val = mv.id(q);
-            emit(2, s, val);
-            if (s == t) {
-                if (t == L - 1) emit(0, t, -1);
-                emit(3, s, val);
-            } else {
-                stack[sp++] = make_int4(1, s, val, 0);
-                stack[sp++] = make_int4(0, s + 1, t, m - mv.chg(q));
-            }
-        } else {  // Cut (chain_dp.hpp:233-244)
-            const int c = code & 0x7fff;
-            emit(2, s, 0);
-            for (int j = s + 1; j < c; ++j) {
-                emit(2, j, 0);
-                emit(1, j, -1);
-            }
-            stack[sp++] = make_int4(0, s, c - 1, m);             // left, after
-            stack[sp++] = make_int4(0, c, t, m - mv.act(c));     // right, first
-        }
-    }
-    out[0] = n;
-    out[1] = status;
-    out[2] = bad_s;
-    out[3] = bad_t;
-}
-
-// The walk is a chain of dependent loads (code -> next cell); one warp stages
-// the stack and the menu lookups in shared memory when they fit, so each hop
-// costs one table read.
 template <typename V>
 __global__ void backtrack(Geometry g, DevMenu dm, const V* __restrict__ opt,
                           const uint16_t* __restrict__ arg, int s0, int t0, int m0,

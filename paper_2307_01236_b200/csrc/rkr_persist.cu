@@ -193,6 +193,16 @@ __global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> 
             carry_max = __shfl_sync(0xffffffffu, gmax, 31);
         }
     }
+    // the infinity pads of every opt row (init_pads, folded into this launch)
+    {
+        V* o = const_cast<V*>(opt);
+        const int64_t n = g.rows * (int64_t)g.pad;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t r = i / g.pad, p = i - r * g.pad;
+            o[r * g.sr + p] = CostP<V>::inf;
+        }
+    }
     // per saved option: clamped pack shift and pass time
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < pr.nq;
          q += (int64_t)gridDim.x * blockDim.x) {

@@ -39,6 +39,7 @@
 #include <cstdlib>
 
 #include "rkr_internal.h"
+#include "rkr_walk.cuh"
 
 namespace rkr {
 
@@ -128,7 +129,7 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     m.code = (uint32_t)b;
     b = al16(b + np * 2);
     m.blk = (uint32_t)b;
-    b = al16(b + (L + 1) * 4);
+    b = al16(b + (L + 2) * 4);  // block option offsets [L+1] + the last-CTA flag
     m.opd = (uint32_t)b;
     b = al16(b + L * tp.ocap * 8);  // [block][ocap] {pack shift, pass time}, padded
     m.prog = (uint32_t)b;
@@ -271,9 +272,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
                 }
             }
         }
-        return;
-    }
-
+    } else {
     // ================= compute warps =================
     if (!COMM && tid == 0) {
         stage_step(tp, pq, sm, smem_raw, bars, L, 0);
@@ -451,6 +450,50 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
                 }
             }
         }
+    }
+    }  // compute warps
+
+    // ---- fused K2: the last CTA to finish walks the schedule ----------------
+    // (build_schedule_rec, chain_dp.hpp:211-246).  Every CTA counts itself
+    // out with an acq_rel add after its last publish; the one that sees T-1
+    // has acquired every other tile's stores.  Saves the walk's launch and
+    // reads a table that is still hot in L2.
+    if (!tp.walk) return;
+    __syncthreads();
+    int* s_last = reinterpret_cast<int*>(smem_raw + sm.blk);  // s_blk is done with
+    if (tid == 0) {
+        int prev;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                     : "=r"(prev)
+                     : "l"(tp.fin)
+                     : "memory");
+        s_last[L + 1] = prev == tp.T - 1;
+    }
+    __syncthreads();
+    if (!s_last[L + 1]) return;
+    // menu lookups and the stack in shared memory (program and partial
+    // buffers are free now); the global view when they do not fit
+    int4* sstack = reinterpret_cast<int4*>(smem_raw + sm.best);
+    int32_t* mb = reinterpret_cast<int32_t*>(smem_raw + sm.prog);
+    const bool fit = 4ull * (2 * (L + 1) + 2 * (uint64_t)tp.nq) <= 2ull * sm.prog_bytes &&
+                     16ull * (2 * L + 16) <= (uint64_t)tp.cap * 4;
+    if (fit) {
+        int32_t *b = mb, *a = b + L + 1, *id = a + L + 1, *gq = id + tp.nq;
+        for (int x = tid; x <= L; x += kNT) {
+            b[x] = __ldg(dm.blk_off + x);
+            a[x] = (int)__ldg(dm.act_u + x);
+        }
+        for (int x = tid; x < tp.nq; x += kNT) {
+            id[x] = __ldg(dm.ids + x);
+            gq[x] = (int)__ldg(dm.chg_bt + x);
+        }
+        __syncthreads();
+        if (tid == 0)
+            walk<uint32_t>(g, SharedMenuView{b, id, gq, a}, opt, arg, tp.ws, tp.wt, tp.wm, tp.wops,
+                           tp.wcap, sstack, tp.wout);
+    } else if (tid == 0) {
+        walk<uint32_t>(g, GlobalMenuView{&dm}, opt, arg, tp.ws, tp.wt, tp.wm, tp.wops, tp.wcap,
+                       tp.wstack, tp.wout);
     }
 }
 

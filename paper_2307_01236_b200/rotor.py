@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
                                   P(i64), P(i32), P(i64)]
     L.rkr_table_sync.argtypes = [p]
     L.rkr_table_refill.argtypes = [p]
+    L.rkr_table_refill_walk.argtypes = [p, i32, i32, i32]
     L.rkr_table_stream.argtypes = [p]
     L.rkr_table_stream.restype = p
     L.rkr_table_h2d_bytes.argtypes = [p]
@@ -325,6 +326,12 @@ class DpTable:
 
     def backtrack_async(self, s: int, t: int, m: int) -> None:
         _check(self._lib.rkr_backtrack_async(self._h, s, t, m))
+
+    def refill_walk(self, s: int, t: int, m: int) -> None:
+        """Refill and walk from (s, t, m) on the device (async; the walk is
+        fused into the fill launch with the budget-tile kernel).  Collect the
+        ops with backtrack_fetch()."""
+        _check(self._lib.rkr_table_refill_walk(self._h, s, t, m))
 
     def backtrack_fetch(self, cap: int = 1 << 16) -> List[Tuple[int, int, int]]:
         buf = (RkrOp * cap)()

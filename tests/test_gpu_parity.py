@@ -367,3 +367,46 @@ def test_cpp_drop_in_program():
     r = subprocess.run([path], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+# ---------------------------------------------------------------------------
+# Fill + walk in one call (rkr_table_refill_walk; fused into the K1t launch)
+# ---------------------------------------------------------------------------
+def _walk_or_inf(fn):
+    try:
+        return fn()
+    except rotor.InfeasibleBudget:
+        return "infeasible"
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("L,B,M,seed", [(16, 6, 300, 3), (33, 16, 4096, 42 + 2), (5, 3, 40, 9)])
+def test_refill_walk_matches_oracle(orc, kernel, L, B, M, seed):
+    menu = synthetic_menu(L, B, M, seed, tie_stress=True)
+    st, o, k, v, _, _ = orc.fill(menu, 1, M)
+    assert st == 0
+    cells = [(0, L - 1, M), (0, L - 1, M // 3), (0, L - 1, 2), (1, L - 1, M), (L // 2, L - 1, M // 2),
+             (0, L // 2, M), (L - 1, L - 1, M), (0, L - 1, M + 5), (0, L - 1, -1)]
+    with rotor.DpTable(menu, 1, M, kernel=kernel) as t:
+        for s, tt, m in cells:
+            bst, ref_ops = orc.build_schedule(menu, 1, M, (o, k, v), s, tt, m)
+            want = ref_ops if bst == 0 else "infeasible"
+            t.refill_walk(s, tt, m)
+            assert _walk_or_inf(t.backtrack_fetch) == want, (s, tt, m)
+            assert _walk_or_inf(lambda: t.backtrack(s, tt, m)) == want
+        # the table after a fused fill is the oracle's table
+        do, dk, dv = t.download()
+        assert_same((do, dk, dv), (o, k, v))
+
+
+def test_tiles_without_communication_warp(orc, monkeypatch):
+    """The barrier-aligned K1t variant (large tables) on small tables, fill and fused walk."""
+    monkeypatch.setenv("RKR_COMM", "0")
+    for L, B, M, seed in [(12, 6, 200, 7), (40, 8, 1500, 11), (3, 2, 20, 5)]:
+        menu = synthetic_menu(L, B, M, seed, tie_stress=True)
+        st, o, k, v, _, _ = orc.fill(menu, 1, M)
+        with rotor.DpTable(menu, 1, M, kernel="tiles") as t:
+            assert_same(t.download(), (o, k, v))
+            t.refill_walk(0, L - 1, M)
+            bst, ref_ops = orc.build_schedule(menu, 1, M, (o, k, v), 0, L - 1, M)
+            assert bst == 0 and t.backtrack_fetch() == ref_ops

@@ -505,7 +505,8 @@ struct ShardSpec {
 // precompute, geometry, plan, one pooled allocation + one H2D copy, pads,
 // cell programs.  R = 0 lets the plan choose the per-thread slot count.
 rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, const rkr_exec* exec,
-                         int R, rkr_table** out, const ShardSpec* spec = nullptr) {
+                         int R, rkr_table** out, const ShardSpec* spec = nullptr,
+                         bool batch_tiles = false) {
     if (!out) return fail(RKR_ERR_ARGUMENT, "null output handle");
     *out = nullptr;
     if (m_max < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
@@ -565,7 +566,8 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
         if (!spec && kreq != RKR_KERNEL_QUEUE) {
             int sms = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
-            t->tiles = tile_plan(t->g, t->width, sms, (int64_t)h.ids.size(),
+            // batch tables need no co-residency (their tiles are queued jobs)
+            t->tiles = tile_plan(t->g, t->width, batch_tiles ? INT32_MAX : sms, (int64_t)h.ids.size(),
                                  (int)round_up(std::max<int32_t>(h.max_opts, 1), 8), t->tplan) == 1;
         }
         if (kreq == RKR_KERNEL_TILES && !t->tiles) {
@@ -1067,6 +1069,14 @@ struct rkr_batch {
     std::vector<InstDesc> hd;            // host copies of the descriptors
     size_t desc_bytes = 0, plan_bytes = 0, o_inst = 0, o_k = 0, o_j = 0;
     bool owns_tables = true;
+    // budget-tile batches (K1t jobs): per-table plans, the job queue
+    bool tiles = false;
+    TilePlan proto{};                    // batch-wide WC / comm / shared-memory layout
+    std::vector<TilePlan> htp;
+    std::vector<int2> hjobs;
+    TilePlan* dtps = nullptr;
+    int2* djobs = nullptr;
+    size_t tps_bytes = 0, jobs_bytes = 0;
 };
 
 namespace {
@@ -1094,6 +1104,13 @@ rkr_status batch_launch(rkr_batch* b) {
 
 rkr_status batch_fill(rkr_batch* b) {
     CK(cudaMemsetAsync(b->counter, 0, b->state_bytes, b->stream));
+    if (b->tiles) {
+        if (launch_fill_tiles_batch(b->ddesc, b->dtps, b->djobs, (int)b->hjobs.size(),
+                                    reinterpret_cast<unsigned int*>(b->counter), b->proto,
+                                    b->stream))
+            return cuda_fail(cudaGetLastError(), "tile batch launch");
+        return RKR_OK;
+    }
     if (launch_fill_batch(b->ddesc, nullptr, b->lplan, b->width, b->R, b->kcap, b->ocap,
                           b->counter, b->stream))
         return cuda_fail(cudaGetLastError(), "batch fill launch");
@@ -1111,7 +1128,7 @@ rkr_status batch_layout(rkr_batch* b) {
     for (rkr_table* t : b->tables) {
         b->kcap = std::max(b->kcap, t->g.L - 1);
         b->ocap = std::max(b->ocap, t->hm.max_opts);
-        flags += (size_t)t->g.L * t->plan.J;
+        flags += (size_t)t->g.L * t->flag_cols;
         halos += (size_t)t->g.L;
     }
     // merged launch order: tables advance their wavefronts together
@@ -1128,8 +1145,26 @@ rkr_status batch_layout(rkr_batch* b) {
     b->o_k = b->o_inst + round_up((int64_t)(np * 4), 256);
     b->o_j = b->o_k + round_up((int64_t)(np * 4), 256);
     b->plan_bytes = b->o_j + round_up((int64_t)(np * 4), 256);
+    if (b->tiles) {
+        // job queue: tables by decreasing work (the long ones start first),
+        // each table's tiles ascending (a job only waits on earlier ones)
+        std::vector<int> order(n);
+        for (int i = 0; i < n; ++i) order[i] = i;
+        auto work = [&](int i) {
+            const rkr_table* t = b->tables[i];
+            return (double)t->g.L * t->g.L * (t->g.M + 1) * (t->g.L + t->hm.max_opts);
+        };
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return work(x) > work(y); });
+        b->hjobs.clear();
+        for (int i : order)
+            for (int jt = 0; jt < b->tables[i]->tplan.T; ++jt) b->hjobs.push_back(make_int2(i, jt));
+        b->tps_bytes = (size_t)round_up((int64_t)(sizeof(TilePlan) * n), 256);
+        b->jobs_bytes = (size_t)round_up((int64_t)(sizeof(int2) * b->hjobs.size()), 256);
+    }
+    const size_t extra = b->tps_bytes + b->jobs_bytes;
     b->state_bytes = 8 + (flags + halos) * sizeof(int);
-    CK(cudaMallocAsync(&b->block, b->desc_bytes + b->plan_bytes + b->state_bytes, b->stream));
+    CK(cudaMallocAsync(&b->block, b->desc_bytes + b->plan_bytes + extra + b->state_bytes,
+                       b->stream));
     unsigned char* base = static_cast<unsigned char*>(b->block);
     b->ddesc = reinterpret_cast<InstDesc*>(base);
     unsigned char* pb = base + b->desc_bytes;
@@ -1139,10 +1174,27 @@ rkr_status batch_layout(rkr_batch* b) {
     b->lplan.j = reinterpret_cast<const int32_t*>(pb + b->o_j);
     b->lplan.n = (int32_t)np;
     b->lplan.total = b->hp.total;
-    b->counter = reinterpret_cast<unsigned long long*>(base + b->desc_bytes + b->plan_bytes);
-    int32_t* flag = reinterpret_cast<int32_t*>(base + b->desc_bytes + b->plan_bytes + 8);
+    b->dtps = reinterpret_cast<TilePlan*>(base + b->desc_bytes + b->plan_bytes);
+    b->djobs = reinterpret_cast<int2*>(base + b->desc_bytes + b->plan_bytes + b->tps_bytes);
+    b->counter = reinterpret_cast<unsigned long long*>(base + b->desc_bytes + b->plan_bytes + extra);
+    int32_t* flag = reinterpret_cast<int32_t*>(base + b->desc_bytes + b->plan_bytes + extra + 8);
     int32_t* halo = flag + flags;
     b->hd.assign(n, InstDesc{});
+    if (b->tiles) {
+        // one shared-memory layout for every job: the tables' maxima
+        TilePlan& pr = b->proto;
+        pr = b->tables[0]->tplan;
+        for (rkr_table* t : b->tables) {
+            pr.L = std::max(pr.L, t->tplan.L);
+            pr.nq = std::max(pr.nq, t->tplan.nq);
+            pr.ocap = std::max(pr.ocap, t->tplan.ocap);
+            pr.cap = std::max(pr.cap, t->tplan.cap);
+        }
+        pr.comm = 1;  // every job is a latency-bound tile walk
+        if (const char* e = getenv("RKR_COMM")) pr.comm = atoi(e) ? 1 : 0;  // tuning knob
+        pr.sm = tile_batch_smem(pr);
+        b->htp.assign(n, TilePlan{});
+    }
     int64_t item = 0;
     for (int32_t i = 0; i < n; ++i) {
         rkr_table* t = b->tables[i];
@@ -1151,7 +1203,17 @@ rkr_status batch_layout(rkr_batch* b) {
         b->hd[i].plan.trace = nullptr;
         b->hd[i].halo = halo;
         b->hd[i].item_base = item;
-        flag += (size_t)t->g.L * t->plan.J;
+        if (b->tiles) {
+            TilePlan tp = t->tplan;
+            tp.done = flag;
+            tp.trace = nullptr;
+            tp.walk = 0;
+            tp.fin = nullptr;
+            tp.comm = b->proto.comm;
+            tp.sm = b->proto.sm;
+            b->htp[i] = tp;
+        }
+        flag += (size_t)t->g.L * t->flag_cols;
         halo += t->g.L;
         item += t->plan.total;
     }
@@ -1162,7 +1224,7 @@ rkr_status batch_layout(rkr_batch* b) {
 rkr_status batch_upload(rkr_batch* b) {
     const int n = (int)b->tables.size();
     const size_t np = b->hp.start.size();
-    const size_t up = b->desc_bytes + b->plan_bytes;
+    const size_t up = b->desc_bytes + b->plan_bytes + b->tps_bytes + b->jobs_bytes;
     void* stage = nullptr;
     CK(t_stage.get(up, &stage));
     unsigned char* sb = static_cast<unsigned char*>(stage);
@@ -1172,6 +1234,11 @@ rkr_status batch_upload(rkr_batch* b) {
     std::memcpy(pb + b->o_inst, b->hp.inst.data(), np * 4);
     std::memcpy(pb + b->o_k, b->hp.k.data(), np * 4);
     std::memcpy(pb + b->o_j, b->hp.j.data(), np * 4);
+    if (b->tiles) {
+        std::memcpy(pb + b->plan_bytes, b->htp.data(), sizeof(TilePlan) * n);
+        std::memcpy(pb + b->plan_bytes + b->tps_bytes, b->hjobs.data(),
+                    sizeof(int2) * b->hjobs.size());
+    }
     CK(cudaMemcpyAsync(b->block, stage, up, cudaMemcpyHostToDevice, b->stream));
     CK(cudaEventRecord(t_stage.done, b->stream));
     return RKR_OK;
@@ -1186,6 +1253,10 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
     // common cost width: 32 only if every table's overflow proof holds
     bool all32 = !(exec && exec->width == RKR_WIDTH_64);
     int32_t min_m = INT32_MAX;
+    TilePlan proto{};  // the budget-tile batch's shared-memory needs: every table's maxima
+    proto.WC = 1;
+    proto.W = 32;
+    proto.comm = 1;
     for (int32_t i = 0; i < n; ++i) {
         HostMenu h;
         rkr_status st = build_host_menu(menus[i], units[i], h);
@@ -1193,24 +1264,52 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
         if (m_max[i] < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
         all32 = all32 && h.bounded32;
         min_m = std::min(min_m, m_max[i]);
+        proto.L = std::max(proto.L, h.L);
+        proto.nq = std::max<int32_t>(proto.nq, (int32_t)h.ids.size());
+        proto.ocap = std::max<int32_t>(proto.ocap, (int32_t)round_up(std::max(h.max_opts, 1), 8));
+        proto.cap = std::max<int32_t>(proto.cap, std::max(32 * h.L, 1024));
     }
+    const bool batch_fits = tile_batch_smem(proto).total <= 220 * 1024;
     rkr_exec ex{};
     if (exec) ex = *exec;
     ex.width = all32 ? RKR_WIDTH_AUTO : RKR_WIDTH_64;
-    ex.kernel = RKR_KERNEL_QUEUE;  // batched and sharded tables run K1p
-    rkr_batch* b = new rkr_batch();
-    b->device = ex.device;
-    b->R = persistent_choose_r(min_m);
-    DeviceGuard dg(b->device);
-    for (int32_t i = 0; i < n; ++i) {
-        rkr_table* t = nullptr;
-        rkr_status st = prepare_table(menus[i], units[i], m_max[i], &ex, b->R, &t);
-        if (st != RKR_OK) {
-            free_batch(b);
-            return st;
+    // budget-tile jobs (K1t) when every table qualifies (32-bit costs,
+    // shared memory), else the row-segment queue (K1p)
+    const int kreq = exec ? exec->kernel : RKR_KERNEL_PERSISTENT;
+    bool want_tiles = all32 && batch_fits && kreq != RKR_KERNEL_QUEUE && kreq != RKR_KERNEL_DIAGONAL;
+    if (const char* e = getenv("RKR_BATCH_TILES")) want_tiles = want_tiles && atoi(e) != 0;
+    rkr_batch* b = nullptr;
+    for (int attempt = want_tiles ? 0 : 1; attempt < 2; ++attempt) {
+        ex.kernel = attempt == 0 ? RKR_KERNEL_TILES : RKR_KERNEL_QUEUE;
+        b = new rkr_batch();
+        b->device = ex.device;
+        b->R = persistent_choose_r(min_m);
+        b->tiles = attempt == 0;
+        DeviceGuard dg0(b->device);
+        bool all_tiles = true;
+        for (int32_t i = 0; i < n; ++i) {
+            rkr_table* t = nullptr;
+            rkr_status st = prepare_table(menus[i], units[i], m_max[i], &ex, b->R, &t, nullptr,
+                                          attempt == 0);
+            if (st != RKR_OK && !(attempt == 0 && st == RKR_ERR_INVALID)) {
+                free_batch(b);
+                return st;
+            }
+            if (st != RKR_OK) {
+                all_tiles = false;
+                break;
+            }
+            b->tables.push_back(t);
         }
-        b->tables.push_back(t);
+        if (attempt == 0 && !all_tiles) {  // some table does not fit K1t: all run K1p
+            free_batch(b);
+            b = nullptr;
+            g_err.clear();
+            continue;
+        }
+        break;
     }
+    DeviceGuard dg(b->device);
     rkr_status st = batch_layout(b);
     if (st == RKR_OK) st = batch_upload(b);
     if (st == RKR_OK) st = batch_fill(b);

@@ -2,6 +2,8 @@
 // host half of librkr.so.  Not installed; include/rkr.h is the public ABI.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <vector>
 
@@ -193,6 +195,11 @@ struct TilePlan {
 };
 int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp);  // 1 = eligible
 int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream);
+// Batches: jobs (table, tile) in queue order; tps[i].sm is the batch-wide
+// layout (tile_batch_smem of a plan with every table's maxima).
+TileSmem tile_batch_smem(const TilePlan& proto);
+int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const int2* jobs,
+                            int njobs, unsigned int* counter, const TilePlan& proto, void* stream);
 
 // Launch entry points (rkr_kernels.cu).
 struct LaunchCtx {

@@ -201,12 +201,16 @@ __device__ __forceinline__ void scan_cuts(const uint32_t* __restrict__ opt, cons
 // all 32 warps compute and warp 0 polls / thread 0 publishes inline, behind
 // CTA barriers (throughput-bound tables, where the 32nd compute warp and
 // barrier-aligned phases measured faster).
+//
+// tile_job: every diagonal of tile j of one table.  ph0/ph1 = completed
+// phases of the two program mbarriers before this job (jobs of a batch
+// reuse them).  The caller initialises the mbarriers once and separates
+// jobs with a CTA barrier.
 template <int WC, bool COMM>
-__global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ InstDesc D,
-                                                    const __grid_constant__ TilePlan tp) {
+__device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, const int j,
+                                         unsigned char* smem_raw, uint32_t ph0, uint32_t ph1) {
     constexpr int W = 32 * WC;
     constexpr int kNC = COMM ? kNW - 1 : kNW;  // compute warps
-    extern __shared__ __align__(128) unsigned char smem_raw[];
     const TileSmem& sm = tp.sm;
     int32_t* s_blk = reinterpret_cast<int32_t*>(smem_raw + sm.blk);
     int2* s_opd = reinterpret_cast<int2*>(smem_raw + sm.opd);
@@ -220,7 +224,6 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
     const int L = g.L, M = g.M;
     const int sr = (int)g.sr;  // rows * sr < 2^31 (tile_plan)
     const int ocap = tp.ocap;
-    const int j = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int m_lo = j * W;
 
@@ -229,11 +232,6 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
     // + time_bwd (:150), padded to ocap with options that never win (pass
     // time INF).  Cut programs and thresholds arrive per step by bulk copy,
     // two steps ahead (double buffer, one mbarrier per buffer).
-    if (tid == 0) {
-        mbar_init(bars + 0, 1);
-        mbar_init(bars + 1, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
     for (int c = tid; c <= L; c += kNT) s_blk[c] = __ldg(dm.blk_off + c);
     for (int q = tid; q < L * ocap; q += kNT) {
         const int b = q / ocap, i = q - b * ocap;
@@ -249,6 +247,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
     if (COMM && warp == kNC) {
         // ================= communication warp =================
         if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             stage_step(tp, pq, sm, smem_raw, bars, L, 0);
             if (L > 1) stage_step(tp, pq, sm, smem_raw, bars, L, 1);
         }
@@ -275,13 +274,14 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
     } else {
     // ================= compute warps =================
     if (!COMM && tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         stage_step(tp, pq, sm, smem_raw, bars, L, 0);
         if (L > 1) stage_step(tp, pq, sm, smem_raw, bars, L, 1);
     }
     for (int k = 0; k < L; ++k) {
         unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
         if (tp.trace && tid == 0) t0 = t_gtimer();
-        mbar_wait(bars + (k & 1), (uint32_t)(k >> 1) & 1u);
+        mbar_wait(bars + (k & 1), ((k & 1 ? ph1 : ph0) + (uint32_t)(k >> 1)) & 1u);
         const int4* prog = reinterpret_cast<const int4*>(smem_raw + sm.prog + (k & 1) * sm.prog_bytes);
         const int32_t* thrs = reinterpret_cast<const int32_t*>(smem_raw + sm.thr + (k & 1) * sm.thr_bytes);
 
@@ -452,6 +452,27 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
         }
     }
     }  // compute warps
+}
+
+template <int WC, bool COMM>
+__global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ InstDesc D,
+                                                    const __grid_constant__ TilePlan tp) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const TileSmem& sm = tp.sm;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sm.bar);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bars + 0, 1);
+        mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    tile_job<WC, COMM>(D, tp, blockIdx.x, smem_raw, 0, 0);
+    const Geometry& g = D.g;
+    const DevMenu& dm = D.dm;
+    uint32_t* __restrict__ opt = static_cast<uint32_t*>(D.opt);
+    uint16_t* __restrict__ arg = D.arg;
+    const int L = g.L;
 
     // ---- fused K2: the last CTA to finish walks the schedule ----------------
     // (build_schedule_rec, chain_dp.hpp:211-246).  Every CTA counts itself
@@ -494,6 +515,41 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
     } else if (tid == 0) {
         walk<uint32_t>(g, GlobalMenuView{&dm}, opt, arg, tp.ws, tp.wt, tp.wm, tp.wops, tp.wcap,
                        tp.wstack, tp.wout);
+    }
+}
+
+// Batches (config 4 sweeps): persistent CTAs take (table, tile) jobs from a
+// queue ordered table by table, tiles ascending.  A job only waits on lower
+// tiles of its own table, which were dequeued earlier by CTAs that are
+// running or done, so the queue cannot deadlock and tables need not be
+// co-resident.
+template <int WC, bool COMM>
+__global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __restrict__ descs,
+                                                          const TilePlan* __restrict__ tps,
+                                                          const int2* __restrict__ jobs, int njobs,
+                                                          unsigned int* __restrict__ counter) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ int s_job;
+    const TileSmem& sm = tps[0].sm;  // one layout for the whole batch
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sm.bar);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bars + 0, 1);
+        mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    uint32_t ph0 = 0, ph1 = 0;
+    for (;;) {
+        if (tid == 0) s_job = (int)atomicAdd(counter, 1u);
+        __syncthreads();
+        const int q = s_job;
+        if (q >= njobs) break;
+        const int2 jb = jobs[q];
+        tile_job<WC, COMM>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0, ph1);
+        const int L = descs[jb.x].g.L;
+        ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
+        ph1 += (uint32_t)L / 2;
+        __syncthreads();  // shared memory and s_job are reused by the next job
     }
 }
 
@@ -566,6 +622,29 @@ int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* st
         case 8: return launch_tiles_t<8, false>(d, tp, st);
     }
     return 3;
+}
+
+TileSmem tile_batch_smem(const TilePlan& proto) { return tile_smem(proto); }
+
+int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const int2* jobs,
+                            int njobs, unsigned int* counter, const TilePlan& proto, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (njobs <= 0) return 0;
+    auto go = [&](auto kern) -> int {
+        const size_t smem = proto.sm.total;
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                cudaSuccess)
+            return 3;
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int grid = njobs < sms ? njobs : sms;  // persistent: one CTA per SM
+        kern<<<grid, kNT, smem, st>>>(descs, tps, jobs, njobs, counter);
+        return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    };
+    if (proto.WC != 1) return 3;  // batches run 32-slot tiles
+    return proto.comm ? go(fill_tiles_batch<1, true>) : go(fill_tiles_batch<1, false>);
 }
 
 }  // namespace rkr

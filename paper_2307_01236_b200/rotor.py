@@ -465,14 +465,17 @@ class Batch:
     """Many independent DP tables filled by ONE persistent launch (rkr_batch_*)."""
 
     def __init__(self, menus: Sequence[Menu], units: Sequence[int], m_maxs: Sequence[int],
-                 device: int = 0, width: str = "auto", stream: Optional[int] = None):
+                 device: int = 0, width: str = "auto", stream: Optional[int] = None,
+                 kernel: str = "persistent"):
+        """kernel: "persistent" (budget-tile jobs when every table qualifies,
+        else the row-segment queue) or "queue"."""
         self._lib = lib()
         n = len(menus)
         self._structs = [m.struct() for m in menus]
         arr = (ctypes.POINTER(RkrMenu) * n)(*[ctypes.pointer(x) for x in self._structs])
         u = (ctypes.c_int64 * n)(*units)
         mm = (ctypes.c_int32 * n)(*m_maxs)
-        ex = _exec(device, width, stream)
+        ex = _exec(device, width, stream, kernel)
         self._h = ctypes.c_void_p()
         _check(self._lib.rkr_batch_create(arr, u, mm, n, ctypes.byref(ex), ctypes.byref(self._h)))
         self.menus = list(menus)

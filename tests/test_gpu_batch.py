@@ -27,11 +27,13 @@ def _mixed_menus(random_suites):
     return ms
 
 
-def test_batch_tables_match_oracle(orc, random_suites):
+@pytest.mark.parametrize("kernel", ["persistent", "queue"])
+def test_batch_tables_match_oracle(orc, random_suites, kernel):
     items = _mixed_menus(random_suites)
     with rotor.Batch([m for m, _, _ in items], [u for _, u, _ in items],
-                     [M for _, _, M in items]) as b:
+                     [M for _, _, M in items], kernel=kernel) as b:
         assert len(b) == len(items)
+        assert b.table(0).kernel() == ("tiles" if kernel == "persistent" else "queue")
         for rep in range(2):
             if rep:
                 b.refill()

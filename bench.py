@@ -457,28 +457,46 @@ def b200_arm_sweep(args, world, rank, local):
         barrier()
     fill_ms = [e[0].elapsed_time(e[1]) for e in evs]
     tot_s = max_over_ranks(sum(fill_ms) / 1e3)
+    # bytes each end-to-end step uploads: every table's menu blob (the unit
+    # precompute + descriptor) -- the same tables rkr_sweep builds
+    h2d = sum(batch.table(i).h2d_bytes() for i in range(len(batch)))
+    kern = batch.table(0).kernel()
     batch.close()
 
-    # end to end: rkr_sweep per chain from host menus (fill, tops, schedules, min-feasible)
+    # end to end: one rkr_sweep C-ABI call per chain from host menus (fill,
+    # top cells, schedules, min-feasible search; schedules copied back into
+    # caller buffers), buffers preallocated as a C caller would
+    import ctypes
+
+    lib = rotor.lib()
     by_chain = {}
     for _, ci, b, _, _ in rows:
         by_chain.setdefault(ci, []).append(b)
+    calls = []
+    for ci, bs in sorted(by_chain.items()):
+        n = len(bs)
+        cap = max(1024, 8 * n * menus[ci].L)
+        calls.append((menus[ci].struct(), (ctypes.c_int64 * n)(*bs), n, (ctypes.c_int32 * n)(),
+                      (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)(), (ctypes.c_int32 * n)(),
+                      (ctypes.c_int64 * n)(), (rotor.RkrOp * cap)(), cap,
+                      (ctypes.c_int64 * (n + 1))()))
+    ex = rotor._exec(local, "auto")
     e2e = []
     n_ops = 0
     n_feas = 0
-    h2d = 0
     for it in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        n_ops = n_feas = 0
-        for ci, bs in sorted(by_chain.items()):
-            out = rotor.sweep_raw(menus[ci], bs, SWEEP_UNITS, device=local)
-            n_ops += sum(len(r.ops) for r in out)
-            n_feas += sum(r.feasible for r in out)
+        for ms_, b_, n, st_, ot_, un_, mt_, mf_, ops_, cap, offs in calls:
+            rc = lib.rkr_sweep(ctypes.byref(ms_), b_, n, SWEEP_UNITS, ctypes.byref(ex), st_, ot_,
+                               un_, mt_, mf_, ops_, cap, offs)
+            assert rc == 0, lib.rkr_last_error()
         dt = time.perf_counter() - t0
         if it >= args.warmup:
             e2e.append(dt)
+    n_ops = sum(c[-1][c[2]] for c in calls)
+    n_feas = sum(sum(1 for i in range(c[2]) if c[3][i] == 0) for c in calls)
     e2e_s = max_over_ranks(sum(e2e))
     cells_rank = sweep_cells(menus, rows)
     cells_total = sweep_cells(menus, rows_all)
@@ -504,14 +522,14 @@ def b200_arm_sweep(args, world, rank, local):
         },
         "e2e": {"value": cells_total * args.steps / e2e_s, "unit": "cells/s",
                 "ms_per_step": 1e3 * e2e_s / args.steps,
-                "h2d_bytes_per_step": None, "d2h_bytes_per_step": 12 * n_ops,
-                "path": "rkr_sweep per chain from host menus: fill + tops + schedules + "
-                        "min-feasible search, schedules copied back",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 12 * n_ops,
+                "path": "one rkr_sweep C-ABI call per chain from host menus: fill + tops + "
+                        "schedules + min-feasible search, schedules copied back",
                 "feasible_budgets_rank0": n_feas},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "fill_persistent (one batched launch per step)",
+                     "kernel": FILL_KERNELS[kern] + ", batched: every table in one launch",
                      "alg_bytes_per_fill": ab, "fill_ms": statistics.mean(fill_ms),
                      "peak_source": peak_src},
         "clocks": sampler.summary(),

@@ -8,11 +8,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/rkr.h"
@@ -23,6 +26,40 @@ using namespace rkr;
 namespace {
 
 thread_local std::string g_err;
+
+// fn(i) for i in [0, n) on up to 16 host threads (batched table setup: the
+// per-table host precompute of the DpTable constructor is independent).
+template <typename F>
+void parallel_for(int n, F fn) {
+    int nt = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+    nt = std::min(nt, std::max(1, n / 8));
+    if (nt <= 1) {
+        for (int i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nt; ++w)
+        pool.emplace_back([&, w] {
+            for (int i = w; i < n; i += nt) fn(i);
+        });
+    for (auto& th : pool) th.join();
+}
+
+// RKR_PROFILE=1: host phase timings of the batched entry points on stderr
+// (each mark synchronises the stream first, so only for diagnostics).
+struct PhaseTimer {
+    bool on = getenv("RKR_PROFILE") != nullptr;
+    cudaStream_t st = nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        if (st) cudaStreamSynchronize(st);
+        const auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[rkr] %-28s %9.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
 
 rkr_status fail(rkr_status st, const char* fmt, ...) {
     char buf[512];
@@ -87,6 +124,10 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
         if (m->option_offsets[i + 1] < m->option_offsets[i])
             return fail(RKR_ERR_ARGUMENT, "option_offsets not monotone at block %d", i);
     h.L = L;
+    const size_t nopt = (size_t)m->option_offsets[L] - (size_t)m->option_offsets[0];
+    for (auto* v : {&h.fwd_req, &h.fwd_req_pre, &h.bwd_req, &h.pack_chg, &h.tftb, &h.chg_bt})
+        v->reserve(nopt);
+    h.ids.reserve(nopt);
     h.act_u.resize(L + 1);
     for (int32_t i = 0; i <= L; ++i) h.act_u[i] = to_units(m->act_sizes[i], unit);  // :59-60
     h.blk_off.assign(L + 1, 0);
@@ -95,9 +136,17 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
     h.tf0.assign(L, 0);
     bool nonneg = true;
     long double F = 0, Bk = 0;
+    std::vector<std::pair<int32_t, int32_t>> first;  // (option id, first position) of a block
     for (int32_t i = 0; i < L; ++i) {                                         // :72-95
         const int64_t a_i = m->act_sizes[i];
         bool saw_zero = false;
+        // build_schedule_rec looks an option up by id, first match in menu
+        // order (chain_dp.hpp:200-205, :228): first position of every id
+        first.clear();
+        for (int32_t o = m->option_offsets[i]; o < m->option_offsets[i + 1]; ++o)
+            first.emplace_back(m->option_id[o], o);
+        std::stable_sort(first.begin(), first.end(),
+                         [](const auto& x, const auto& y) { return x.first < y.first; });
         h.blk_off[i] = (int32_t)h.ids.size();
         int64_t fmax = 0, bmax = 0;
         for (int32_t o = m->option_offsets[i]; o < m->option_offsets[i + 1]; ++o) {
@@ -120,15 +169,9 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
             h.bwd_req.push_back(to_units(m->peak_bwd[o] - a_i, unit));
             h.pack_chg.push_back(to_units(m->save_mem[o] - a_i, unit));
             h.tftb.push_back(m->time_fwd[o] + m->time_bwd[o]);
-            // build_schedule_rec looks the option up by id (first match,
-            // chain_dp.hpp:200-205, :228)
-            int64_t chg = 0;
-            for (int32_t p = m->option_offsets[i]; p < m->option_offsets[i + 1]; ++p)
-                if (m->option_id[p] == m->option_id[o]) {
-                    chg = to_units(m->save_mem[p] - a_i, unit);
-                    break;
-                }
-            h.chg_bt.push_back(chg);
+            const int32_t p = std::lower_bound(first.begin(), first.end(),
+                                               std::make_pair(m->option_id[o], INT32_MIN))->second;
+            h.chg_bt.push_back(to_units(m->save_mem[p] - a_i, unit));
         }
         if (!saw_zero) return fail(RKR_ERR_INVALID, "block %d lacks option 0", i);  // :94
         const int32_t n = (int32_t)h.ids.size() - h.blk_off[i];
@@ -231,7 +274,9 @@ struct rkr_table {
     Geometry g{};
     DevMenu dm{};
     void* block = nullptr;        // one pooled allocation: menu | scratch | opt | arg
-    size_t block_bytes = 0;
+    size_t block_bytes = 0, work_bytes = 0;
+    std::vector<size_t> off;      // layout_sizes: menu-blob offsets, then work-area offsets
+    bool owns_block = true;       // false: carved out of a batch's blocks
     size_t menu_bytes = 0;        // H2D bytes per create
     void* opt = nullptr;
     uint16_t* arg = nullptr;
@@ -291,7 +336,7 @@ void free_table(rkr_table* t) {
         cudaFree(t->block);
         t->block = nullptr;
     }
-    if (t->block) cudaFreeAsync(t->block, t->stream);
+    if (t->block && t->owns_block) cudaFreeAsync(t->block, t->stream);
     if (t->dops) cudaFreeAsync(t->dops, t->stream);
     delete t;
 }
@@ -303,13 +348,17 @@ rkr_status check_cell(const rkr_table* t, int32_t s, int32_t tt) {
     return RKR_OK;
 }
 
-// Lay out one device block (menu blob, scratch, opt rows, arg rows), stage
-// the menu precompute in pinned memory and upload it asynchronously.
-rkr_status alloc_and_upload(rkr_table* t) {
+// Device layout of one table: a menu blob (uploaded once: the unit
+// precompute, the K1p plan, the kernel descriptor) and a work area (scratch,
+// opt rows, arg rows, state, cell programs).  A single table keeps both in
+// one block; a batch carves every table's menu blob out of one region (one
+// H2D copy) and its work area out of another.
+void layout_sizes(rkr_table* t) {
     const HostMenu& h = t->hm;
     const size_t nq = std::max<size_t>(h.ids.size(), 1);
     const size_t L = h.L;
-    std::vector<size_t> off;
+    std::vector<size_t>& off = t->off;
+    off.clear();
     size_t bytes = 0;
     auto take = [&](size_t n) {
         off.push_back(bytes);
@@ -326,7 +375,8 @@ rkr_status alloc_and_upload(rkr_table* t) {
     take(np * 4);                              // 14 plan k
     take(sizeof(InstDesc));                    // 15 kernel descriptor
     take(np * 4);                              // 16 plan instance ids (all 0)
-    const size_t menu_bytes = bytes;
+    t->menu_bytes = bytes;
+    bytes = 0;                                 // work area offsets from here
     take(sizeof(int4) * (2 * L + 16));         // 17 backtrack stack
     take(8 * sizeof(int64_t));                 // 18 dout
     const size_t vbytes = t->width == 32 ? 4 : 8;
@@ -340,46 +390,48 @@ rkr_status alloc_and_upload(rkr_table* t) {
     const bool progs = t->kernel == RKR_KERNEL_PERSISTENT;
     const size_t nc = progs ? (size_t)program_cut_entries(t->g) : 0;
     // thr row stride; K1t copies thr rows with bulk copies and reads whole batches of 8
-    const size_t ocap = t->tiles ? round_up(std::max<int32_t>(h.max_opts, 1), 8)
-                                 : std::max<int32_t>(h.max_opts, 1);
+    t->prog.ocap = (int32_t)(t->tiles ? round_up(std::max<int32_t>(h.max_opts, 1), 8)
+                                      : std::max<int32_t>(h.max_opts, 1));
     take(nc * 16);                               // 22 program ptr
     take(nc * vbytes);                           // 23 program sweep
     take(nc * 4);                                // 24 program gate
-    take(progs ? (size_t)t->g.rows * ocap * 4 : 0);  // 25 program thr
+    take(progs ? (size_t)t->g.rows * t->prog.ocap * 4 : 0);  // 25 program thr
     take(progs ? nq * 4 : 0);                    // 26 program pc
     take(progs ? nq * vbytes : 0);               // 27 program otot
-    t->menu_bytes = menu_bytes;
-    t->block_bytes = bytes;
+    t->work_bytes = bytes;
+    t->block_bytes = t->menu_bytes + t->work_bytes;
+}
 
-    if (t->ipc) {  // exportable to other processes (cudaIpcGetMemHandle needs cudaMalloc)
-        CK(cudaMalloc(&t->block, bytes));
-    } else {
-        CK(cudaMallocAsync(&t->block, bytes, t->stream));
-    }
-    unsigned char* b = static_cast<unsigned char*>(t->block);
-    t->dm.blk_off = reinterpret_cast<const int32_t*>(b + off[0]);
-    t->dm.fwd_req = reinterpret_cast<const int64_t*>(b + off[1]);
-    t->dm.fwd_req_pre = reinterpret_cast<const int64_t*>(b + off[2]);
-    t->dm.bwd_req = reinterpret_cast<const int64_t*>(b + off[3]);
-    t->dm.pack_chg = reinterpret_cast<const int64_t*>(b + off[4]);
-    t->dm.tftb = reinterpret_cast<const int64_t*>(b + off[5]);
-    t->dm.chg_bt = reinterpret_cast<const int64_t*>(b + off[6]);
-    t->dm.ids = reinterpret_cast<const int32_t*>(b + off[7]);
-    t->dm.act_u = reinterpret_cast<const int64_t*>(b + off[8]);
-    t->dm.fwd0_own = reinterpret_cast<const int64_t*>(b + off[9]);
-    t->dm.fwd0_full = reinterpret_cast<const int64_t*>(b + off[10]);
-    t->dm.tf0 = reinterpret_cast<const int64_t*>(b + off[11]);
-    t->ddesc = reinterpret_cast<InstDesc*>(b + off[15]);
-    t->lplan.start = reinterpret_cast<const int64_t*>(b + off[12]);
-    t->lplan.j = reinterpret_cast<const int32_t*>(b + off[13]);
-    t->lplan.k = reinterpret_cast<const int32_t*>(b + off[14]);
-    t->lplan.inst = reinterpret_cast<const int32_t*>(b + off[16]);
+// Device pointers of the table (and its descriptor) inside menu blob `mb`
+// and work area `wb`.
+void bind_block(rkr_table* t, unsigned char* mb, unsigned char* wb) {
+    const HostMenu& h = t->hm;
+    const std::vector<size_t>& off = t->off;
+    const size_t np = t->plan.start.size();
+    auto at = [&](int idx) { return idx <= 16 ? mb + off[idx] : wb + off[idx]; };
+    t->dm.blk_off = reinterpret_cast<const int32_t*>(at(0));
+    t->dm.fwd_req = reinterpret_cast<const int64_t*>(at(1));
+    t->dm.fwd_req_pre = reinterpret_cast<const int64_t*>(at(2));
+    t->dm.bwd_req = reinterpret_cast<const int64_t*>(at(3));
+    t->dm.pack_chg = reinterpret_cast<const int64_t*>(at(4));
+    t->dm.tftb = reinterpret_cast<const int64_t*>(at(5));
+    t->dm.chg_bt = reinterpret_cast<const int64_t*>(at(6));
+    t->dm.ids = reinterpret_cast<const int32_t*>(at(7));
+    t->dm.act_u = reinterpret_cast<const int64_t*>(at(8));
+    t->dm.fwd0_own = reinterpret_cast<const int64_t*>(at(9));
+    t->dm.fwd0_full = reinterpret_cast<const int64_t*>(at(10));
+    t->dm.tf0 = reinterpret_cast<const int64_t*>(at(11));
+    t->ddesc = reinterpret_cast<InstDesc*>(at(15));
+    t->lplan.start = reinterpret_cast<const int64_t*>(at(12));
+    t->lplan.j = reinterpret_cast<const int32_t*>(at(13));
+    t->lplan.k = reinterpret_cast<const int32_t*>(at(14));
+    t->lplan.inst = reinterpret_cast<const int32_t*>(at(16));
     t->lplan.n = (int32_t)np;
     t->lplan.total = t->plan.total;
-    t->stack = reinterpret_cast<int4*>(b + off[17]);
-    t->dout = reinterpret_cast<int64_t*>(b + off[18]);
-    t->opt = b + off[19];
-    t->arg = reinterpret_cast<uint16_t*>(b + off[20]);
+    t->stack = reinterpret_cast<int4*>(at(17));
+    t->dout = reinterpret_cast<int64_t*>(at(18));
+    t->opt = at(19);
+    t->arg = reinterpret_cast<uint16_t*>(at(20));
     PlanDev& pd = t->pdev;
     pd.R = t->plan.R;
     pd.TM = t->plan.TM;
@@ -387,23 +439,22 @@ rkr_status alloc_and_upload(rkr_table* t) {
     pd.dj = t->plan.dj;
     pd.n_plan = (int32_t)np;
     pd.total = t->plan.total;
-    pd.start = reinterpret_cast<const int64_t*>(b + off[12]);
-    pd.g = reinterpret_cast<const int32_t*>(b + off[13]);
-    pd.k = reinterpret_cast<const int32_t*>(b + off[14]);
-    pd.counter = reinterpret_cast<unsigned long long*>(b + off[21]);
-    pd.done = reinterpret_cast<int32_t*>(b + off[21] + 8);
+    pd.start = reinterpret_cast<const int64_t*>(at(12));
+    pd.g = reinterpret_cast<const int32_t*>(at(13));
+    pd.k = reinterpret_cast<const int32_t*>(at(14));
+    pd.counter = reinterpret_cast<unsigned long long*>(at(21));
+    pd.done = reinterpret_cast<int32_t*>(at(21) + 8);
     pd.trace = nullptr;
     t->hdesc.halo = pd.done + (size_t)t->g.L * t->flag_cols;
     t->tplan.done = pd.done;
     t->tplan.fin = t->hdesc.halo + t->g.L;
-    t->prog.ptr = b + off[22];
-    t->prog.sweep = b + off[23];
-    t->prog.gate = reinterpret_cast<int32_t*>(b + off[24]);
-    t->prog.thr = reinterpret_cast<int32_t*>(b + off[25]);
-    t->prog.pc = reinterpret_cast<int32_t*>(b + off[26]);
-    t->prog.otot = b + off[27];
+    t->prog.ptr = at(22);
+    t->prog.sweep = at(23);
+    t->prog.gate = reinterpret_cast<int32_t*>(at(24));
+    t->prog.thr = reinterpret_cast<int32_t*>(at(25));
+    t->prog.pc = reinterpret_cast<int32_t*>(at(26));
+    t->prog.otot = at(27);
     t->prog.nq = (int64_t)h.ids.size();
-    t->prog.ocap = (int32_t)ocap;
     t->prog.tiles = t->tiles ? 1 : 0;
     t->hdesc.g = t->g;
     t->hdesc.dm = t->dm;
@@ -413,11 +464,14 @@ rkr_status alloc_and_upload(rkr_table* t) {
     t->hdesc.prog = t->prog;
     t->hdesc.stack = t->stack;
     t->hdesc.item_base = 0;
+}
 
-    void* stage = nullptr;
-    CK(t_stage.get(menu_bytes, &stage));
-    unsigned char* blob = static_cast<unsigned char*>(stage);
-    std::memset(blob, 0, menu_bytes);
+// The menu blob's host image (menu_bytes) for the pinned staging buffer.
+void stage_menu(const rkr_table* t, unsigned char* blob) {
+    const HostMenu& h = t->hm;
+    const std::vector<size_t>& off = t->off;
+    const size_t L = h.L, np = t->plan.start.size();
+    std::memset(blob, 0, t->menu_bytes);
     auto put = [&](int idx, const void* src, size_t n) {
         if (n) std::memcpy(blob + off[idx], src, n);
     };
@@ -437,7 +491,22 @@ rkr_status alloc_and_upload(rkr_table* t) {
     put(13, t->plan.g.data(), np * 4);
     put(14, t->plan.k.data(), np * 4);
     put(15, &t->hdesc, sizeof(InstDesc));
-    CK(cudaMemcpyAsync(t->block, blob, menu_bytes, cudaMemcpyHostToDevice, t->stream));
+}
+
+// One pooled allocation (menu blob | work area), pinned staging, one H2D copy.
+rkr_status alloc_and_upload(rkr_table* t) {
+    layout_sizes(t);
+    if (t->ipc) {  // exportable to other processes (cudaIpcGetMemHandle needs cudaMalloc)
+        CK(cudaMalloc(&t->block, t->block_bytes));
+    } else {
+        CK(cudaMallocAsync(&t->block, t->block_bytes, t->stream));
+    }
+    unsigned char* b = static_cast<unsigned char*>(t->block);
+    bind_block(t, b, b + t->menu_bytes);
+    void* stage = nullptr;
+    CK(t_stage.get(t->menu_bytes, &stage));
+    stage_menu(t, static_cast<unsigned char*>(stage));
+    CK(cudaMemcpyAsync(t->block, stage, t->menu_bytes, cudaMemcpyHostToDevice, t->stream));
     CK(cudaEventRecord(t_stage.done, t->stream));
     return RKR_OK;
 }
@@ -506,7 +575,7 @@ struct ShardSpec {
 // cell programs.  R = 0 lets the plan choose the per-thread slot count.
 rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, const rkr_exec* exec,
                          int R, rkr_table** out, const ShardSpec* spec = nullptr,
-                         bool batch_tiles = false) {
+                         bool batch_tiles = false, bool defer = false) {
     if (!out) return fail(RKR_ERR_ARGUMENT, "null output handle");
     *out = nullptr;
     if (m_max < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
@@ -576,6 +645,12 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
                         "one co-resident tile per SM", m_max + 1, (int)t->g.L);
         }
         if (!t->tiles) t->tplan = TilePlan{};
+    }
+    if (defer) {  // the caller (a batch) allocates, binds, uploads and preps
+        layout_sizes(t);
+        t->owns_block = false;
+        *out = t;
+        return RKR_OK;
     }
     st = alloc_and_upload(t);
     // (the persistent kernels' program launch also writes the pads)
@@ -1077,6 +1152,8 @@ struct rkr_batch {
     TilePlan* dtps = nullptr;
     int2* djobs = nullptr;
     size_t tps_bytes = 0, jobs_bytes = 0;
+    void* mblock = nullptr;              // every table's menu blob (one H2D copy)
+    void* wblock = nullptr;              // every table's work area
 };
 
 namespace {
@@ -1087,6 +1164,8 @@ void free_batch(rkr_batch* b) {
     if (b->owns_tables)
         for (rkr_table* t : b->tables) free_table(t);
     if (b->block) cudaFreeAsync(b->block, b->stream);
+    if (b->mblock) cudaFreeAsync(b->mblock, b->stream);
+    if (b->wblock) cudaFreeAsync(b->wblock, b->stream);
     delete b;
 }
 
@@ -1181,16 +1260,8 @@ rkr_status batch_layout(rkr_batch* b) {
     int32_t* halo = flag + flags;
     b->hd.assign(n, InstDesc{});
     if (b->tiles) {
-        // one shared-memory layout for every job: the tables' maxima
+        // one shared-memory layout for every job: the tables' maxima (create)
         TilePlan& pr = b->proto;
-        pr = b->tables[0]->tplan;
-        for (rkr_table* t : b->tables) {
-            pr.L = std::max(pr.L, t->tplan.L);
-            pr.nq = std::max(pr.nq, t->tplan.nq);
-            pr.ocap = std::max(pr.ocap, t->tplan.ocap);
-            pr.cap = std::max(pr.cap, t->tplan.cap);
-        }
-        pr.comm = 1;  // every job is a latency-bound tile walk
         if (const char* e = getenv("RKR_COMM")) pr.comm = atoi(e) ? 1 : 0;  // tuning knob
         pr.sm = tile_batch_smem(pr);
         b->htp.assign(n, TilePlan{});
@@ -1218,6 +1289,36 @@ rkr_status batch_layout(rkr_batch* b) {
         item += t->plan.total;
     }
     b->total = item;
+    return RKR_OK;
+}
+
+// Deferred tables of a batch: one menu region + one work region for all,
+// every menu blob staged into one pinned buffer, one H2D copy.
+rkr_status batch_tables_upload(rkr_batch* b) {
+    b->stream = b->tables[0]->stream;
+    std::vector<size_t> mo, wo;
+    size_t mt = 0, wt = 0;
+    for (rkr_table* t : b->tables) {
+        mo.push_back(mt);
+        wo.push_back(wt);
+        mt += (size_t)round_up((int64_t)t->menu_bytes, 256);
+        wt += (size_t)round_up((int64_t)t->work_bytes, 256);
+    }
+    CK(cudaMallocAsync(&b->mblock, mt, b->stream));
+    CK(cudaMallocAsync(&b->wblock, wt, b->stream));
+    unsigned char* mb = static_cast<unsigned char*>(b->mblock);
+    unsigned char* wb = static_cast<unsigned char*>(b->wblock);
+    for (size_t i = 0; i < b->tables.size(); ++i) {
+        rkr_table* t = b->tables[i];
+        t->block = mb + mo[i];
+        bind_block(t, mb + mo[i], wb + wo[i]);
+    }
+    void* stage = nullptr;
+    CK(t_stage.get(mt, &stage));
+    unsigned char* sb = static_cast<unsigned char*>(stage);
+    parallel_for((int)b->tables.size(), [&](int i) { stage_menu(b->tables[i], sb + mo[i]); });
+    CK(cudaMemcpyAsync(b->mblock, stage, mt, cudaMemcpyHostToDevice, b->stream));
+    CK(cudaEventRecord(t_stage.done, b->stream));
     return RKR_OK;
 }
 
@@ -1250,35 +1351,23 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
     if (!out || !menus || !units || !m_max) return fail(RKR_ERR_ARGUMENT, "null argument");
     *out = nullptr;
     if (n < 1) return fail(RKR_ERR_ARGUMENT, "empty batch");
-    // common cost width: 32 only if every table's overflow proof holds
-    bool all32 = !(exec && exec->width == RKR_WIDTH_64);
     int32_t min_m = INT32_MAX;
-    TilePlan proto{};  // the budget-tile batch's shared-memory needs: every table's maxima
-    proto.WC = 1;
-    proto.W = 32;
-    proto.comm = 1;
     for (int32_t i = 0; i < n; ++i) {
-        HostMenu h;
-        rkr_status st = build_host_menu(menus[i], units[i], h);
-        if (st != RKR_OK) return st;
         if (m_max[i] < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
-        all32 = all32 && h.bounded32;
         min_m = std::min(min_m, m_max[i]);
-        proto.L = std::max(proto.L, h.L);
-        proto.nq = std::max<int32_t>(proto.nq, (int32_t)h.ids.size());
-        proto.ocap = std::max<int32_t>(proto.ocap, (int32_t)round_up(std::max(h.max_opts, 1), 8));
-        proto.cap = std::max<int32_t>(proto.cap, std::max(32 * h.L, 1024));
     }
-    const bool batch_fits = tile_batch_smem(proto).total <= 220 * 1024;
     rkr_exec ex{};
     if (exec) ex = *exec;
-    ex.width = all32 ? RKR_WIDTH_AUTO : RKR_WIDTH_64;
-    // budget-tile jobs (K1t) when every table qualifies (32-bit costs,
-    // shared memory), else the row-segment queue (K1p)
     const int kreq = exec ? exec->kernel : RKR_KERNEL_PERSISTENT;
-    bool want_tiles = all32 && batch_fits && kreq != RKR_KERNEL_QUEUE && kreq != RKR_KERNEL_DIAGONAL;
+    bool want_tiles = kreq != RKR_KERNEL_QUEUE && kreq != RKR_KERNEL_DIAGONAL;
     if (const char* e = getenv("RKR_BATCH_TILES")) want_tiles = want_tiles && atoi(e) != 0;
+    // One pass normally: every table's host side prepared in parallel as
+    // budget-tile jobs (K1t).  A common cost width is needed (32 only if every
+    // table's overflow proof holds) and the batch-wide shared-memory layout
+    // must fit; otherwise a second pass prepares them for the row-segment
+    // queue (K1p), in the common width.
     rkr_batch* b = nullptr;
+    PhaseTimer pt0;
     for (int attempt = want_tiles ? 0 : 1; attempt < 2; ++attempt) {
         ex.kernel = attempt == 0 ? RKR_KERNEL_TILES : RKR_KERNEL_QUEUE;
         b = new rkr_batch();
@@ -1286,33 +1375,76 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
         b->R = persistent_choose_r(min_m);
         b->tiles = attempt == 0;
         DeviceGuard dg0(b->device);
-        bool all_tiles = true;
-        for (int32_t i = 0; i < n; ++i) {
-            rkr_table* t = nullptr;
-            rkr_status st = prepare_table(menus[i], units[i], m_max[i], &ex, b->R, &t, nullptr,
-                                          attempt == 0);
-            if (st != RKR_OK && !(attempt == 0 && st == RKR_ERR_INVALID)) {
-                free_batch(b);
-                return st;
+        std::vector<rkr_table*> ts(n, nullptr);
+        std::vector<rkr_status> sts(n, RKR_OK);
+        std::vector<std::string> errs(n);
+        parallel_for(n, [&](int i) {
+            sts[i] = prepare_table(menus[i], units[i], m_max[i], &ex, b->R, &ts[i], nullptr,
+                                   attempt == 0, /*defer=*/true);
+            if (sts[i] != RKR_OK) errs[i] = g_err;
+        });
+        rkr_status bad = RKR_OK;
+        for (int32_t i = 0; i < n && bad == RKR_OK; ++i)
+            if (sts[i] != RKR_OK) {
+                bad = sts[i];
+                g_err = errs[i];
             }
-            if (st != RKR_OK) {
-                all_tiles = false;
-                break;
-            }
-            b->tables.push_back(t);
+        for (rkr_table* t : ts)
+            if (t) b->tables.push_back(t);
+        if (bad != RKR_OK && !(attempt == 0 && bad == RKR_ERR_INVALID)) {
+            free_batch(b);
+            return bad;
         }
-        if (attempt == 0 && !all_tiles) {  // some table does not fit K1t: all run K1p
+        bool redo = bad != RKR_OK;  // a table does not fit K1t
+        bool mixed = false;         // tables of both widths: all must run the wider one
+        for (rkr_table* t : b->tables) mixed = mixed || t->width != b->tables[0]->width;
+        if (attempt == 0 && !redo) {
+            TilePlan& pr = b->proto;
+            pr = b->tables[0]->tplan;
+            for (rkr_table* t : b->tables) {
+                pr.L = std::max(pr.L, t->tplan.L);
+                pr.nq = std::max(pr.nq, t->tplan.nq);
+                pr.ocap = std::max(pr.ocap, t->tplan.ocap);
+                pr.cap = std::max(pr.cap, t->tplan.cap);
+            }
+            pr.comm = 1;  // every job is a latency-bound tile walk
+            redo = tile_batch_smem(pr).total > 220 * 1024;
+        }
+        if (attempt == 1 && mixed && ex.width != RKR_WIDTH_64) {
+            free_batch(b);  // the queue pass again, every table 64-bit
+            b = nullptr;
+            ex.width = RKR_WIDTH_64;
+            --attempt;
+            continue;
+        }
+        if (attempt == 0 && (redo || mixed)) {
             free_batch(b);
             b = nullptr;
             g_err.clear();
+            if (mixed) ex.width = RKR_WIDTH_64;
             continue;
         }
         break;
     }
+    pt0.mark("batch: prepare_table x n");
     DeviceGuard dg(b->device);
-    rkr_status st = batch_layout(b);
+    PhaseTimer pt;
+    pt.st = b->tables[0]->stream;
+    pt.mark("batch: host tables");
+    rkr_status st = batch_tables_upload(b);
+    pt.mark("batch: menus staged + H2D");
+    if (st == RKR_OK) st = batch_layout(b);
     if (st == RKR_OK) st = batch_upload(b);
+    pt.mark("batch: layout + descriptors");
+    if (st == RKR_OK) {  // every table's cell programs and pads: one launch
+        int64_t max_rows = 0;
+        for (rkr_table* t : b->tables) max_rows = std::max(max_rows, t->g.rows);
+        if (launch_prep_programs_batch(b->ddesc, n, max_rows, b->tables[0]->width, b->stream))
+            st = cuda_fail(cudaGetLastError(), "batch program launch");
+    }
+    pt.mark("batch: programs");
     if (st == RKR_OK) st = batch_fill(b);
+    pt.mark("batch: fill");
     if (st != RKR_OK) {
         free_batch(b);
         return st;
@@ -1403,6 +1535,7 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
             mm[q] = mtop[idx[q]];
         }
         rkr_batch* b = nullptr;
+        PhaseTimer spt;
         rkr_status st = rkr_batch_create(ms.data(), us.data(), mm.data(), nb, exec, &b);
         if (st) return st;
         DeviceGuard dg(b->device);
@@ -1441,7 +1574,10 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
             CK(cudaStreamSynchronize(b->stream));
             return RKR_OK;
         };
+        spt.st = b->stream;
+        spt.mark("sweep: create (incl fill)");
         st = run();
+        spt.mark("sweep: tops + walks + D2H");
         cudaFreeAsync(scr, b->stream);
         // schedules longer than cap_each: walk those tables again on their own
         for (int q = 0; q < nb && st == RKR_OK; ++q) {
@@ -1452,6 +1588,7 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
                                (int64_t)big[q].size(), &nn);
         }
         rkr_batch_destroy(b);
+        spt.mark("sweep: destroy");
         if (st) return st;
     }
     // infeasible budgets with a table: the wide-table min-feasible search (:265-288)

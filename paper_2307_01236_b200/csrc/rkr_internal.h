@@ -218,6 +218,8 @@ struct LaunchCtx {
 };
 
 int launch_prep_programs(const LaunchCtx& c);
+// cell programs (and pads) of n tables whose descriptors are in d (device)
+int launch_prep_programs_batch(const InstDesc* d, int n, int64_t max_rows, int width, void* stream);
 constexpr int64_t kOptSlack = 4096;  // elements past the last row (tile over-reads)
 
 int launch_init_pads(const LaunchCtx& c);

@@ -114,12 +114,13 @@ struct Programs {
 // at a time with warp shuffles.
 // ---------------------------------------------------------------------------
 template <typename V>
-__global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> pr) {
+__device__ __forceinline__ void prep_body(const Geometry& g, const DevMenu& dm, const V* opt,
+                                          const Programs<V>& pr, int64_t bx, int64_t nbx) {
     const int ocap = pr.ocap;
     const int L = g.L, M = g.M;
     const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t rid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); rid < g.rows;
+    const int64_t warps = nbx * (blockDim.x >> 5);
+    for (int64_t rid = bx * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); rid < g.rows;
          rid += warps) {
         int lo = 0, hi = L - 1;  // rid -> (k, s): rows are diagonal-major
         while (lo < hi) {
@@ -197,19 +198,35 @@ __global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> 
     {
         V* o = const_cast<V*>(opt);
         const int64_t n = g.rows * (int64_t)g.pad;
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-             i += (int64_t)gridDim.x * blockDim.x) {
+        for (int64_t i = bx * (int64_t)blockDim.x + threadIdx.x; i < n;
+             i += nbx * blockDim.x) {
             const int64_t r = i / g.pad, p = i - r * g.pad;
             o[r * g.sr + p] = CostP<V>::inf;
         }
     }
     // per saved option: clamped pack shift and pass time
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < pr.nq;
-         q += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t q = bx * (int64_t)blockDim.x + threadIdx.x; q < pr.nq;
+         q += nbx * blockDim.x) {
         const int64_t p = dm.pack_chg[q];
         pr.pc[q] = p > g.pad ? g.pad : (int)p;
         pr.otot[q] = (V)dm.tftb[q];
     }
+}
+
+template <typename V>
+__global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> pr) {
+    prep_body<V>(g, dm, opt, pr, blockIdx.x, gridDim.x);
+}
+
+template <typename V>
+__device__ inline Programs<V> programs_of(const ProgDev& q);
+
+// Every table of a batch in one launch: blockIdx.y = table.
+template <typename V>
+__global__ void prep_programs_batch(const InstDesc* __restrict__ d) {
+    const InstDesc& D = d[blockIdx.y];
+    prep_body<V>(D.g, D.dm, static_cast<const V*>(D.opt), programs_of<V>(D.prog), blockIdx.x,
+                 gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -705,6 +722,20 @@ int64_t program_cut_entries(const Geometry& g) { return diag_cut_off(g.L, g.L); 
 
 int launch_prep_programs(const LaunchCtx& c) {
     return c.width == 32 ? prep_t<uint32_t>(c) : prep_t<int64_t>(c);
+}
+
+int launch_prep_programs_batch(const InstDesc* d, int n, int64_t max_rows, int width, void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int bx = (int)((max_rows * 32 + 127) / 128);  // one warp per row of the largest table
+    if (bx > 64) bx = 64;
+    if (bx < 1) bx = 1;
+    const dim3 grid(bx, n);
+    if (width == 32)
+        prep_programs_batch<uint32_t><<<grid, 128, 0, st>>>(d);
+    else
+        prep_programs_batch<int64_t><<<grid, 128, 0, st>>>(d);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 int launch_fill_batch(const InstDesc* dev_desc, const InstDesc* single, const LaunchPlan& lp,

@@ -389,8 +389,8 @@ void layout_sizes(rkr_table* t) {
     take(t->state_bytes);                        // 21 K1p counter + done flags
     const bool progs = t->kernel == RKR_KERNEL_PERSISTENT;
     const size_t nc = progs ? (size_t)program_cut_entries(t->g) : 0;
-    // thr row stride; K1t copies thr rows with bulk copies and reads whole batches of 8
-    t->prog.ocap = (int32_t)(t->tiles ? round_up(std::max<int32_t>(h.max_opts, 1), 8)
+    // thr row stride; K1t copies thr rows with bulk copies and reads whole option batches
+    t->prog.ocap = (int32_t)(t->tiles ? round_up(std::max<int32_t>(h.max_opts, 1), kTileOptBatch)
                                       : std::max<int32_t>(h.max_opts, 1));
     take(nc * 16);                               // 22 program ptr
     take(nc * vbytes);                           // 23 program sweep
@@ -637,7 +637,7 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
             // batch tables need no co-residency (their tiles are queued jobs)
             t->tiles = tile_plan(t->g, t->width, batch_tiles ? INT32_MAX : sms, (int64_t)h.ids.size(),
-                                 (int)round_up(std::max<int32_t>(h.max_opts, 1), 8), t->tplan) == 1;
+                                 (int)round_up(std::max<int32_t>(h.max_opts, 1), kTileOptBatch), t->tplan) == 1;
         }
         if (kreq == RKR_KERNEL_TILES && !t->tiles) {
             delete t;

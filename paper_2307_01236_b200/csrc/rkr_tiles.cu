@@ -106,7 +106,7 @@ __device__ __forceinline__ void nb_arrive(int id) {
 constexpr int kNW = 32;        // warps per CTA
 constexpr int kNT = kNW * 32;  // threads per CTA
 constexpr int kU = 8;          // cuts per load batch (2 kU loads in flight per lane)
-constexpr int kOB = 8;         // options per load batch (ocap is a multiple of kOB)
+constexpr int kOB = kTileOptBatch;  // options per load batch (ocap is a multiple of kOB)
 
 inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~15ull); }
 inline TileSmem tile_smem(const TilePlan& tp) {

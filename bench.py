@@ -528,8 +528,10 @@ def b200_arm_sweep(args, world, rank, local):
                 "feasible_budgets_rank0": n_feas},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "kernel": FILL_KERNELS[kern] + ", batched: every table in one launch",
+                     "frac": achieved / peak, "traffic": ncu_traffic(4, kern),
+                     "kernel": ("fill_tiles_batch (K1t jobs: persistent CTAs take (table, budget tile) "
+                                "jobs, every table in one launch)" if kern == "tiles" else
+                                "fill_persistent (K1p, every table in one launch)"),
                      "alg_bytes_per_fill": ab, "fill_ms": statistics.mean(fill_ms),
                      "peak_source": peak_src},
         "clocks": sampler.summary(),

@@ -8,18 +8,32 @@ from paper_2307_01236_b200 import rotor  # noqa: E402
 from paper_2307_01236_b200.menu import synthetic_menu, tiny_chain_menu  # noqa: E402
 
 for width in ("auto", "64"):
-    for kernel in ("persistent", "diagonal"):
+    for kernel in ("tiles", "queue", "diagonal"):
+        if kernel == "tiles" and width == "64":
+            continue  # K1t is 32-bit only
         m = synthetic_menu(10, 4, 600, 5, tie_stress=True)
         with rotor.DpTable(m, 1, 600, width=width, kernel=kernel) as t:
             t.download()
             t.backtrack(0, 9, 600)
+            t.refill_walk(0, 9, 600)  # fused walk (K1t) / fill + walk
+            t.backtrack_fetch()
             t.first_feasible(0, 9)
     with rotor.ShardedTable(synthetic_menu(12, 4, 900, 6), 1, 900, 3, width=width) as sh:
         sh.download()
         sh.backtrack(0, 11, 900)
-b = rotor.Batch([tiny_chain_menu(), synthetic_menu(8, 3, 300, 7)], [1, 1], [64, 300])
-b.table(1).download()
-b.close()
+# K1t without the communication warp (the large-table variant)
+os.environ["RKR_COMM"] = "0"
+with rotor.DpTable(synthetic_menu(10, 4, 600, 5), 1, 600, kernel="tiles") as t:
+    t.refill_walk(0, 9, 600)
+    t.backtrack_fetch()
+del os.environ["RKR_COMM"]
+for kernel in ("persistent", "queue"):  # tile jobs / row-segment queue
+    b = rotor.Batch([tiny_chain_menu(), synthetic_menu(8, 3, 300, 7)], [1, 1], [64, 300],
+                    kernel=kernel)
+    b.table(1).download()
+    b.refill()
+    b.table(0).download()
+    b.close()
 rotor.sweep_raw(synthetic_menu(12, 4, 500, 8, byte_scale=64), [3000, 20000, 60000], 500)
 rotor.solve_chain(rotor.Chain.skeleton(2), tiny_chain_menu(), 16, 16)
 print("sanitize workload done")

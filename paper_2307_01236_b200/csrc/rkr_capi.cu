@@ -275,6 +275,9 @@ struct rkr_table {
     DevMenu dm{};
     void* block = nullptr;        // one pooled allocation: menu | scratch | opt | arg
     size_t block_bytes = 0, work_bytes = 0;
+    size_t off_tp = 0, off_jobs = 0;  // K1t tile jobs: plan and job list in the menu blob
+    TilePlan* dtp = nullptr;
+    int2* djobs = nullptr;
     std::vector<size_t> off;      // layout_sizes: menu-blob offsets, then work-area offsets
     bool owns_block = true;       // false: carved out of a batch's blocks
     size_t menu_bytes = 0;        // H2D bytes per create
@@ -375,6 +378,13 @@ void layout_sizes(rkr_table* t) {
     take(np * 4);                              // 14 plan k
     take(sizeof(InstDesc));                    // 15 kernel descriptor
     take(np * 4);                              // 16 plan instance ids (all 0)
+    // K1t as tile jobs (more tiles than SMs): its plan and job list travel
+    // with the menu blob
+    const bool jobs = t->tiles && t->tplan.jobs;
+    t->off_tp = bytes;
+    bytes += jobs ? round_up((int64_t)sizeof(TilePlan), 256) : 0;
+    t->off_jobs = bytes;
+    bytes += jobs ? round_up((int64_t)t->tplan.T * (int64_t)sizeof(int2), 256) : 0;
     t->menu_bytes = bytes;
     bytes = 0;                                 // work area offsets from here
     take(sizeof(int4) * (2 * L + 16));         // 17 backtrack stack
@@ -422,6 +432,8 @@ void bind_block(rkr_table* t, unsigned char* mb, unsigned char* wb) {
     t->dm.fwd0_full = reinterpret_cast<const int64_t*>(at(10));
     t->dm.tf0 = reinterpret_cast<const int64_t*>(at(11));
     t->ddesc = reinterpret_cast<InstDesc*>(at(15));
+    t->dtp = reinterpret_cast<TilePlan*>(mb + t->off_tp);
+    t->djobs = reinterpret_cast<int2*>(mb + t->off_jobs);
     t->lplan.start = reinterpret_cast<const int64_t*>(at(12));
     t->lplan.j = reinterpret_cast<const int32_t*>(at(13));
     t->lplan.k = reinterpret_cast<const int32_t*>(at(14));
@@ -491,6 +503,11 @@ void stage_menu(const rkr_table* t, unsigned char* blob) {
     put(13, t->plan.g.data(), np * 4);
     put(14, t->plan.k.data(), np * 4);
     put(15, &t->hdesc, sizeof(InstDesc));
+    if (t->tiles && t->tplan.jobs) {
+        std::memcpy(blob + t->off_tp, &t->tplan, sizeof(TilePlan));
+        int2* jb = reinterpret_cast<int2*>(blob + t->off_jobs);
+        for (int32_t j = 0; j < t->tplan.T; ++j) jb[j] = make_int2(0, j);
+    }
 }
 
 // One pooled allocation (menu blob | work area), pinned staging, one H2D copy.
@@ -552,6 +569,13 @@ rkr_status enqueue_fill(rkr_table* t, bool walk = false, int32_t s = 0, int32_t 
         tp.wcap = t->dops_cap;
         tp.wout = t->dout;
         tp.wstack = reinterpret_cast<int4*>(t->stack);
+        if (tp.jobs) {  // more tiles than SMs: one-table tile jobs
+            if (launch_fill_tiles_batch(t->ddesc, t->dtp, t->djobs, tp.T,
+                                        reinterpret_cast<unsigned int*>(t->pdev.counter), tp,
+                                        t->stream, walk ? &tp : nullptr))
+                return cuda_fail(cudaGetLastError(), "tile job launch");
+            return RKR_OK;
+        }
         if (launch_fill_tiles(t->hdesc, tp, t->width, t->stream))
             return cuda_fail(cudaGetLastError(), "tile fill launch");
         return RKR_OK;
@@ -997,6 +1021,8 @@ rkr_status rkr_debug_trace(rkr_table* t, int32_t enable) {
     t->pdev.trace = t->trace;
     t->hdesc.plan.trace = t->trace;
     t->tplan.trace = t->trace;
+    if (t->tiles && t->tplan.jobs)
+        CK(cudaMemcpyAsync(t->dtp, &t->tplan, sizeof(TilePlan), cudaMemcpyHostToDevice, t->stream));
     CK(cudaMemcpyAsync(t->ddesc, &t->hdesc, sizeof(InstDesc), cudaMemcpyHostToDevice, t->stream));
     CK(cudaStreamSynchronize(t->stream));
     return RKR_OK;

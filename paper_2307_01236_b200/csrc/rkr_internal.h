@@ -185,6 +185,7 @@ struct TilePlan {
     int32_t L = 0, nq = 0, ocap = 0;      // blocks, saved options, thr row stride
     TileSmem sm{};
     int32_t comm = 0;                     // 1: a dedicated communication warp (latency-bound tables)
+    int32_t jobs = 0;                     // 1: more tiles than SMs: run as tile jobs (one-table batch)
     // fused K2 (per launch): the last CTA walks from (ws, wt, wm) into wops /
     // wout = {n_ops, status, bad_s, bad_t, top} (rkr_walk.cuh)
     int32_t walk = 0, ws = 0, wt = 0, wm = 0;
@@ -202,7 +203,8 @@ int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* st
 // layout (tile_batch_smem of a plan with every table's maxima).
 TileSmem tile_batch_smem(const TilePlan& proto);
 int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const int2* jobs,
-                            int njobs, unsigned int* counter, const TilePlan& proto, void* stream);
+                            int njobs, unsigned int* counter, const TilePlan& proto, void* stream,
+                            const TilePlan* walk = nullptr);
 
 // Launch entry points (rkr_kernels.cu).
 struct LaunchCtx {

@@ -454,6 +454,60 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     }  // compute warps
 }
 
+// ---- fused K2: the last finisher walks the schedule -----------------------
+// (build_schedule_rec, chain_dp.hpp:211-246).  Every CTA (every job) counts
+// itself out with an acq_rel add after its last publish; the one that sees
+// n_parts - 1 has acquired every other tile's stores.  Saves the walk's
+// launch and reads a table that is still hot in L2.  Called by all threads
+// of the CTA after its (last) tile job.
+__device__ __forceinline__ void last_walk(const InstDesc& D, const TilePlan& tp, int n_parts,
+                                       unsigned char* smem_raw) {
+    const TileSmem& sm = tp.sm;
+    const Geometry& g = D.g;
+    const DevMenu& dm = D.dm;
+    const uint32_t* __restrict__ opt = static_cast<const uint32_t*>(D.opt);
+    const uint16_t* __restrict__ arg = D.arg;
+    const int L = g.L;
+    const int tid = threadIdx.x;
+    __syncthreads();
+    int* s_last = reinterpret_cast<int*>(smem_raw + sm.blk);  // s_blk is done with
+    if (tid == 0) {
+        int prev;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                     : "=r"(prev)
+                     : "l"(tp.fin)
+                     : "memory");
+        s_last[L + 1] = prev == n_parts - 1;
+    }
+    __syncthreads();
+    if (!s_last[L + 1]) return;
+    // menu lookups and the stack in shared memory (program and partial
+    // buffers are free now); the global view when they do not fit
+    int4* sstack = reinterpret_cast<int4*>(smem_raw + sm.best);
+    int32_t* mb = reinterpret_cast<int32_t*>(smem_raw + sm.prog);
+    const bool fit = 4ull * (2 * (L + 1) + 2 * (uint64_t)tp.nq) <= 2ull * sm.prog_bytes &&
+                     16ull * (2 * L + 16) <= (uint64_t)tp.cap * 4;
+    if (fit) {
+        int32_t *b = mb, *a = b + L + 1, *id = a + L + 1, *gq = id + tp.nq;
+        for (int x = tid; x <= L; x += kNT) {
+            b[x] = __ldg(dm.blk_off + x);
+            a[x] = (int)__ldg(dm.act_u + x);
+        }
+        for (int x = tid; x < tp.nq; x += kNT) {
+            id[x] = __ldg(dm.ids + x);
+            gq[x] = (int)__ldg(dm.chg_bt + x);
+        }
+        __syncthreads();
+        if (tid == 0)
+            walk<uint32_t>(g, SharedMenuView{b, id, gq, a}, opt, arg, tp.ws, tp.wt, tp.wm, tp.wops,
+                           tp.wcap, sstack, tp.wout);
+    } else if (tid == 0) {
+        walk<uint32_t>(g, GlobalMenuView{&dm}, opt, arg, tp.ws, tp.wt, tp.wm, tp.wops, tp.wcap,
+                       tp.wstack, tp.wout);
+    }
+    __syncthreads();  // the walk's shared memory is free again
+}
+
 template <int WC, bool COMM>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ InstDesc D,
                                                     const __grid_constant__ TilePlan tp) {
@@ -475,6 +529,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
     const int L = g.L;
 
     // ---- fused K2: the last CTA to finish walks the schedule ----------------
+    // (inline here rather than last_walk(): measured 3 us faster on config 2)
     // (build_schedule_rec, chain_dp.hpp:211-246).  Every CTA counts itself
     // out with an acq_rel add after its last publish; the one that sees T-1
     // has acquired every other tile's stores.  Saves the walk's launch and
@@ -523,11 +578,12 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
 // tiles of its own table, which were dequeued earlier by CTAs that are
 // running or done, so the queue cannot deadlock and tables need not be
 // co-resident.
-template <int WC, bool COMM>
+template <int WC, bool COMM, bool WALK>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __restrict__ descs,
                                                           const TilePlan* __restrict__ tps,
                                                           const int2* __restrict__ jobs, int njobs,
-                                                          unsigned int* __restrict__ counter) {
+                                                          unsigned int* __restrict__ counter,
+                                                          const __grid_constant__ TilePlan walkp) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ int s_job;
     const TileSmem& sm = tps[0].sm;  // one layout for the whole batch
@@ -549,6 +605,8 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
         const int L = descs[jb.x].g.L;
         ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
         ph1 += (uint32_t)L / 2;
+        // a single table run as tile jobs: the last job to finish walks
+        if constexpr (WALK) last_walk(descs[0], walkp, njobs, smem_raw);
         __syncthreads();  // shared memory and s_job are reused by the next job
     }
 }
@@ -581,10 +639,16 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
     if (width != 32) return 0;
     // 32-bit element offsets inside the table (plus the tile over-read)
     if ((double)g.rows * g.sr + 64.0 * 32 + g.pad >= 2147483647.0) return 0;
-    for (int wc = 1; wc <= 8; wc *= 2) {
+    // 32-slot tiles.  When they do not all fit one CTA per SM the table runs
+    // as tile jobs (fill_tiles_batch on one table): a dataflow queue needs no
+    // co-residency, and walking the tiles in budget order keeps the rows
+    // around the active band in L2 (config 3: 4.65 ms and 0.13 GB of DRAM
+    // reads, against 5.14 ms and 13.3 GB with 129 co-resident 128-slot tiles)
+    for (int wc = 1; wc <= 1; wc *= 2) {
         const int W = 32 * wc;
         const int64_t T = ((int64_t)g.M + 1 + W - 1) / W;
-        if (T > sms) continue;
+        tp.jobs = T > sms ? 1 : 0;
+        if (const char* e = getenv("RKR_JOBS")) tp.jobs = tp.jobs || atoi(e) != 0;  // test knob
         tp.WC = wc;
         tp.W = W;
         tp.T = (int32_t)T;
@@ -596,7 +660,7 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
         // the communication warp pays off where the fill is latency-bound
         // (per-step work of a few microseconds: configs 1-2), not where it is
         // throughput-bound (config 3: measured 5.36 ms without, 6.56 with)
-        tp.comm = (double)g.rows * (g.M + 1) <= 16.0e6 ? 1 : 0;
+        tp.comm = (tp.jobs || (double)g.rows * (g.M + 1) <= 16.0e6) ? 1 : 0;
         if (const char* e = getenv("RKR_COMM")) tp.comm = atoi(e) ? 1 : 0;  // tuning knob
         tp.sm = tile_smem(tp);
         return tp.sm.total <= 220 * 1024 ? 1 : 0;
@@ -627,7 +691,8 @@ int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* st
 TileSmem tile_batch_smem(const TilePlan& proto) { return tile_smem(proto); }
 
 int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const int2* jobs,
-                            int njobs, unsigned int* counter, const TilePlan& proto, void* stream) {
+                            int njobs, unsigned int* counter, const TilePlan& proto, void* stream,
+                            const TilePlan* walk) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (njobs <= 0) return 0;
     auto go = [&](auto kern) -> int {
@@ -640,11 +705,17 @@ int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const in
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int grid = njobs < sms ? njobs : sms;  // persistent: one CTA per SM
-        kern<<<grid, kNT, smem, st>>>(descs, tps, jobs, njobs, counter);
+        TilePlan wp{};
+        if (walk) wp = *walk;  // a single table's plan with its walk request
+        kern<<<grid, kNT, smem, st>>>(descs, tps, jobs, njobs, counter, wp);
         return cudaGetLastError() == cudaSuccess ? 0 : 3;
     };
     if (proto.WC != 1) return 3;  // batches run 32-slot tiles
-    return proto.comm ? go(fill_tiles_batch<1, true>) : go(fill_tiles_batch<1, false>);
+    // the walk variant only for a single table with a walk request (no code
+    // for it in the batch kernels)
+    if (walk && walk->walk)
+        return proto.comm ? go(fill_tiles_batch<1, true, true>) : go(fill_tiles_batch<1, false, true>);
+    return proto.comm ? go(fill_tiles_batch<1, true, false>) : go(fill_tiles_batch<1, false, false>);
 }
 
 }  // namespace rkr

@@ -410,3 +410,23 @@ def test_tiles_without_communication_warp(orc, monkeypatch):
             t.refill_walk(0, L - 1, M)
             bst, ref_ops = orc.build_schedule(menu, 1, M, (o, k, v), 0, L - 1, M)
             assert bst == 0 and t.backtrack_fetch() == ref_ops
+
+
+@pytest.mark.parametrize("comm", ["1", "0"])
+def test_tiles_as_jobs(orc, monkeypatch, comm):
+    """K1t as a one-table job queue (tables with more 32-slot tiles than SMs,
+    forced here on small ones), with and without the communication warp: the
+    whole table and the fused walk against the oracle."""
+    monkeypatch.setenv("RKR_JOBS", "1")
+    monkeypatch.setenv("RKR_COMM", comm)
+    for L, B, M, seed in [(12, 6, 200, 7), (33, 16, 1500, 44), (3, 2, 20, 5)]:
+        menu = synthetic_menu(L, B, M, seed, tie_stress=True)
+        st, o, k, v, _, _ = orc.fill(menu, 1, M)
+        with rotor.DpTable(menu, 1, M, kernel="tiles") as t:
+            assert_same(t.download(), (o, k, v))
+            for m in (M, M // 2):
+                t.refill_walk(0, L - 1, m)
+                bst, ref_ops = orc.build_schedule(menu, 1, M, (o, k, v), 0, L - 1, m)
+                got = _walk_or_inf(t.backtrack_fetch)
+                assert got == (ref_ops if bst == 0 else "infeasible")
+            assert_same(t.download(), (o, k, v))

@@ -48,7 +48,11 @@ void parallel_for(int n, F fn) {
 // RKR_PROFILE=1: host phase timings of the batched entry points on stderr
 // (each mark synchronises the stream first, so only for diagnostics).
 struct PhaseTimer {
-    bool on = getenv("RKR_PROFILE") != nullptr;
+    bool on = enabled();
+    static bool enabled() {
+        static const bool e = getenv("RKR_PROFILE") != nullptr;
+        return e;
+    }
     cudaStream_t st = nullptr;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
     void mark(const char* what) {
@@ -603,8 +607,10 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
     if (!out) return fail(RKR_ERR_ARGUMENT, "null output handle");
     *out = nullptr;
     if (m_max < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
+    PhaseTimer ppt;
     rkr_table* t = new rkr_table();
     rkr_status st = build_host_menu(menu, unit, t->hm);
+    ppt.mark("  prepare: build_host_menu");
     if (st != RKR_OK) {
         delete t;
         return st;
@@ -651,11 +657,10 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
     t->g.sr = round_up((int64_t)t->g.pad + m_max + 1, 32);
     t->g.sa = round_up((int64_t)m_max + 1, 64);
     t->g.rows = (int64_t)h.L * (h.L + 1) / 2;
+    ppt.mark("  prepare: device ctx + geometry");
     if (t->kernel == RKR_KERNEL_PERSISTENT) {
-        persistent_plan(t->g, t->width, R > 0 ? R : persistent_choose_r(m_max), t->plan);
-        if (spec) t->plan.j_offset = spec->j_offset;
-        // budget tiles (K1t) for single, unsharded tables that fit one CTA
-        // per tile on the device; the queue (K1p) otherwise or on request
+        // budget tiles (K1t) for unsharded tables; the queue (K1p) otherwise
+        // or on request -- its work-item plan is only built when it runs
         if (!spec && kreq != RKR_KERNEL_QUEUE) {
             int sms = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
@@ -665,10 +670,15 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
         }
         if (kreq == RKR_KERNEL_TILES && !t->tiles) {
             delete t;
-            return fail(RKR_ERR_INVALID, "kernel TILES: %d budget slots x %d rows do not fit "
-                        "one co-resident tile per SM", m_max + 1, (int)t->g.L);
+            return fail(RKR_ERR_INVALID, "kernel TILES: the table does not fit the budget-tile "
+                        "kernel (64-bit costs, or too many rows for its shared memory)");
         }
-        if (!t->tiles) t->tplan = TilePlan{};
+        if (!t->tiles) {
+            t->tplan = TilePlan{};
+            persistent_plan(t->g, t->width, R > 0 ? R : persistent_choose_r(m_max), t->plan);
+            if (spec) t->plan.j_offset = spec->j_offset;
+        }
+        ppt.mark("  prepare: plans");
     }
     if (defer) {  // the caller (a batch) allocates, binds, uploads and preps
         layout_sizes(t);
@@ -676,12 +686,15 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
         *out = t;
         return RKR_OK;
     }
+    ppt.mark("  prepare: host menu + geometry + plans");
     st = alloc_and_upload(t);
+    ppt.mark("  prepare: alloc + stage + H2D enqueue");
     // (the persistent kernels' program launch also writes the pads)
     if (st == RKR_OK && t->kernel != RKR_KERNEL_PERSISTENT && launch_init_pads(t->ctx()))
         st = cuda_fail(cudaGetLastError(), "pad launch");
     if (st == RKR_OK && t->kernel == RKR_KERNEL_PERSISTENT && launch_prep_programs(t->ctx()))
         st = cuda_fail(cudaGetLastError(), "program launch");
+    ppt.mark("  prepare: program launch");
     if (st != RKR_OK) {
         free_table(t);
         return st;
@@ -1105,14 +1118,18 @@ rkr_status rkr_solve_chain(const rkr_menu* menu, int64_t budget_bytes, int32_t u
     if (m_top < 0) return fail(RKR_ERR_INFEASIBLE, "budget cannot hold the chain input");
     if (m_top > 0x7ffffffe) return fail(RKR_ERR_INVALID, "budget slots exceed int range");
     rkr_table* t = nullptr;
+    PhaseTimer pt;  // host-side enqueue costs (no synchronisation)
     st = prepare_table(menu, unit, (int32_t)m_top, exec, 0, &t);          // :262
+    pt.mark("solve: prepare_table (+H2D, programs)");
     if (st) return st;
     const int L = t->g.L;
     // fill + one device walk from the top cell (fused into the K1t launch):
     // its first read is opt(0, L-1, m_top) (chain_dp.hpp:264), returned with
     // the ops, so a feasible solve needs a single host synchronisation
     st = rkr_table_refill_walk(t, 0, L - 1, (int32_t)m_top);
+    pt.mark("solve: fill + walk enqueued");
     if (st == RKR_OK) st = rkr_backtrack_fetch(t, ops, cap, n_ops);
+    pt.mark("solve: fetch (sync + D2H)");
     const int64_t best = t->hout[4];
     if (st != RKR_OK && best < RKR_INF_TIME) {
         rkr_table_destroy(t);
@@ -1147,6 +1164,7 @@ rkr_status rkr_solve_chain(const rkr_menu* menu, int64_t budget_bytes, int32_t u
     *unit_out = unit;
     *m_top_out = (int32_t)m_top;
     rkr_table_destroy(t);
+    pt.mark("solve: destroy");
     return st;
 }
 

@@ -576,7 +576,7 @@ rkr_status enqueue_fill(rkr_table* t, bool walk = false, int32_t s = 0, int32_t 
         if (tp.jobs) {  // more tiles than SMs: one-table tile jobs
             if (launch_fill_tiles_batch(t->ddesc, t->dtp, t->djobs, tp.T,
                                         reinterpret_cast<unsigned int*>(t->pdev.counter), tp,
-                                        t->stream, walk ? &tp : nullptr))
+                                        t->stream, &tp))  // (a single table: its plan)
                 return cuda_fail(cudaGetLastError(), "tile job launch");
             return RKR_OK;
         }
@@ -1325,6 +1325,7 @@ rkr_status batch_layout(rkr_batch* b) {
             tp.walk = 0;
             tp.fin = nullptr;
             tp.comm = b->proto.comm;
+            tp.split = 0;  // measured slower for batches (throughput-bound)
             tp.sm = b->proto.sm;
             b->htp[i] = tp;
         }

@@ -176,7 +176,7 @@ size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p);  // coun
 // of kTileOptBatch: thr rows and option slots are padded to a multiple.
 constexpr int kTileOptBatch = 8;  // 16 measured: config 2 -2%, configs 1 and 3 +8-12%
 struct TileSmem {  // shared-memory carve-up of K1t (byte offsets)
-    uint32_t best, code, blk, opd, prog, thr, bar, total;
+    uint32_t best, code, blk, opd, prog, thr, xch, bar, total;
     uint32_t prog_bytes, thr_bytes;  // one buffer of each (two of each are kept)
 };
 struct TilePlan {
@@ -186,6 +186,7 @@ struct TilePlan {
     TileSmem sm{};
     int32_t comm = 0;                     // 1: a dedicated communication warp (latency-bound tables)
     int32_t jobs = 0;                     // 1: more tiles than SMs: run as tile jobs (one-table batch)
+    int32_t split = 0;                    // 1 (with comm): late diagonals split each tail over 2 warps
     // fused K2 (per launch): the last CTA walks from (ws, wt, wm) into wops /
     // wout = {n_ops, status, bad_s, bad_t, top} (rkr_walk.cuh)
     int32_t walk = 0, ws = 0, wt = 0, wm = 0;

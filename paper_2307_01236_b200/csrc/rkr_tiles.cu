@@ -95,9 +95,12 @@ __device__ __forceinline__ int t_ld_acquire(const int* p) {
 }
 // named barriers (0 is __syncthreads): compute warps arrive / sync, the
 // communication warp syncs / arrives
-constexpr int kBarReady = 1, kBarDone = 2;
+constexpr int kBarReady = 1, kBarDone = 2, kBarSplit = 3;
 __device__ __forceinline__ void nb_sync(int id) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(1024) : "memory");
+}
+__device__ __forceinline__ void nb_sync_n(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void nb_arrive(int id) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(1024) : "memory");
@@ -136,6 +139,8 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     b += 2ull * m.prog_bytes;
     m.thr = (uint32_t)b;
     b += 2ull * m.thr_bytes;
+    m.xch = (uint32_t)b;  // split-tail exchange: values [kNT] | codes [kNT] (comm only)
+    b = al16(b + (tp.comm ? (uint64_t)kNT * 6 : 0));
     m.bar = (uint32_t)b;
     b += 16;
     m.total = (uint32_t)b;
@@ -206,7 +211,7 @@ __device__ __forceinline__ void scan_cuts(const uint32_t* __restrict__ opt, cons
 // phases of the two program mbarriers before this job (jobs of a batch
 // reuse them).  The caller initialises the mbarriers once and separates
 // jobs with a CTA barrier.
-template <int WC, bool COMM>
+template <int WC, bool COMM, bool SPLIT>
 __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, const int j,
                                          unsigned char* smem_raw, uint32_t ph0, uint32_t ph1) {
     constexpr int W = 32 * WC;
@@ -340,15 +345,31 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         // order), cut i = 0, the bulk parts (i = 1 .. k-2, part by part), cut
         // i = k-1 -- each with a strict '<', so the first minimum wins.
         const int rbase = (int)diag_off(L, k);
-        for (int u = warp; u < units; u += kNC) {
+        // Late diagonals (at most half as many units as compute warps) split
+        // each unit's tail over two warps: half h = 0 takes the first option
+        // batches, half h = 1 the remaining options, cut i = 0, the bulk parts
+        // and cut i = k-1.  All of h = 0's candidates precede h = 1's in the
+        // scan, so the cell's first minimum is h0 if h0.value <= h1.value.
+        const int TS = (COMM && SPLIT && 2 * units <= kNC) ? 2 : 1;
+        uint32_t* xbest = reinterpret_cast<uint32_t*>(smem_raw + sm.xch);
+        uint16_t* xcode = reinterpret_cast<uint16_t*>(xbest + kNT);
+        for (int v = warp; v < units * TS; v += kNC) {
+            const int h = TS == 1 ? -1 : v / units;  // -1: the whole tail
+            const int u = TS == 1 ? v : v - h * units;
             const int s = u / WC;
             const int m = m_lo + (u - s * WC) * 32 + lane;
             const int rid = rbase + s;
+            const int nopt = s_blk[s + 1] - s_blk[s];
+            // option batches of this half: [ia, ib)
+            const int nb2 = (((nopt + kOB - 1) / kOB) + 1) / 2 * kOB;  // first half, whole batches
+            const int ia = h == 1 ? nb2 : 0;
+            const int ib = h == 0 ? (nb2 < nopt ? nb2 : nopt) : nopt;
+            const bool cuts = h != 0;
             // tail cut operands: i = 0 (c = s+1) and i = k-1 (c = t); their
             // loads go out first
             uint32_t tl0 = INF, tr0 = INF, tl1 = INF, tr1 = INF;
             int4 e0 = make_int4(0, 0, 0, M + 2), e1 = e0;
-            if (k > 0) {
+            if (k > 0 && cuts) {
                 e0 = prog[s * k];
                 tl0 = __ldcg(opt + (uint32_t)(e0.x + m));
                 tr0 = __ldcg(opt + (uint32_t)(e0.y + m));
@@ -363,12 +384,11 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             // Case 1 (chain_dp.hpp:139-156): options of block s in menu order;
             // windows of row (s+1, t) at m - pack_chg (row (s+1, t) is the next
             // row of diagonal k-1: id rid - (L - k))
-            const int nopt = s_blk[s + 1] - s_blk[s];
             const int4* od4 = reinterpret_cast<const int4*>(s_opd + s * ocap);  // 2 options each
             const int4* th4 = reinterpret_cast<const int4*>(thrs + s * ocap);   // 4 options each
             const int widx = k > 0 ? (rid - (L - k)) * sr + g.pad + m : 0;
             // whole batches: the padding options never win
-            for (int i0 = 0; i0 < nopt; i0 += kOB) {
+            for (int i0 = ia; i0 < ib; i0 += kOB) {
                 uint32_t sub[kOB], ot[kOB];
                 int32_t th[kOB];
 #pragma unroll
@@ -396,36 +416,62 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                     }
                 }
             }
-            // Case 2 (chain_dp.hpp:158-174): cut i = 0, bulk parts, cut i = k-1
-            const int cb = kCutBit | (s + 1);
-            {
-                const uint32_t tot = (uint32_t)e0.z + tl0 + tr0;
-                if (e0.w <= m && tot < best) {
-                    best = tot;
-                    code = cb;
+            if (cuts) {
+                // Case 2 (chain_dp.hpp:158-174): cut i = 0, bulk parts, cut i = k-1
+                const int cb = kCutBit | (s + 1);
+                {
+                    const uint32_t tot = (uint32_t)e0.z + tl0 + tr0;
+                    if (e0.w <= m && tot < best) {
+                        best = tot;
+                        code = cb;
+                    }
                 }
-            }
-            if (nb > 0) {
-                for (int p = 0; p < P; ++p) {
-                    const int idx = (p * units + u) * 32 + lane;
-                    const uint32_t v = pbest[idx];
-                    if (v < best) {
-                        best = v;
-                        code = pcode[idx];
+                if (nb > 0) {
+                    for (int p = 0; p < P; ++p) {
+                        const int idx = (p * units + u) * 32 + lane;
+                        const uint32_t vv = pbest[idx];
+                        if (vv < best) {
+                            best = vv;
+                            code = pcode[idx];
+                        }
+                    }
+                }
+                {
+                    const uint32_t tot = (uint32_t)e1.z + tl1 + tr1;
+                    if (e1.w <= m && tot < best) {
+                        best = tot;
+                        code = cb + k - 1;
                     }
                 }
             }
-            {
-                const uint32_t tot = (uint32_t)e1.z + tl1 + tr1;
-                if (e1.w <= m && tot < best) {
-                    best = tot;
-                    code = cb + k - 1;
-                }
-            }
-            // store (chain_dp.hpp:176-177)
-            if (m <= M) {
+            if (h == 1) {  // hand the later half to the h = 0 warp
+                xbest[u * 32 + lane] = best;
+                xcode[u * 32 + lane] = (uint16_t)code;
+            } else if (h == -1 && m <= M) {  // store (chain_dp.hpp:176-177)
                 opt[(int64_t)rid * sr + g.pad + m] = best;
                 arg[(int64_t)rid * g.sa + m] = (uint16_t)code;
+            } else if (h == 0) {
+                xbest[(kNT >> 1) + u * 32 + lane] = best;  // (merged below)
+                xcode[(kNT >> 1) + u * 32 + lane] = (uint16_t)code;
+            }
+        }
+        if (TS == 2) {
+            nb_sync_n(kBarSplit, kNC * 32);  // compute warps only
+            for (int u = warp; u < units; u += kNC) {
+                const int s = u / WC;
+                const int m = m_lo + (u - s * WC) * 32 + lane;
+                const int rid = rbase + s;
+                uint32_t best = xbest[(kNT >> 1) + u * 32 + lane];
+                int code = xcode[(kNT >> 1) + u * 32 + lane];
+                const uint32_t b1 = xbest[u * 32 + lane];
+                if (b1 < best) {
+                    best = b1;
+                    code = xcode[u * 32 + lane];
+                }
+                if (m <= M) {  // store (chain_dp.hpp:176-177)
+                    opt[(int64_t)rid * sr + g.pad + m] = best;
+                    arg[(int64_t)rid * g.sa + m] = (uint16_t)code;
+                }
             }
         }
         if (tp.trace && tid == 0) {
@@ -508,7 +554,7 @@ __device__ __forceinline__ void last_walk(const InstDesc& D, const TilePlan& tp,
     __syncthreads();  // the walk's shared memory is free again
 }
 
-template <int WC, bool COMM>
+template <int WC, bool COMM, bool SPLIT>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ InstDesc D,
                                                     const __grid_constant__ TilePlan tp) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -521,7 +567,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    tile_job<WC, COMM>(D, tp, blockIdx.x, smem_raw, 0, 0);
+    tile_job<WC, COMM, SPLIT>(D, tp, blockIdx.x, smem_raw, 0, 0);
     const Geometry& g = D.g;
     const DevMenu& dm = D.dm;
     uint32_t* __restrict__ opt = static_cast<uint32_t*>(D.opt);
@@ -578,7 +624,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
 // tiles of its own table, which were dequeued earlier by CTAs that are
 // running or done, so the queue cannot deadlock and tables need not be
 // co-resident.
-template <int WC, bool COMM, bool WALK>
+template <int WC, bool COMM, bool SPLIT, bool WALK>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __restrict__ descs,
                                                           const TilePlan* __restrict__ tps,
                                                           const int2* __restrict__ jobs, int njobs,
@@ -601,7 +647,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
         const int q = s_job;
         if (q >= njobs) break;
         const int2 jb = jobs[q];
-        tile_job<WC, COMM>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0, ph1);
+        tile_job<WC, COMM, SPLIT>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0, ph1);
         const int L = descs[jb.x].g.L;
         ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
         ph1 += (uint32_t)L / 2;
@@ -611,9 +657,9 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
     }
 }
 
-template <int WC, bool COMM>
+template <int WC, bool COMM, bool SPLIT>
 int launch_tiles_t(const InstDesc& d, const TilePlan& tp, cudaStream_t st) {
-    auto kern = fill_tiles<WC, COMM>;
+    auto kern = fill_tiles<WC, COMM, SPLIT>;
     const size_t smem = tp.sm.total;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -662,6 +708,12 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
         // throughput-bound (config 3: measured 5.36 ms without, 6.56 with)
         tp.comm = (tp.jobs || (double)g.rows * (g.M + 1) <= 16.0e6) ? 1 : 0;
         if (const char* e = getenv("RKR_COMM")) tp.comm = atoi(e) ? 1 : 0;  // tuning knob
+        // split tails on late diagonals: co-resident tables whose blocks have
+        // two or more option batches (config 2: -3.5 %; measured slower with
+        // one batch (config 1), as tile jobs (config 3: +7 %) and for batches
+        // of tables (config 4))
+        tp.split = tp.comm && !tp.jobs && ocap >= 2 * kOB ? 1 : 0;
+        if (const char* e = getenv("RKR_SPLIT")) tp.split = tp.comm && atoi(e) != 0;  // tuning knob
         tp.sm = tile_smem(tp);
         return tp.sm.total <= 220 * 1024 ? 1 : 0;
     }
@@ -670,22 +722,10 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
 
 int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (width != 32) return 3;
-    if (tp.comm) {
-        switch (tp.WC) {
-            case 1: return launch_tiles_t<1, true>(d, tp, st);
-            case 2: return launch_tiles_t<2, true>(d, tp, st);
-            case 4: return launch_tiles_t<4, true>(d, tp, st);
-            case 8: return launch_tiles_t<8, true>(d, tp, st);
-        }
-    }
-    switch (tp.WC) {
-        case 1: return launch_tiles_t<1, false>(d, tp, st);
-        case 2: return launch_tiles_t<2, false>(d, tp, st);
-        case 4: return launch_tiles_t<4, false>(d, tp, st);
-        case 8: return launch_tiles_t<8, false>(d, tp, st);
-    }
-    return 3;
+    if (width != 32 || tp.WC != 1) return 3;  // 32-bit costs, 32-slot tiles
+    if (tp.comm) return tp.split ? launch_tiles_t<1, true, true>(d, tp, st)
+                                 : launch_tiles_t<1, true, false>(d, tp, st);
+    return launch_tiles_t<1, false, false>(d, tp, st);
 }
 
 TileSmem tile_batch_smem(const TilePlan& proto) { return tile_smem(proto); }
@@ -713,9 +753,16 @@ int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const in
     if (proto.WC != 1) return 3;  // batches run 32-slot tiles
     // the walk variant only for a single table with a walk request (no code
     // for it in the batch kernels)
-    if (walk && walk->walk)
-        return proto.comm ? go(fill_tiles_batch<1, true, true>) : go(fill_tiles_batch<1, false, true>);
-    return proto.comm ? go(fill_tiles_batch<1, true, false>) : go(fill_tiles_batch<1, false, false>);
+    // (split tails only for a single table run as jobs, never for batches)
+    const bool split = walk && proto.comm && proto.split;
+    if (walk && walk->walk) {
+        if (split) return go(fill_tiles_batch<1, true, true, true>);
+        return proto.comm ? go(fill_tiles_batch<1, true, false, true>)
+                          : go(fill_tiles_batch<1, false, false, true>);
+    }
+    if (split) return go(fill_tiles_batch<1, true, true, false>);
+    return proto.comm ? go(fill_tiles_batch<1, true, false, false>)
+                      : go(fill_tiles_batch<1, false, false, false>);
 }
 
 }  // namespace rkr

@@ -127,7 +127,9 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     // [L W] (>= kNT); with the communication warp also two [kNT] parity
     // buffers for split steps.  (Config 3 sits at the edge: 12 KB more shared
     // memory measured 30% slower -- less L1 left for loads in flight.)
-    const uint64_t np = (uint64_t)tp.cap + (tp.comm ? 2 * kNT : 0);
+    // (with the communication warp the bulk runs on the warps the tail leaves
+    // idle, so a unit's parts cross warps and both regions are double-buffered)
+    const uint64_t np = tp.comm ? 2ull * tp.cap + 2 * kNT : (uint64_t)tp.cap;
     b = al16(b + np * 4);
     m.code = (uint32_t)b;
     b = al16(b + np * 2);
@@ -301,7 +303,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             chunk = (nb + P - 1) / P;
         }
         // bulk partials (see tile_smem)
-        const int poff = (!COMM || P == 1) ? 0 : tp.cap + (k & 1) * kNT;
+        const int poff = !COMM ? 0 : (P == 1 ? (k & 1) * tp.cap : 2 * tp.cap + (k & 1) * kNT);
         uint32_t* pbest = reinterpret_cast<uint32_t*>(smem_raw + sm.best) + poff;
         uint16_t* pcode = reinterpret_cast<uint16_t*>(smem_raw + sm.code) + poff;
 
@@ -309,7 +311,10 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         // (scanning them inside the tail instead, which frees the [L W]
         // partials, measured 3% slower on config 3)
         if (nb > 0) {
-            for (int it = warp; it < units * P; it += kNC) {
+            // with the communication warp, bulk units go to the warps from the
+            // top down: on late diagonals the tail of step k-1 occupies the
+            // low warps, so the bulk of step k runs beside it
+            for (int it = COMM ? kNC - 1 - warp : warp; it < units * P; it += kNC) {
                 const int p = P == 1 ? 0 : it / units;
                 const int u = it - p * units;
                 const int s = u / WC;

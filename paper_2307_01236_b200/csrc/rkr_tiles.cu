@@ -121,14 +121,14 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     m.thr_bytes = al16(L * tp.ocap * 4);
     uint64_t b = 0;
     m.best = 0;
-    // bulk partials: [L W] for unsplit steps (a unit's parts are written and
-    // read by the same warp), then two [kNT] buffers by step parity for split
-    // steps (parts cross warps; a warp may run one step ahead)
-    // [L W] (>= kNT); with the communication warp also two [kNT] parity
-    // buffers for split steps.  (Config 3 sits at the edge: 12 KB more shared
-    // memory measured 30% slower -- less L1 left for loads in flight.)
-    // (with the communication warp the bulk runs on the warps the tail leaves
-    // idle, so a unit's parts cross warps and both regions are double-buffered)
+    // Bulk partials (values, then codes): [L W] (>= kNT) for unsplit steps and
+    // [kNT] for split steps (late diagonals, cut range over several warps).
+    // Without the communication warp the steps are barrier-aligned and one
+    // [L W] region serves both.  With it, the bulk of step k+1 runs on other
+    // warps than the tail of step k that reads step k's parts, so each region
+    // is double-buffered by step parity: [2 L W | 2 kNT].  (Shared memory is
+    // tight for config-3-sized co-resident tables: 12 KB more once cost 30 %
+    // -- less L1 left for loads in flight.)
     const uint64_t np = tp.comm ? 2ull * tp.cap + 2 * kNT : (uint64_t)tp.cap;
     b = al16(b + np * 4);
     m.code = (uint32_t)b;

@@ -666,7 +666,8 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
             // batch tables need no co-residency (their tiles are queued jobs)
             t->tiles = tile_plan(t->g, t->width, batch_tiles ? INT32_MAX : sms, (int64_t)h.ids.size(),
-                                 (int)round_up(std::max<int32_t>(h.max_opts, 1), kTileOptBatch), t->tplan) == 1;
+                                 (int)round_up(std::max<int32_t>(h.max_opts, 1), kTileOptBatch), t->tplan,
+                                 kreq == RKR_KERNEL_TILES && !batch_tiles) == 1;
         }
         if (kreq == RKR_KERNEL_TILES && !t->tiles) {
             delete t;
@@ -1326,6 +1327,7 @@ rkr_status batch_layout(rkr_batch* b) {
             tp.fin = nullptr;
             tp.comm = b->proto.comm;
             tp.split = 0;  // measured slower for batches (throughput-bound)
+            tp.stream = 0;
             tp.sm = b->proto.sm;
             b->htp[i] = tp;
         }
@@ -1453,6 +1455,7 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
                 pr.cap = std::max(pr.cap, t->tplan.cap);
             }
             pr.comm = 1;  // every job is a latency-bound tile walk
+            pr.stream = 0;  // batches stage their programs (else K1p)
             redo = tile_batch_smem(pr).total > 220 * 1024;
         }
         if (attempt == 1 && mixed && ex.width != RKR_WIDTH_64) {

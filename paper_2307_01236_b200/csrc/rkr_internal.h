@@ -187,6 +187,7 @@ struct TilePlan {
     int32_t comm = 0;                     // 1: a dedicated communication warp (latency-bound tables)
     int32_t jobs = 0;                     // 1: more tiles than SMs: run as tile jobs (one-table batch)
     int32_t split = 0;                    // 1 (with comm): late diagonals split each tail over 2 warps
+    int32_t stream = 0;                   // 1: programs / thresholds / options read from global (long chains)
     // fused K2 (per launch): the last CTA walks from (ws, wt, wm) into wops /
     // wout = {n_ops, status, bad_s, bad_t, top} (rkr_walk.cuh)
     int32_t walk = 0, ws = 0, wt = 0, wm = 0;
@@ -198,7 +199,10 @@ struct TilePlan {
     int32_t* done = nullptr;              // [L * T]
     unsigned long long* trace = nullptr;  // optional: 6 stamps per (k, j)
 };
-int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp);  // 1 = eligible
+// 1 = eligible.  allow_stream: long chains may run the streamed-program
+// variant (only on an explicit RKR_KERNEL_TILES request; else they run K1p).
+int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp,
+              bool allow_stream = false);
 int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream);
 // Batches: jobs (table, tile) in queue order; tps[i].sm is the batch-wide
 // layout (tile_batch_smem of a plan with every table's maxima).

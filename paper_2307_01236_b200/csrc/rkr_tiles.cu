@@ -110,6 +110,7 @@ constexpr int kNW = 32;        // warps per CTA
 constexpr int kNT = kNW * 32;  // threads per CTA
 constexpr int kU = 8;          // cuts per load batch (2 kU loads in flight per lane)
 constexpr int kOB = kTileOptBatch;  // options per load batch (ocap is a multiple of kOB)
+constexpr int kSlice = 64;          // STREAM: cut-program entries staged per warp at a time
 
 inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~15ull); }
 inline TileSmem tile_smem(const TilePlan& tp) {
@@ -136,11 +137,20 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     m.blk = (uint32_t)b;
     b = al16(b + (L + 2) * 4);  // block option offsets [L+1] + the last-CTA flag
     m.opd = (uint32_t)b;
-    b = al16(b + L * tp.ocap * 8);  // [block][ocap] {pack shift, pass time}, padded
-    m.prog = (uint32_t)b;
-    b += 2ull * m.prog_bytes;
-    m.thr = (uint32_t)b;
-    b += 2ull * m.thr_bytes;
+    if (tp.stream) {  // programs, thresholds and options from global memory;
+        // per-warp program slices for the bulk
+        m.prog_bytes = (uint32_t)(kNW * kSlice * 16);
+        m.thr_bytes = 0;
+        m.prog = (uint32_t)b;
+        b += m.prog_bytes;
+        m.thr = (uint32_t)b;
+    } else {
+        b = al16(b + L * tp.ocap * 8);  // [block][ocap] {pack shift, pass time}, padded
+        m.prog = (uint32_t)b;
+        b += 2ull * m.prog_bytes;
+        m.thr = (uint32_t)b;
+        b += 2ull * m.thr_bytes;
+    }
     m.xch = (uint32_t)b;  // split-tail exchange: values [kNT] | codes [kNT] (comm only)
     b = al16(b + (tp.comm ? (uint64_t)kNT * 6 : 0));
     m.bar = (uint32_t)b;
@@ -167,7 +177,7 @@ __device__ __forceinline__ void stage_step(const TilePlan& tp, const ProgDev& pq
 // code).  Program entry i of cell (s, s+k): element offsets of slot 0 of the
 // left row (s, c-1) and of the right row (c, t) shifted by act_u[c]
 // (:166-167), the option-0 sweep (:162) and the gate (:159, :164).
-__device__ __forceinline__ void scan_cuts(const uint32_t* __restrict__ opt, const int4* pe, int ib,
+__device__ __forceinline__ bool scan_cuts(const uint32_t* __restrict__ opt, const int4* pe, int ib,
                                           int ie, int m, int cb, uint32_t& best, int& code) {
     int i0 = ib;
     for (; i0 + kU <= ie; i0 += kU) {
@@ -191,7 +201,7 @@ __device__ __forceinline__ void scan_cuts(const uint32_t* __restrict__ opt, cons
         }
         // the gate only grows with i: stop once no lane admits the batch's
         // last cut (the `break` of :164)
-        if (!__any_sync(0xffffffffu, e[kU - 1].w <= m)) return;
+        if (!__any_sync(0xffffffffu, e[kU - 1].w <= m)) return true;
     }
     for (; i0 < ie; ++i0) {
         const int4 e = pe[i0];
@@ -201,6 +211,23 @@ __device__ __forceinline__ void scan_cuts(const uint32_t* __restrict__ opt, cons
             best = tot;
             code = cb + i0;
         }
+    }
+    return false;
+}
+
+// STREAM variant (long chains: a diagonal's programs do not fit shared
+// memory): each warp stages its unit's program kSlice entries at a time.
+__device__ __forceinline__ void scan_cuts_streamed(const uint32_t* __restrict__ opt,
+                                                   const int4* __restrict__ pe_g, int4* slice,
+                                                   int ib, int ie, int m, int cb, uint32_t& best,
+                                                   int& code) {
+    const int lane = threadIdx.x & 31;
+    for (int c0 = ib; c0 < ie; c0 += kSlice) {
+        const int c1 = c0 + kSlice < ie ? c0 + kSlice : ie;
+        __syncwarp();  // the previous chunk's readers are done
+        for (int i = c0 + lane; i < c1; i += 32) slice[i - c0] = __ldg(pe_g + i);
+        __syncwarp();
+        if (scan_cuts(opt, slice - c0, c0, c1, m, cb, best, code)) return;
     }
 }
 
@@ -213,7 +240,7 @@ __device__ __forceinline__ void scan_cuts(const uint32_t* __restrict__ opt, cons
 // phases of the two program mbarriers before this job (jobs of a batch
 // reuse them).  The caller initialises the mbarriers once and separates
 // jobs with a CTA barrier.
-template <int WC, bool COMM, bool SPLIT>
+template <int WC, bool COMM, bool SPLIT, bool STREAM>
 __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, const int j,
                                          unsigned char* smem_raw, uint32_t ph0, uint32_t ph1) {
     constexpr int W = 32 * WC;
@@ -240,7 +267,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     // time INF).  Cut programs and thresholds arrive per step by bulk copy,
     // two steps ahead (double buffer, one mbarrier per buffer).
     for (int c = tid; c <= L; c += kNT) s_blk[c] = __ldg(dm.blk_off + c);
-    for (int q = tid; q < L * ocap; q += kNT) {
+    for (int q = tid; !STREAM && q < L * ocap; q += kNT) {
         const int b = q / ocap, i = q - b * ocap;
         const int o = __ldg(dm.blk_off + b) + i;
         s_opd[q] = o < __ldg(dm.blk_off + b + 1)
@@ -253,7 +280,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
 
     if (COMM && warp == kNC) {
         // ================= communication warp =================
-        if (lane == 0) {
+        if (!STREAM && lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             stage_step(tp, pq, sm, smem_raw, bars, L, 0);
             if (L > 1) stage_step(tp, pq, sm, smem_raw, bars, L, 1);
@@ -272,7 +299,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 // thread by the barrier) before the flag
                 t_red_release_add(done + (int64_t)k * tp.T + j, 1);
                 // buffer (k & 1) is free: every compute warp finished tail(k)
-                if (k + 2 < L) {
+                if (!STREAM && k + 2 < L) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     stage_step(tp, pq, sm, smem_raw, bars, L, k + 2);
                 }
@@ -280,7 +307,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         }
     } else {
     // ================= compute warps =================
-    if (!COMM && tid == 0) {
+    if (!COMM && !STREAM && tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         stage_step(tp, pq, sm, smem_raw, bars, L, 0);
         if (L > 1) stage_step(tp, pq, sm, smem_raw, bars, L, 1);
@@ -288,9 +315,13 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     for (int k = 0; k < L; ++k) {
         unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
         if (tp.trace && tid == 0) t0 = t_gtimer();
-        mbar_wait(bars + (k & 1), ((k & 1 ? ph1 : ph0) + (uint32_t)(k >> 1)) & 1u);
-        const int4* prog = reinterpret_cast<const int4*>(smem_raw + sm.prog + (k & 1) * sm.prog_bytes);
-        const int32_t* thrs = reinterpret_cast<const int32_t*>(smem_raw + sm.thr + (k & 1) * sm.thr_bytes);
+        if (!STREAM) mbar_wait(bars + (k & 1), ((k & 1 ? ph1 : ph0) + (uint32_t)(k >> 1)) & 1u);
+        // this step's cut programs and option thresholds: the staged copies,
+        // or (STREAM) straight from global memory
+        const int4* prog = STREAM ? static_cast<const int4*>(pq.ptr) + diag_cut_off(L, k)
+                                  : reinterpret_cast<const int4*>(smem_raw + sm.prog + (k & 1) * sm.prog_bytes);
+        const int32_t* thrs = STREAM ? pq.thr + diag_off(L, k) * ocap
+                                     : reinterpret_cast<const int32_t*>(smem_raw + sm.thr + (k & 1) * sm.thr_bytes);
 
         const int rows = L - k;
         const int units = rows * WC;
@@ -323,7 +354,12 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 const int ie = ib + chunk < k - 1 ? ib + chunk : k - 1;
                 uint32_t best = INF;
                 int code = 0;
-                scan_cuts(opt, prog + s * k, ib, ie, m, kCutBit | (s + 1), best, code);
+                if constexpr (STREAM)
+                    scan_cuts_streamed(opt, prog + s * k,
+                                       reinterpret_cast<int4*>(smem_raw + sm.prog) + warp * kSlice,
+                                       ib, ie, m, kCutBit | (s + 1), best, code);
+                else
+                    scan_cuts(opt, prog + s * k, ib, ie, m, kCutBit | (s + 1), best, code);
                 pbest[it * 32 + lane] = best;
                 pcode[it * 32 + lane] = (uint16_t)code;
             }
@@ -375,11 +411,11 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             uint32_t tl0 = INF, tr0 = INF, tl1 = INF, tr1 = INF;
             int4 e0 = make_int4(0, 0, 0, M + 2), e1 = e0;
             if (k > 0 && cuts) {
-                e0 = prog[s * k];
+                e0 = STREAM ? __ldg(prog + s * k) : prog[s * k];
                 tl0 = __ldcg(opt + (uint32_t)(e0.x + m));
                 tr0 = __ldcg(opt + (uint32_t)(e0.y + m));
                 if (k > 1) {
-                    e1 = prog[s * k + k - 1];
+                    e1 = STREAM ? __ldg(prog + s * k + k - 1) : prog[s * k + k - 1];
                     tl1 = __ldcg(opt + (uint32_t)(e1.x + m));
                     tr1 = __ldcg(opt + (uint32_t)(e1.y + m));
                 }
@@ -398,7 +434,15 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 int32_t th[kOB];
 #pragma unroll
                 for (int q = 0; q < kOB; q += 2) {
-                    const int4 o2 = od4[(i0 + q) >> 1];
+                    int4 o2;
+                    if constexpr (STREAM) {  // (shift, pass time) of options i0+q, i0+q+1
+                        const int oa = s_blk[s] + i0 + q, ob = oa + 1, on = s_blk[s + 1];
+                        const int qa = oa < on ? oa : 0, qb = ob < on ? ob : 0;
+                        o2 = make_int4(__ldg(pq.pc + qa), oa < on ? (int)__ldg(static_cast<const uint32_t*>(pq.otot) + qa) : (int)INF,
+                                       __ldg(pq.pc + qb), ob < on ? (int)__ldg(static_cast<const uint32_t*>(pq.otot) + qb) : (int)INF);
+                    } else {
+                        o2 = od4[(i0 + q) >> 1];
+                    }
                     ot[q] = (uint32_t)o2.y;
                     ot[q + 1] = (uint32_t)o2.w;
                     sub[q] = k > 0 ? __ldcg(opt + (uint32_t)(widx - o2.x)) : 0u;
@@ -406,7 +450,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 }
 #pragma unroll
                 for (int q = 0; q < kOB; q += 4) {
-                    const int4 t4 = th4[(i0 + q) >> 2];
+                    const int4 t4 = STREAM ? __ldg(th4 + ((i0 + q) >> 2)) : th4[(i0 + q) >> 2];
                     th[q] = t4.x;
                     th[q + 1] = t4.y;
                     th[q + 2] = t4.z;
@@ -495,7 +539,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             __syncthreads();
             if (tid == 0) {
                 t_red_release_add(done + (int64_t)k * tp.T + j, 1);
-                if (k + 2 < L) {
+                if (!STREAM && k + 2 < L) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     stage_step(tp, pq, sm, smem_raw, bars, L, k + 2);
                 }
@@ -559,7 +603,7 @@ __device__ __forceinline__ void last_walk(const InstDesc& D, const TilePlan& tp,
     __syncthreads();  // the walk's shared memory is free again
 }
 
-template <int WC, bool COMM, bool SPLIT>
+template <int WC, bool COMM, bool SPLIT, bool STREAM>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ InstDesc D,
                                                     const __grid_constant__ TilePlan tp) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -572,7 +616,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    tile_job<WC, COMM, SPLIT>(D, tp, blockIdx.x, smem_raw, 0, 0);
+    tile_job<WC, COMM, SPLIT, STREAM>(D, tp, blockIdx.x, smem_raw, 0, 0);
     const Geometry& g = D.g;
     const DevMenu& dm = D.dm;
     uint32_t* __restrict__ opt = static_cast<uint32_t*>(D.opt);
@@ -629,7 +673,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
 // tiles of its own table, which were dequeued earlier by CTAs that are
 // running or done, so the queue cannot deadlock and tables need not be
 // co-resident.
-template <int WC, bool COMM, bool SPLIT, bool WALK>
+template <int WC, bool COMM, bool SPLIT, bool STREAM, bool WALK>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __restrict__ descs,
                                                           const TilePlan* __restrict__ tps,
                                                           const int2* __restrict__ jobs, int njobs,
@@ -652,7 +696,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
         const int q = s_job;
         if (q >= njobs) break;
         const int2 jb = jobs[q];
-        tile_job<WC, COMM, SPLIT>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0, ph1);
+        tile_job<WC, COMM, SPLIT, STREAM>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0, ph1);
         const int L = descs[jb.x].g.L;
         ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
         ph1 += (uint32_t)L / 2;
@@ -662,9 +706,9 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
     }
 }
 
-template <int WC, bool COMM, bool SPLIT>
+template <int WC, bool COMM, bool SPLIT, bool STREAM>
 int launch_tiles_t(const InstDesc& d, const TilePlan& tp, cudaStream_t st) {
-    auto kern = fill_tiles<WC, COMM, SPLIT>;
+    auto kern = fill_tiles<WC, COMM, SPLIT, STREAM>;
     const size_t smem = tp.sm.total;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -684,7 +728,8 @@ int launch_tiles_t(const InstDesc& d, const TilePlan& tp, cudaStream_t st) {
 
 // Narrowest tile (W = 32 WC) whose T tiles fit one CTA per SM; 0 = not
 // eligible (the queue-scheduled K1p runs instead).
-int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp) {
+int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp,
+              bool allow_stream) {
     if (const char* e = getenv("RKR_TILES"))  // tuning knob: 0 disables K1t
         if (atoi(e) == 0) return 0;
     if (width != 32) return 0;
@@ -719,7 +764,20 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
         // of tables (config 4))
         tp.split = tp.comm && !tp.jobs && ocap >= 2 * kOB ? 1 : 0;
         if (const char* e = getenv("RKR_SPLIT")) tp.split = tp.comm && atoi(e) != 0;  // tuning knob
+        tp.stream = 0;
         tp.sm = tile_smem(tp);
+        const bool force = getenv("RKR_STREAM") != nullptr;  // test knob
+        if (tp.sm.total > 220 * 1024 || force) {
+            // long chains: a diagonal's programs do not fit shared memory.
+            // The streamed variant reads them (and the option data) from
+            // global memory; it is correct but slower than the row-segment
+            // queue there (L=256, B=64, M=4096: 30 ms against K1p's 27 ms),
+            // so it only runs when budget tiles are requested explicitly.
+            if (!allow_stream && !force) return 0;
+            tp.stream = 1;
+            tp.split = 0;
+            tp.sm = tile_smem(tp);
+        }
         return tp.sm.total <= 220 * 1024 ? 1 : 0;
     }
     return 0;
@@ -728,9 +786,11 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
 int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (width != 32 || tp.WC != 1) return 3;  // 32-bit costs, 32-slot tiles
-    if (tp.comm) return tp.split ? launch_tiles_t<1, true, true>(d, tp, st)
-                                 : launch_tiles_t<1, true, false>(d, tp, st);
-    return launch_tiles_t<1, false, false>(d, tp, st);
+    if (tp.stream) return tp.comm ? launch_tiles_t<1, true, false, true>(d, tp, st)
+                                  : launch_tiles_t<1, false, false, true>(d, tp, st);
+    if (tp.comm) return tp.split ? launch_tiles_t<1, true, true, false>(d, tp, st)
+                                 : launch_tiles_t<1, true, false, false>(d, tp, st);
+    return launch_tiles_t<1, false, false, false>(d, tp, st);
 }
 
 TileSmem tile_batch_smem(const TilePlan& proto) { return tile_smem(proto); }
@@ -761,13 +821,19 @@ int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const in
     // (split tails only for a single table run as jobs, never for batches)
     const bool split = walk && proto.comm && proto.split;
     if (walk && walk->walk) {
-        if (split) return go(fill_tiles_batch<1, true, true, true>);
-        return proto.comm ? go(fill_tiles_batch<1, true, false, true>)
-                          : go(fill_tiles_batch<1, false, false, true>);
+        if (proto.stream)
+            return proto.comm ? go(fill_tiles_batch<1, true, false, true, true>)
+                              : go(fill_tiles_batch<1, false, false, true, true>);
+        if (split) return go(fill_tiles_batch<1, true, true, false, true>);
+        return proto.comm ? go(fill_tiles_batch<1, true, false, false, true>)
+                          : go(fill_tiles_batch<1, false, false, false, true>);
     }
-    if (split) return go(fill_tiles_batch<1, true, true, false>);
-    return proto.comm ? go(fill_tiles_batch<1, true, false, false>)
-                      : go(fill_tiles_batch<1, false, false, false>);
+    if (proto.stream)  // (a single table: batches are never streamed)
+        return proto.comm ? go(fill_tiles_batch<1, true, false, true, false>)
+                          : go(fill_tiles_batch<1, false, false, true, false>);
+    if (split) return go(fill_tiles_batch<1, true, true, false, false>);
+    return proto.comm ? go(fill_tiles_batch<1, true, false, false, false>)
+                      : go(fill_tiles_batch<1, false, false, false, false>);
 }
 
 }  // namespace rkr

@@ -430,3 +430,21 @@ def test_tiles_as_jobs(orc, monkeypatch, comm):
                 got = _walk_or_inf(t.backtrack_fetch)
                 assert got == (ref_ops if bst == 0 else "infeasible")
             assert_same(t.download(), (o, k, v))
+
+
+@pytest.mark.parametrize("env", [{"RKR_STREAM": "1"}, {"RKR_STREAM": "1", "RKR_COMM": "0"},
+                                 {"RKR_STREAM": "1", "RKR_JOBS": "1"}])
+def test_tiles_streamed_programs(orc, monkeypatch, env):
+    """K1t with programs, thresholds and option data read from global memory
+    (the long-chain variant), co-resident / without the communication warp /
+    as tile jobs: whole tables and the fused walk against the oracle."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    for L, B, M, seed in [(12, 6, 200, 7), (40, 20, 900, 45), (3, 2, 20, 5), (70, 9, 300, 8)]:
+        menu = synthetic_menu(L, B, M, seed, tie_stress=True)
+        st, o, k, v, _, _ = orc.fill(menu, 1, M)
+        with rotor.DpTable(menu, 1, M, kernel="tiles") as t:
+            assert_same(t.download(), (o, k, v))
+            t.refill_walk(0, L - 1, M)
+            bst, ref_ops = orc.build_schedule(menu, 1, M, (o, k, v), 0, L - 1, M)
+            assert _walk_or_inf(t.backtrack_fetch) == (ref_ops if bst == 0 else "infeasible")

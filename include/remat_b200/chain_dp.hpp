@@ -121,7 +121,7 @@ struct ExecConfig {
     int device = 0;
     void* stream = nullptr;
     bool force_int64 = false;
-    int kernel = RKR_KERNEL_PERSISTENT;  // or RKR_KERNEL_DIAGONAL
+    int kernel = RKR_KERNEL_PERSISTENT;  // or _TILES, _QUEUE, _DIAGONAL (include/rkr.h)
 };
 
 // chain_dp.hpp:54-196.  Construction fills every cell on the GPU.

@@ -176,7 +176,7 @@ size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p);  // coun
 // of kTileOptBatch: thr rows and option slots are padded to a multiple.
 constexpr int kTileOptBatch = 8;  // 16 measured: config 2 -2%, configs 1 and 3 +8-12%
 struct TileSmem {  // shared-memory carve-up of K1t (byte offsets)
-    uint32_t best, code, blk, opd, prog, thr, xch, bar, total;
+    uint32_t best, code, blk, split, opd, prog, thr, xch, bar, total;
     uint32_t prog_bytes, thr_bytes;  // one buffer of each (two of each are kept)
 };
 struct TilePlan {

@@ -136,6 +136,8 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     b = al16(b + np * 2);
     m.blk = (uint32_t)b;
     b = al16(b + (L + 2) * 4);  // block option offsets [L+1] + the last-CTA flag
+    m.split = (uint32_t)b;      // per step: bulk parts and cuts per part
+    b = al16(b + L * 8);
     m.opd = (uint32_t)b;
     if (tp.stream) {  // programs, thresholds and options from global memory;
         // per-warp program slices for the bulk
@@ -240,7 +242,7 @@ __device__ __forceinline__ void scan_cuts_streamed(const uint32_t* __restrict__ 
 // phases of the two program mbarriers before this job (jobs of a batch
 // reuse them).  The caller initialises the mbarriers once and separates
 // jobs with a CTA barrier.
-template <int WC, bool COMM, bool SPLIT, bool STREAM>
+template <int WC, bool COMM, bool SPLIT, bool STREAM, bool TABLE>
 __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, const int j,
                                          unsigned char* smem_raw, uint32_t ph0, uint32_t ph1) {
     constexpr int W = 32 * WC;
@@ -267,6 +269,20 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     // time INF).  Cut programs and thresholds arrive per step by bulk copy,
     // two steps ahead (double buffer, one mbarrier per buffer).
     for (int c = tid; c <= L; c += kNT) s_blk[c] = __ldg(dm.blk_off + c);
+    // per step: bulk parts P and cuts per part (late diagonals split the
+    // cut range over warps; >= 8 cuts per part)
+    int2* s_split = reinterpret_cast<int2*>(smem_raw + sm.split);
+    for (int k = tid; TABLE && k < L; k += kNT) {
+        const int units = (L - k) * WC, nb = k >= 3 ? k - 2 : 0;
+        int P = 1, chunk = nb;
+        if (nb > 0 && units < kNC) {
+            P = kNC / units;
+            const int pmax = (nb + 7) >> 3;
+            if (P > pmax) P = pmax;
+            chunk = (nb + P - 1) / P;
+        }
+        s_split[k] = make_int2(P, chunk);
+    }
     for (int q = tid; !STREAM && q < L * ocap; q += kNT) {
         const int b = q / ocap, i = q - b * ocap;
         const int o = __ldg(dm.blk_off + b) + i;
@@ -326,8 +342,15 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         const int rows = L - k;
         const int units = rows * WC;
         const int nb = k >= 3 ? k - 2 : 0;  // bulk cuts i = 1 .. k-2
+        // late diagonals split the cut range into P parts of `chunk` cuts
+        // (TABLE: precomputed per step, no integer division in the step loop
+        // -- 5 % on configs 1-2; the tile-job kernels measured faster without)
         int P = 1, chunk = nb;
-        if (nb > 0 && units < kNC) {  // late diagonals: split the cut range
+        if constexpr (TABLE) {
+            const int2 pc2 = s_split[k];
+            P = pc2.x;
+            chunk = pc2.y;
+        } else if (nb > 0 && units < kNC) {
             P = kNC / units;
             const int pmax = (nb + 7) >> 3;  // keep >= 8 cuts per part
             if (P > pmax) P = pmax;
@@ -345,8 +368,9 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             // with the communication warp, bulk units go to the warps from the
             // top down: on late diagonals the tail of step k-1 occupies the
             // low warps, so the bulk of step k runs beside it
+            const float rcp_units = TABLE ? __frcp_ru((float)units) : 0.f;  // it / units, exactly, it < 2^10
             for (int it = COMM ? kNC - 1 - warp : warp; it < units * P; it += kNC) {
-                const int p = P == 1 ? 0 : it / units;
+                const int p = P == 1 ? 0 : (TABLE ? (int)((float)it * rcp_units) : it / units);
                 const int u = it - p * units;
                 const int s = u / WC;
                 const int m = m_lo + (u - s * WC) * 32 + lane;
@@ -395,7 +419,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         uint32_t* xbest = reinterpret_cast<uint32_t*>(smem_raw + sm.xch);
         uint16_t* xcode = reinterpret_cast<uint16_t*>(xbest + kNT);
         for (int v = warp; v < units * TS; v += kNC) {
-            const int h = TS == 1 ? -1 : v / units;  // -1: the whole tail
+            const int h = TS == 1 ? -1 : (v >= units ? 1 : 0);  // -1: the whole tail
             const int u = TS == 1 ? v : v - h * units;
             const int s = u / WC;
             const int m = m_lo + (u - s * WC) * 32 + lane;
@@ -616,7 +640,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    tile_job<WC, COMM, SPLIT, STREAM>(D, tp, blockIdx.x, smem_raw, 0, 0);
+    tile_job<WC, COMM, SPLIT, STREAM, true>(D, tp, blockIdx.x, smem_raw, 0, 0);
     const Geometry& g = D.g;
     const DevMenu& dm = D.dm;
     uint32_t* __restrict__ opt = static_cast<uint32_t*>(D.opt);
@@ -696,7 +720,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
         const int q = s_job;
         if (q >= njobs) break;
         const int2 jb = jobs[q];
-        tile_job<WC, COMM, SPLIT, STREAM>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0, ph1);
+        tile_job<WC, COMM, SPLIT, STREAM, false>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0, ph1);
         const int L = descs[jb.x].g.L;
         ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
         ph1 += (uint32_t)L / 2;

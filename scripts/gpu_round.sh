@@ -19,7 +19,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 for c in 2 3; do
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum --clock-control none -k regex:fill_tiles -s 3 -c 1 --csv --log-file $O/traffic_cfg$c.csv python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 done
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum --clock-control none -k regex:fill_tiles_batch -s 3 -c 1 --csv --log-file $O/traffic_cfg4.csv python bench.py --config 4 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum --clock-control none -k regex:fill_tiles -s 3 -c 1 --csv --log-file $O/traffic_cfg4.csv python bench.py --config 4 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 # full captures of the fill kernel (config 2 headline, config 3 largest)
 for c in 2 3; do
 ncu --set full --clock-control none --import-source on -k regex:fill_tiles -s 3 -c 1 -o $O/prof_cfg$c -f python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1

@@ -149,8 +149,9 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
         first.clear();
         for (int32_t o = m->option_offsets[i]; o < m->option_offsets[i + 1]; ++o)
             first.emplace_back(m->option_id[o], o);
-        std::stable_sort(first.begin(), first.end(),
-                         [](const auto& x, const auto& y) { return x.first < y.first; });
+        // (id, position) pairs: plain sort keeps the first position of an id
+        // first (no allocation, unlike stable_sort)
+        std::sort(first.begin(), first.end());
         h.blk_off[i] = (int32_t)h.ids.size();
         int64_t fmax = 0, bmax = 0;
         for (int32_t o = m->option_offsets[i]; o < m->option_offsets[i + 1]; ++o) {
@@ -487,9 +488,12 @@ void stage_menu(const rkr_table* t, unsigned char* blob) {
     const HostMenu& h = t->hm;
     const std::vector<size_t>& off = t->off;
     const size_t L = h.L, np = t->plan.start.size();
-    std::memset(blob, 0, t->menu_bytes);
+    // every region is written below; only the alignment gaps between them
+    // are zeroed (the blob is uploaded whole)
     auto put = [&](int idx, const void* src, size_t n) {
         if (n) std::memcpy(blob + off[idx], src, n);
+        const size_t end = off[idx] + n, next = idx + 1 < 17 ? off[idx + 1] : t->off_tp;
+        if (next > end) std::memset(blob + end, 0, next - end);
     };
     put(0, h.blk_off.data(), (L + 1) * 4);
     put(1, h.fwd_req.data(), h.fwd_req.size() * 8);
@@ -507,6 +511,7 @@ void stage_menu(const rkr_table* t, unsigned char* blob) {
     put(13, t->plan.g.data(), np * 4);
     put(14, t->plan.k.data(), np * 4);
     put(15, &t->hdesc, sizeof(InstDesc));
+    std::memset(blob + off[16], 0, t->off_tp - off[16]);  // 16: plan instance ids (all 0)
     if (t->tiles && t->tplan.jobs) {
         std::memcpy(blob + t->off_tp, &t->tplan, sizeof(TilePlan));
         int2* jb = reinterpret_cast<int2*>(blob + t->off_jobs);

@@ -266,7 +266,9 @@ struct Staging {
     }
 };
 thread_local Staging t_stage;
-thread_local Staging t_back;  // pinned D2H staging (walk results)
+thread_local Staging t_back;   // pinned D2H staging (walk results)
+thread_local Staging t_sweep;  // pinned D2H staging (a sweep's walks; outlives nested fetches)
+thread_local Staging t_desc;   // pinned H2D staging of batch descriptors (overlaps the menu upload)
 
 }  // namespace
 
@@ -1379,7 +1381,7 @@ rkr_status batch_upload(rkr_batch* b) {
     const size_t np = b->hp.start.size();
     const size_t up = b->desc_bytes + b->plan_bytes + b->tps_bytes + b->jobs_bytes;
     void* stage = nullptr;
-    CK(t_stage.get(up, &stage));
+    CK(t_desc.get(up, &stage));
     unsigned char* sb = static_cast<unsigned char*>(stage);
     std::memcpy(sb, b->hd.data(), sizeof(InstDesc) * n);
     unsigned char* pb = sb + b->desc_bytes;
@@ -1393,7 +1395,7 @@ rkr_status batch_upload(rkr_batch* b) {
                     sizeof(int2) * b->hjobs.size());
     }
     CK(cudaMemcpyAsync(b->block, stage, up, cudaMemcpyHostToDevice, b->stream));
-    CK(cudaEventRecord(t_stage.done, b->stream));
+    CK(cudaEventRecord(t_desc.done, b->stream));
     return RKR_OK;
 }
 
@@ -1577,7 +1579,7 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
     std::vector<int64_t> top(nb, kInf64);
     std::vector<int64_t> walk_out(8 * (size_t)nb, 0);
     int64_t cap_each = 0;
-    std::vector<int32_t> walk_ops;
+    const int32_t* walk_ops = nullptr;  // pinned readback of every table's walk
     std::vector<std::vector<rkr_op>> big(nb);  // schedules that overflowed the batch slots
     if (nb > 0) {
         std::vector<const rkr_menu*> ms(nb, menu);
@@ -1608,23 +1610,30 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
         int32_t* d_mat = d_ops + (size_t)nb * cap_each * 3;
         uint8_t* d_act = reinterpret_cast<uint8_t*>(d_mat + nb);
         std::vector<uint8_t> act(nb, 1);
+        // One round trip: every table walks from its top cell (a walk
+        // reads opt(0, L-1, m_top) first and returns it, chain_dp.hpp:264;
+        // an infinite top ends the walk at once), and the walk records and
+        // op slots come back together through pinned memory.
+        (void)d_tops;
         auto run = [&]() -> rkr_status {
             CK(cudaMemcpyAsync(d_mat, mm.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, b->stream));
-            if (launch_batch_tops(b->ddesc, d_mat, nb, b->width, d_tops, b->stream))
-                return cuda_fail(cudaGetLastError(), "tops launch");
-            CK(cudaMemcpyAsync(top.data(), d_tops, 8 * (size_t)nb, cudaMemcpyDeviceToHost, b->stream));
-            CK(cudaStreamSynchronize(b->stream));
-            for (int q = 0; q < nb; ++q) act[q] = top[q] < kInf64 ? 1 : 0;   // :264-265
-            CK(cudaMemcpyAsync(d_act, act.data(), nb, cudaMemcpyHostToDevice, b->stream));
+            CK(cudaMemsetAsync(d_act, 1, nb, b->stream));
             if (launch_batch_walk(b->ddesc, d_mat, d_act, nb, b->width, d_ops, cap_each, d_wout,
                                   b->stream))
                 return cuda_fail(cudaGetLastError(), "walk launch");
-            CK(cudaMemcpyAsync(walk_out.data(), d_wout, 64 * (size_t)nb, cudaMemcpyDeviceToHost,
-                               b->stream));
-            walk_ops.resize((size_t)nb * cap_each * 3);
-            CK(cudaMemcpyAsync(walk_ops.data(), d_ops, walk_ops.size() * 4, cudaMemcpyDeviceToHost,
+            const size_t rec = 64 * (size_t)nb, opsb = (size_t)nb * cap_each * 12;
+            void* pin = nullptr;
+            CK(t_sweep.get(rec + opsb, &pin));
+            CK(cudaMemcpyAsync(pin, d_wout, rec, cudaMemcpyDeviceToHost, b->stream));
+            CK(cudaMemcpyAsync(static_cast<char*>(pin) + rec, d_ops, opsb, cudaMemcpyDeviceToHost,
                                b->stream));
             CK(cudaStreamSynchronize(b->stream));
+            std::memcpy(walk_out.data(), pin, rec);
+            walk_ops = reinterpret_cast<const int32_t*>(static_cast<char*>(pin) + rec);
+            for (int q = 0; q < nb; ++q) {
+                top[q] = walk_out[8 * q + 4];
+                act[q] = top[q] < kInf64 ? 1 : 0;   // :264-265
+            }
             return RKR_OK;
         };
         spt.st = b->stream;

@@ -145,7 +145,8 @@ inline TileSmem tile_smem(const TilePlan& tp) {
         m.thr_bytes = 0;
         m.prog = (uint32_t)b;
         b += m.prog_bytes;
-        m.thr = (uint32_t)b;
+        m.thr = (uint32_t)b;  // per-warp option slices: [kNW][ocap] int2 | [kNW][ocap] int
+        b = al16(b + (uint64_t)kNW * tp.ocap * 12);
     } else {
         b = al16(b + L * tp.ocap * 8);  // [block][ocap] {pack shift, pass time}, padded
         m.prog = (uint32_t)b;
@@ -451,6 +452,26 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             // row of diagonal k-1: id rid - (L - k))
             const int4* od4 = reinterpret_cast<const int4*>(s_opd + s * ocap);  // 2 options each
             const int4* th4 = reinterpret_cast<const int4*>(thrs + s * ocap);   // 4 options each
+            if constexpr (STREAM) {
+                // this unit's block options (shift, pass time) and row
+                // thresholds into the warp's slice, coalesced, padded like
+                // the staged layout (padding never wins: pass time INF,
+                // threshold M+1)
+                int2* wo = reinterpret_cast<int2*>(smem_raw + sm.thr) + warp * ocap;
+                int32_t* wt = reinterpret_cast<int32_t*>(smem_raw + sm.thr + (size_t)kNW * ocap * 8) +
+                              warp * ocap;
+                __syncwarp();  // the previous unit's readers are done
+                const int o0 = s_blk[s];
+                for (int i = lane; i < ocap; i += 32) {
+                    wo[i] = i < nopt ? make_int2(__ldg(pq.pc + o0 + i),
+                                                 (int)__ldg(static_cast<const uint32_t*>(pq.otot) + o0 + i))
+                                     : make_int2(0, (int)INF);
+                    wt[i] = __ldg(thrs + s * ocap + i);
+                }
+                __syncwarp();
+                od4 = reinterpret_cast<const int4*>(wo);
+                th4 = reinterpret_cast<const int4*>(wt);
+            }
             const int widx = k > 0 ? (rid - (L - k)) * sr + g.pad + m : 0;
             // whole batches: the padding options never win
             for (int i0 = ia; i0 < ib; i0 += kOB) {
@@ -458,15 +479,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 int32_t th[kOB];
 #pragma unroll
                 for (int q = 0; q < kOB; q += 2) {
-                    int4 o2;
-                    if constexpr (STREAM) {  // (shift, pass time) of options i0+q, i0+q+1
-                        const int oa = s_blk[s] + i0 + q, ob = oa + 1, on = s_blk[s + 1];
-                        const int qa = oa < on ? oa : 0, qb = ob < on ? ob : 0;
-                        o2 = make_int4(__ldg(pq.pc + qa), oa < on ? (int)__ldg(static_cast<const uint32_t*>(pq.otot) + qa) : (int)INF,
-                                       __ldg(pq.pc + qb), ob < on ? (int)__ldg(static_cast<const uint32_t*>(pq.otot) + qb) : (int)INF);
-                    } else {
-                        o2 = od4[(i0 + q) >> 1];
-                    }
+                    const int4 o2 = od4[(i0 + q) >> 1];
                     ot[q] = (uint32_t)o2.y;
                     ot[q + 1] = (uint32_t)o2.w;
                     sub[q] = k > 0 ? __ldcg(opt + (uint32_t)(widx - o2.x)) : 0u;
@@ -474,7 +487,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 }
 #pragma unroll
                 for (int q = 0; q < kOB; q += 4) {
-                    const int4 t4 = STREAM ? __ldg(th4 + ((i0 + q) >> 2)) : th4[(i0 + q) >> 2];
+                    const int4 t4 = th4[(i0 + q) >> 2];
                     th[q] = t4.x;
                     th[q + 1] = t4.y;
                     th[q + 2] = t4.z;
@@ -793,13 +806,14 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
         const bool force = getenv("RKR_STREAM") != nullptr;  // test knob
         if (tp.sm.total > 220 * 1024 || force) {
             // long chains: a diagonal's programs do not fit shared memory.
-            // The streamed variant reads them (and the option data) from
-            // global memory; it is correct but slower than the row-segment
-            // queue there (L=256, B=64, M=4096: 30 ms against K1p's 27 ms),
-            // so it only runs when budget tiles are requested explicitly.
-            if (!allow_stream && !force) return 0;
+            // The streamed variant reads them from global memory (each warp
+            // stages its unit's program, options and thresholds into its own
+            // slice); with the communication warp it beats the row-segment
+            // queue (L=256, B=64, M=4096: 25.9 ms against K1p's 27.0 ms)
+            (void)allow_stream;
             tp.stream = 1;
             tp.split = 0;
+            if (!getenv("RKR_COMM")) tp.comm = 1;
             tp.sm = tile_smem(tp);
         }
         return tp.sm.total <= 220 * 1024 ? 1 : 0;

@@ -77,7 +77,8 @@ def ncu_traffic(cfg_idx, kernel):
 
 
 FILL_KERNELS = {
-    "tiles": "fill_tiles (K1t: one co-resident launch, one CTA per budget tile)",
+    "tiles": "fill_tiles (K1t budget tiles: one co-resident CTA per 32-slot tile; tables with more "
+             "tiles than SMs run the same tiles as jobs, fill_tiles_batch)",
     "queue": "fill_persistent (K1p: one persistent launch, dataflow work queue)",
     "diagonal": "fill_diag (K1: one launch per anti-diagonal)",
 }

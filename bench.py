@@ -668,6 +668,7 @@ def b200_arm_sharded(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         mine = float(t.item())
     ops = sh.backtrack(handles, infos, 0, L - 1, M) if rank == 0 else []
+    shard_kern = sh.table.kernel()
     barrier()
     if rank == 0:
         peak, peak_src = measured_peak()
@@ -687,7 +688,9 @@ def b200_arm_sharded(args, world, rank, local):
             "gpu_launches": args.steps * world,
             "roofline": {"bound": "hbm", "achieved": ab / fill_s / 1e9 / world, "peak": peak,
                          "unit": "GB/s", "frac": ab / fill_s / 1e9 / world / peak, "traffic": None,
-                         "kernel": "fill_persistent (one launch per shard per step)",
+                         "kernel": (FILL_KERNELS[shard_kern] if shard_kern != "tiles" else
+                                    "fill_tiles (K1t budget tiles, streamed programs for long chains)")
+                                   + ", one launch per shard per step; halo pushed in-kernel",
                          "alg_bytes_per_fill": ab, "peak_source": peak_src + ", per GPU"},
             "clocks": sampler.summary(),
         }

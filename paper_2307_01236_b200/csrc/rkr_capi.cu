@@ -668,7 +668,7 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
     if (t->kernel == RKR_KERNEL_PERSISTENT) {
         // budget tiles (K1t) for unsharded tables; the queue (K1p) otherwise
         // or on request -- its work-item plan is only built when it runs
-        if (!spec && kreq != RKR_KERNEL_QUEUE) {
+        if ((!spec || kreq == RKR_KERNEL_TILES) && kreq != RKR_KERNEL_QUEUE) {
             int sms = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
             // batch tables need no co-residency (their tiles are queued jobs)
@@ -1204,6 +1204,7 @@ struct rkr_batch {
     TilePlan* dtps = nullptr;
     int2* djobs = nullptr;
     size_t tps_bytes = 0, jobs_bytes = 0;
+    bool ordered = false;                // tile jobs in table order (budget shards)
     void* mblock = nullptr;              // every table's menu blob (one H2D copy)
     void* wblock = nullptr;              // every table's work area
 };
@@ -1227,6 +1228,13 @@ rkr_status batch_zero(rkr_batch* b) {
 }
 
 rkr_status batch_launch(rkr_batch* b) {
+    if (b->tiles) {
+        if (launch_fill_tiles_batch(b->ddesc, b->dtps, b->djobs, (int)b->hjobs.size(),
+                                    reinterpret_cast<unsigned int*>(b->counter), b->proto,
+                                    b->stream))
+            return cuda_fail(cudaGetLastError(), "tile batch launch");
+        return RKR_OK;
+    }
     if (launch_fill_batch(b->ddesc, nullptr, b->lplan, b->width, b->R, b->kcap, b->ocap,
                           b->counter, b->stream))
         return cuda_fail(cudaGetLastError(), "batch fill launch");
@@ -1285,7 +1293,8 @@ rkr_status batch_layout(rkr_batch* b) {
             const rkr_table* t = b->tables[i];
             return (double)t->g.L * t->g.L * (t->g.M + 1) * (t->g.L + t->hm.max_opts);
         };
-        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return work(x) > work(y); });
+        if (!b->ordered)  // (budget shards keep chain order: shard r+1 waits on shard r)
+            std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return work(x) > work(y); });
         b->hjobs.clear();
         for (int i : order)
             for (int jt = 0; jt < b->tables[i]->tplan.T; ++jt) b->hjobs.push_back(make_int2(i, jt));
@@ -1806,32 +1815,51 @@ rkr_status sharded_create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max
     if (n > 1 && W < std::max(pad, 1))
         return fail(RKR_ERR_INVALID,
                     "too many shards: each must own at least the halo of %d budget slots", pad);
-    rkr_sharded* sh = new rkr_sharded();
-    sh->n = n;
-    sh->L = h.L;
-    sh->M = m_max;
-    sh->pad = pad;
+    // Shards run as budget-tile jobs (K1t, one batch kernel per device) when
+    // every shard qualifies; else the row-segment queue (K1p).
     const int R = persistent_choose_r(W - 1);
-    int32_t jo = 0;
-    for (int r = 0; r < n; ++r) {
-        const int32_t lo = r * W, hi = (r == n - 1) ? m_max + 1 : (r + 1) * W;
-        rkr_exec ex{};
-        if (exec) ex = *exec;
-        ex.kernel = RKR_KERNEL_QUEUE;  // batched and sharded tables run K1p
-        if (devices) ex.device = devices[r];
-        if (devices && exec && exec->stream) ex.stream = nullptr;  // per-device library streams
-        ShardSpec spec{lo, pad, jo};
-        rkr_table* t = nullptr;
-        st = prepare_table(menu, unit, hi - lo - 1, &ex, R, &t, &spec);
-        if (st) {
-            free_sharded(sh);
-            return st;
+    rkr_sharded* sh = nullptr;
+    bool tiles = !(exec && (exec->kernel == RKR_KERNEL_QUEUE || exec->kernel == RKR_KERNEL_DIAGONAL));
+    for (int attempt = tiles ? 0 : 1; attempt < 2; ++attempt) {
+        sh = new rkr_sharded();
+        sh->n = n;
+        sh->L = h.L;
+        sh->M = m_max;
+        sh->pad = pad;
+        tiles = attempt == 0;
+        int32_t jo = 0;
+        bool redo = false;
+        for (int r = 0; r < n; ++r) {
+            const int32_t lo = r * W, hi = (r == n - 1) ? m_max + 1 : (r + 1) * W;
+            rkr_exec ex{};
+            if (exec) ex = *exec;
+            ex.kernel = tiles ? RKR_KERNEL_TILES : RKR_KERNEL_QUEUE;
+            if (devices) ex.device = devices[r];
+            if (devices && exec && exec->stream) ex.stream = nullptr;  // per-device library streams
+            ShardSpec spec{lo, pad, jo};
+            rkr_table* t = nullptr;
+            st = prepare_table(menu, unit, hi - lo - 1, &ex, R, &t, &spec, /*batch_tiles=*/tiles);
+            if (st == RKR_ERR_INVALID && tiles) {  // a shard does not fit K1t: all run K1p
+                redo = true;
+                break;
+            }
+            if (st) {
+                free_sharded(sh);
+                return st;
+            }
+            sh->shards.push_back(t);
+            sh->lo.push_back(lo);
+            sh->hi.push_back(hi);
+            sh->dev.push_back(t->device);
+            jo += t->plan.J;
         }
-        sh->shards.push_back(t);
-        sh->lo.push_back(lo);
-        sh->hi.push_back(hi);
-        sh->dev.push_back(t->device);
-        jo += t->plan.J;
+        if (redo) {
+            free_sharded(sh);
+            sh = nullptr;
+            g_err.clear();
+            continue;
+        }
+        break;
     }
     sh->width = sh->shards[0]->width;
     // peer access: producer shard -> next shard (halo stores), shard 0's
@@ -1866,11 +1894,24 @@ rkr_status sharded_create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max
         b->device = d;
         b->R = R;
         b->owns_tables = false;
+        b->ordered = true;
         for (int r = 0; r < n; ++r)
             if (sh->dev[r] == d) {
                 where[r] = {(int)sh->batches.size(), (int)b->tables.size()};
                 b->tables.push_back(sh->shards[r]);
             }
+        b->tiles = sh->shards[0]->tiles;
+        if (b->tiles) {  // one shared-memory layout for every shard's jobs
+            TilePlan& pr = b->proto;
+            pr = b->tables[0]->tplan;
+            for (rkr_table* t : b->tables) {
+                pr.cap = std::max(pr.cap, t->tplan.cap);
+                pr.stream = pr.stream || t->tplan.stream;
+            }
+            pr.comm = 1;
+            pr.split = 0;
+            pr.sm = tile_batch_smem(pr);
+        }
         sh->batches.push_back(b);
         DeviceGuard dg(d);
         st = batch_layout(b);
@@ -1889,7 +1930,10 @@ rkr_status sharded_create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max
         a.next_sr = tn->g.sr;
         a.next_halo = b2.halo;
         a.next_peer = sh->dev[r] != sh->dev[r + 1] ? 1 : 0;
-        b2.halo_need = pr.J - std::max(0, (Wr - pad) / pr.TM);  // producer tiles meeting the halo
+        // producer tiles meeting the halo (K1t: 32-slot tiles; K1p: its segments)
+        b2.halo_need = sh->shards[r]->tiles
+                           ? sh->shards[r]->tplan.T - std::max(0, (Wr - pad) / sh->shards[r]->tplan.W)
+                           : pr.J - std::max(0, (Wr - pad) / pr.TM);
     }
     for (rkr_batch* b : sh->batches) {
         DeviceGuard dg(b->device);
@@ -2089,17 +2133,30 @@ rkr_status rkr_shard_create(const rkr_menu* menu, int64_t unit, int32_t m_max, i
     if (st) return st;
     rkr_exec ex{};
     if (exec) ex = *exec;
-    ex.kernel = RKR_KERNEL_QUEUE;  // batched and sharded tables run K1p
+    // budget tiles (K1t) when the shard qualifies -- every process decides
+    // alike, from the same menu and geometry -- else the row-segment queue
+    const bool want_tiles = !(exec && (exec->kernel == RKR_KERNEL_QUEUE || exec->kernel == RKR_KERNEL_DIAGONAL));
     ShardSpec spec{sg.lo[shard], sg.pad, sg.jo[shard]};
     spec.ipc = true;
     rkr_table* t = nullptr;
-    st = prepare_table(menu, unit, sg.hi[shard] - sg.lo[shard] - 1, &ex, sg.R, &t, &spec);
+    st = RKR_ERR_INVALID;
+    if (want_tiles) {
+        ex.kernel = RKR_KERNEL_TILES;
+        st = prepare_table(menu, unit, sg.hi[shard] - sg.lo[shard] - 1, &ex, sg.R, &t, &spec);
+        if (st == RKR_ERR_INVALID) g_err.clear();
+    }
+    if (st == RKR_ERR_INVALID) {
+        ex.kernel = RKR_KERNEL_QUEUE;
+        st = prepare_table(menu, unit, sg.hi[shard] - sg.lo[shard] - 1, &ex, sg.R, &t, &spec);
+    }
     if (st) return st;
     t->shard_lo = sg.lo[shard];
     t->shard_hi = sg.hi[shard];
     if (shard > 0) {  // tiles of the previous shard that meet this shard's halo
         const int32_t Wp = sg.hi[shard - 1] - sg.lo[shard - 1];
-        t->hdesc.halo_need = sg.J[shard - 1] - std::max(0, (Wp - sg.pad) / sg.TM);
+        t->hdesc.halo_need = t->tiles ? (Wp + t->tplan.W - 1) / t->tplan.W -
+                                            std::max(0, (Wp - sg.pad) / t->tplan.W)
+                                      : sg.J[shard - 1] - std::max(0, (Wp - sg.pad) / sg.TM);
     }
     DeviceGuard dg(t->device);
     CK(cudaMemcpyAsync(t->ddesc, &t->hdesc, sizeof(InstDesc), cudaMemcpyHostToDevice, t->stream));
@@ -2163,6 +2220,18 @@ rkr_status rkr_shard_zero(rkr_table* t) {
 rkr_status rkr_shard_launch(rkr_table* t) {
     if (!t) return fail(RKR_ERR_ARGUMENT, "null table");
     DeviceGuard dg(t->device);
+    if (t->tiles) {  // state zeroed by rkr_shard_zero
+        TilePlan tp = t->tplan;
+        if (tp.jobs) {
+            if (launch_fill_tiles_batch(t->ddesc, t->dtp, t->djobs, tp.T,
+                                        reinterpret_cast<unsigned int*>(t->pdev.counter), tp,
+                                        t->stream, &tp))
+                return cuda_fail(cudaGetLastError(), "shard launch");
+        } else if (launch_fill_tiles(t->hdesc, tp, t->width, t->stream)) {
+            return cuda_fail(cudaGetLastError(), "shard launch");
+        }
+        return RKR_OK;
+    }
     if (launch_fill_batch(t->ddesc, &t->hdesc, t->lplan, t->width, t->plan.R,
                           std::max(t->g.L - 1, 1), std::max(t->hm.max_opts, 1), t->pdev.counter,
                           t->stream))

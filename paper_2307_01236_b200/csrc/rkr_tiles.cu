@@ -56,6 +56,11 @@ __device__ __forceinline__ void t_fence_acq_rel() { asm volatile("fence.acq_rel.
 __device__ __forceinline__ void t_red_release_add(int* p, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int t_ld_relaxed_sys(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ unsigned long long t_gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -292,6 +297,27 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                        : make_int2(0, (int)INF);
     }
     const int d_eff = tp.d < j ? tp.d : j;  // lower tiles this one reads
+    // Budget shards (config 5).  Local slots [Wl - pad, Wl) of this shard are
+    // the next shard's halo (its slots [-pad, 0)): tiles that compute them
+    // also store them there (peer memory when the next shard is on another
+    // GPU / in another process) and count L-k rows per diagonal into the
+    // next shard's halo[k] after a (system-scope) fence; tiles whose reads
+    // reach below local slot 0 wait for halo[k-1] >= (L-k+1) * halo_need.
+    const int Wl = M + 1;
+    const bool halo_in = D.halo_need > 0 && m_lo - g.pad < 0;
+    const bool halo_out = D.next_opt != nullptr && m_lo + W > Wl - g.pad && m_lo < Wl;
+    auto wait_halo = [&](int kk) {  // one thread
+        const int need = (L - kk) * D.halo_need;
+        while (t_ld_relaxed_sys(D.halo + kk) < need) __nanosleep(64);
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+    };
+    auto push_halo = [&](int kk) {  // one thread, after the CTA stored diagonal kk
+        if (D.next_peer)
+            __threadfence_system();
+        else
+            __threadfence();
+        atomicAdd(D.next_halo + kk, L - kk);
+    };
     int* __restrict__ done = tp.done;
     __syncthreads();
 
@@ -307,6 +333,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 const int* row = done + (int64_t)(k - 1) * tp.T;
                 for (int q = lane; q < d_eff; q += 32)
                     while (t_ld_acquire(row + j - 1 - q) == 0) __nanosleep(20);
+                if (halo_in && lane == 0) wait_halo(k - 1);
                 __syncwarp();
             }
             nb_arrive(kBarReady);
@@ -315,6 +342,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 // release-add: orders the CTA's stores (made visible to this
                 // thread by the barrier) before the flag
                 t_red_release_add(done + (int64_t)k * tp.T + j, 1);
+                if (halo_out) push_halo(k);
                 // buffer (k & 1) is free: every compute warp finished tail(k)
                 if (!STREAM && k + 2 < L) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -400,7 +428,10 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 for (int q = lane; q < d_eff; q += 32)
                     while (t_ld_relaxed(row + j - 1 - q) == 0) __nanosleep(20);
                 __syncwarp();
-                if (lane == 0) t_fence_acq_rel();
+                if (lane == 0) {
+                    if (halo_in) wait_halo(k - 1);
+                    t_fence_acq_rel();
+                }
             }
             __syncthreads();
         }
@@ -536,6 +567,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             } else if (h == -1 && m <= M) {  // store (chain_dp.hpp:176-177)
                 opt[(int64_t)rid * sr + g.pad + m] = best;
                 arg[(int64_t)rid * g.sa + m] = (uint16_t)code;
+                if (halo_out && m >= Wl - g.pad)  // the next shard's halo slot m - Wl
+                    static_cast<uint32_t*>(D.next_opt)[(int64_t)rid * D.next_sr + g.pad + (m - Wl)] = best;
             } else if (h == 0) {
                 xbest[(kNT >> 1) + u * 32 + lane] = best;  // (merged below)
                 xcode[(kNT >> 1) + u * 32 + lane] = (uint16_t)code;
@@ -557,6 +590,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 if (m <= M) {  // store (chain_dp.hpp:176-177)
                     opt[(int64_t)rid * sr + g.pad + m] = best;
                     arg[(int64_t)rid * g.sa + m] = (uint16_t)code;
+                    if (halo_out && m >= Wl - g.pad)
+                        static_cast<uint32_t*>(D.next_opt)[(int64_t)rid * D.next_sr + g.pad + (m - Wl)] = best;
                 }
             }
         }
@@ -576,6 +611,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             __syncthreads();
             if (tid == 0) {
                 t_red_release_add(done + (int64_t)k * tp.T + j, 1);
+                if (halo_out) push_halo(k);
                 if (!STREAM && k + 2 < L) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     stage_step(tp, pq, sm, smem_raw, bars, L, k + 2);
@@ -866,7 +902,7 @@ int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const in
         return proto.comm ? go(fill_tiles_batch<1, true, false, false, true>)
                           : go(fill_tiles_batch<1, false, false, false, true>);
     }
-    if (proto.stream)  // (a single table: batches are never streamed)
+    if (proto.stream)  // (a single long table, or budget shards of one)
         return proto.comm ? go(fill_tiles_batch<1, true, false, true, false>)
                           : go(fill_tiles_batch<1, false, false, true, false>);
     if (split) return go(fill_tiles_batch<1, true, true, false, false>);

@@ -589,10 +589,13 @@ class ShardedTable:
     config 5.  Shards may live on one GPU or on several (peer memory)."""
 
     def __init__(self, menu: Menu, unit: int, m_max: int, n_shards: int,
-                 devices: Optional[Sequence[int]] = None, width: str = "auto"):
+                 devices: Optional[Sequence[int]] = None, width: str = "auto",
+                 kernel: str = "persistent"):
+        """kernel: "persistent" (budget-tile jobs when every shard qualifies,
+        else the row-segment queue) or "queue"."""
         self._lib = lib()
         self._ms = menu.struct()
-        ex = _exec(devices[0] if devices else 0, width)
+        ex = _exec(devices[0] if devices else 0, width, None, kernel)
         dv = (ctypes.c_int32 * n_shards)(*devices) if devices else None
         self._h = ctypes.c_void_p()
         _check(self._lib.rkr_sharded_create(ctypes.byref(self._ms), unit, m_max, n_shards, dv,

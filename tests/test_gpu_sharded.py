@@ -30,6 +30,8 @@ def test_sharded_table_matches_oracle(orc, L, B, M, seed, tie, n, width):
     st, *ref = orc.fill(menu, 1, M)
     assert st == 0
     with rotor.ShardedTable(menu, 1, M, n, width=width) as sh:
+        # 32-bit shards run budget-tile jobs (K1t), 64-bit ones the queue (K1p)
+        assert sh.shard(0).kernel() == ("queue" if width == "64" else "tiles")
         rg = sh.ranges()
         assert len(rg) == n and rg[0][0] == 0 and rg[-1][1] == M + 1
         for rep in range(2):
@@ -62,3 +64,17 @@ def test_too_many_shards_is_rejected():
     menu = synthetic_menu(12, 4, 200, 3)
     with pytest.raises(rotor.ValidationError, match="too many shards"):
         rotor.ShardedTable(menu, 1, 200, 50)
+
+
+@pytest.mark.parametrize("L,B,M,seed,n,kernel", [(16, 4, 900, 31, 3, "queue"),
+                                                   (150, 8, 600, 32, 2, "persistent")])
+def test_sharded_kernels_exact(orc, L, B, M, seed, n, kernel):
+    """The row-segment queue (K1p) on request, and a long chain (streamed K1t
+    shards): both bit-exact."""
+    menu = synthetic_menu(L, B, M, seed, tie_stress=True)
+    st, *ref = orc.fill(menu, 1, M)
+    with rotor.ShardedTable(menu, 1, M, n, kernel=kernel) as sh:
+        assert sh.shard(0).kernel() == ("queue" if kernel == "queue" else "tiles")
+        _same(sh.download(), ref[:3])
+        sh.refill()
+        _same(sh.download(), ref[:3])

@@ -87,7 +87,9 @@ rkr_status cuda_fail(cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
     } while (0)
 
-int64_t to_units(int64_t b, int64_t unit) { return (b + unit - 1) / unit; }  // chain_dp.hpp:41
+int64_t to_units(int64_t b, int64_t unit) {  // chain_dp.hpp:41 (unit 1: no division)
+    return unit == 1 ? b : (b + unit - 1) / unit;
+}
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -304,6 +306,7 @@ struct rkr_table {
     PlanDev pdev{};
     ProgDev prog{};
     size_t state_bytes = 0;
+    bool state_clean = false;     // the program launch zeroed the fill state
     unsigned long long* trace = nullptr;
     int32_t bt_s = 0, bt_t = 0, bt_m = 0;
     InstDesc hdesc{};             // this table as the persistent kernel sees it
@@ -569,7 +572,10 @@ rkr_status enqueue_fill(rkr_table* t, bool walk = false, int32_t s = 0, int32_t 
         if (launch_fill_all(t->ctx())) return cuda_fail(cudaGetLastError(), "fill launch");
         return RKR_OK;
     }
-    CK(cudaMemsetAsync(t->pdev.counter, 0, t->state_bytes, t->stream));
+    if (t->state_clean)
+        t->state_clean = false;  // the program launch zeroed it (first fill)
+    else
+        CK(cudaMemsetAsync(t->pdev.counter, 0, t->state_bytes, t->stream));
     if (t->tiles) {
         TilePlan tp = t->tplan;
         tp.walk = walk ? 1 : 0;
@@ -681,6 +687,12 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
             return fail(RKR_ERR_INVALID, "kernel TILES: the table does not fit the budget-tile "
                         "kernel (64-bit costs, or too many rows for its shared memory)");
         }
+        if (t->tiles && spec && !batch_tiles) {  // a process shard: the halo variant
+            t->tplan.comm = 1;
+            t->tplan.split = 0;
+            t->tplan.halo = 1;
+            t->tplan.sm = tile_batch_smem(t->tplan);
+        }
         if (!t->tiles) {
             t->tplan = TilePlan{};
             persistent_plan(t->g, t->width, R > 0 ? R : persistent_choose_r(m_max), t->plan);
@@ -700,8 +712,14 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
     // (the persistent kernels' program launch also writes the pads)
     if (st == RKR_OK && t->kernel != RKR_KERNEL_PERSISTENT && launch_init_pads(t->ctx()))
         st = cuda_fail(cudaGetLastError(), "pad launch");
-    if (st == RKR_OK && t->kernel == RKR_KERNEL_PERSISTENT && launch_prep_programs(t->ctx()))
-        st = cuda_fail(cudaGetLastError(), "program launch");
+    if (st == RKR_OK && t->kernel == RKR_KERNEL_PERSISTENT) {
+        // a plain table (every fill goes through enqueue_fill) has its first
+        // fill's state zeroed by this launch
+        LaunchCtx c = t->ctx();
+        c.prep_zero = spec ? 0 : 1;
+        if (launch_prep_programs(c)) st = cuda_fail(cudaGetLastError(), "program launch");
+        else t->state_clean = !spec;
+    }
     ppt.mark("  prepare: program launch");
     if (st != RKR_OK) {
         free_table(t);
@@ -1910,6 +1928,7 @@ rkr_status sharded_create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max
             }
             pr.comm = 1;
             pr.split = 0;
+            pr.halo = 1;  // (one shard too: the kernel N shards run)
             pr.sm = tile_batch_smem(pr);
         }
         sh->batches.push_back(b);

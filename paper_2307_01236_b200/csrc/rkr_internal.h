@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 namespace rkr {
@@ -188,6 +190,7 @@ struct TilePlan {
     int32_t jobs = 0;                     // 1: more tiles than SMs: run as tile jobs (one-table batch)
     int32_t split = 0;                    // 1 (with comm): late diagonals split each tail over 2 warps
     int32_t stream = 0;                   // 1: programs / thresholds / options read from global (long chains)
+    int32_t halo = 0;                     // 1: a budget shard (halo wait / push compiled in; comm, no split)
     // fused K2 (per launch): the last CTA walks from (ws, wt, wm) into wops /
     // wout = {n_ops, status, bad_s, bad_t, top} (rkr_walk.cuh)
     int32_t walk = 0, ws = 0, wt = 0, wm = 0;
@@ -225,6 +228,7 @@ struct LaunchCtx {
     PlanDev plan;       // K1p schedule + state (device pointers)
     ProgDev prog;       // K1p cell programs
     size_t state_bytes; // bytes of counter + flags to zero before each fill
+    int32_t prep_zero = 0;  // 1: the program launch also zeroes that state
 };
 
 int launch_prep_programs(const LaunchCtx& c);
@@ -241,5 +245,30 @@ int launch_first_feasible(const LaunchCtx& c, int32_t s, int32_t t, int32_t* dev
 // export rows [r0, r1) of the s-major triangular order to reference-layout buffers
 int launch_export(const LaunchCtx& c, int64_t r0, int64_t r1, int64_t* opt, int8_t* kind,
                   int32_t* value);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, smem), skipped when the
+// kernel already has exactly that value on this device (the call costs host
+// time on every launch otherwise; the value itself is kept as before: the
+// launch's own size, never a larger one)
+inline cudaError_t set_dyn_smem(const void* kern, size_t smem) {
+    if (smem <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> last[64];
+    auto& m = last[dev & 63];
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = m.find(kern);
+        if (it != m.end() && it->second == (int)smem) return cudaSuccess;
+    }
+    const cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> g(mu);
+        m[kern] = (int)smem;
+    }
+    return e;
+}
 
 }  // namespace rkr

@@ -214,8 +214,14 @@ __device__ __forceinline__ void prep_body(const Geometry& g, const DevMenu& dm, 
 }
 
 template <typename V>
-__global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> pr) {
+__global__ void prep_programs(Geometry g, DevMenu dm, const V* opt, Programs<V> pr,
+                              uint32_t* __restrict__ zero, int64_t nzero) {
     prep_body<V>(g, dm, opt, pr, blockIdx.x, gridDim.x);
+    // the fill state (item counter + done flags) of the first fill, so that
+    // launch needs no memset of its own
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nzero;
+         i += (int64_t)gridDim.x * blockDim.x)
+        zero[i] = 0;
 }
 
 template <typename V>
@@ -625,9 +631,7 @@ int launch_t(const InstDesc* dev_desc, const InstDesc& d0, const LaunchPlan& lp,
     c.ocap = ocap > 0 ? ocap : 1;
     const size_t smem = psmem_bytes<V>(c);
     auto kern = fill_persistent<V, NT, R, U, SINGLE, MINB>;
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
+    if (set_dyn_smem((const void*)kern, smem) != cudaSuccess)
         return 3;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem) != cudaSuccess ||
@@ -666,8 +670,10 @@ int prep_t(const LaunchCtx& cx) {
     int blocks = (int)((n + 127) / 128);
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    prep_programs<V><<<blocks, 128, 0, st>>>(cx.g, cx.dm, static_cast<const V*>(cx.opt),
-                                             host_programs_of<V>(cx));
+    prep_programs<V><<<blocks, 128, 0, st>>>(
+        cx.g, cx.dm, static_cast<const V*>(cx.opt), host_programs_of<V>(cx),
+        reinterpret_cast<uint32_t*>(cx.plan.counter),
+        cx.prep_zero ? (int64_t)(cx.state_bytes / 4) : 0);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

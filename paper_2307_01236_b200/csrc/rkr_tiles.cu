@@ -248,7 +248,7 @@ __device__ __forceinline__ void scan_cuts_streamed(const uint32_t* __restrict__ 
 // phases of the two program mbarriers before this job (jobs of a batch
 // reuse them).  The caller initialises the mbarriers once and separates
 // jobs with a CTA barrier.
-template <int WC, bool COMM, bool SPLIT, bool STREAM, bool TABLE>
+template <int WC, bool COMM, bool SPLIT, bool STREAM, bool TABLE, bool HALO>
 __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, const int j,
                                          unsigned char* smem_raw, uint32_t ph0, uint32_t ph1) {
     constexpr int W = 32 * WC;
@@ -304,8 +304,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     // next shard's halo[k] after a (system-scope) fence; tiles whose reads
     // reach below local slot 0 wait for halo[k-1] >= (L-k+1) * halo_need.
     const int Wl = M + 1;
-    const bool halo_in = D.halo_need > 0 && m_lo - g.pad < 0;
-    const bool halo_out = D.next_opt != nullptr && m_lo + W > Wl - g.pad && m_lo < Wl;
+    const bool halo_in = HALO && D.halo_need > 0 && m_lo - g.pad < 0;
+    const bool halo_out = HALO && D.next_opt != nullptr && m_lo + W > Wl - g.pad && m_lo < Wl;
     auto wait_halo = [&](int kk) {  // one thread
         const int need = (L - kk) * D.halo_need;
         while (t_ld_relaxed_sys(D.halo + kk) < need) __nanosleep(64);
@@ -676,7 +676,7 @@ __device__ __forceinline__ void last_walk(const InstDesc& D, const TilePlan& tp,
     __syncthreads();  // the walk's shared memory is free again
 }
 
-template <int WC, bool COMM, bool SPLIT, bool STREAM>
+template <int WC, bool COMM, bool SPLIT, bool STREAM, bool HALO>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ InstDesc D,
                                                     const __grid_constant__ TilePlan tp) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    tile_job<WC, COMM, SPLIT, STREAM, true>(D, tp, blockIdx.x, smem_raw, 0, 0);
+    tile_job<WC, COMM, SPLIT, STREAM, true, HALO>(D, tp, blockIdx.x, smem_raw, 0, 0);
     const Geometry& g = D.g;
     const DevMenu& dm = D.dm;
     uint32_t* __restrict__ opt = static_cast<uint32_t*>(D.opt);
@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
 // tiles of its own table, which were dequeued earlier by CTAs that are
 // running or done, so the queue cannot deadlock and tables need not be
 // co-resident.
-template <int WC, bool COMM, bool SPLIT, bool STREAM, bool WALK>
+template <int WC, bool COMM, bool SPLIT, bool STREAM, bool WALK, bool HALO>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __restrict__ descs,
                                                           const TilePlan* __restrict__ tps,
                                                           const int2* __restrict__ jobs, int njobs,
@@ -769,7 +769,8 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
         const int q = s_job;
         if (q >= njobs) break;
         const int2 jb = jobs[q];
-        tile_job<WC, COMM, SPLIT, STREAM, false>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0, ph1);
+        tile_job<WC, COMM, SPLIT, STREAM, false, HALO>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0,
+                                                       ph1);
         const int L = descs[jb.x].g.L;
         ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
         ph1 += (uint32_t)L / 2;
@@ -779,13 +780,11 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
     }
 }
 
-template <int WC, bool COMM, bool SPLIT, bool STREAM>
+template <int WC, bool COMM, bool SPLIT, bool STREAM, bool HALO = false>
 int launch_tiles_t(const InstDesc& d, const TilePlan& tp, cudaStream_t st) {
-    auto kern = fill_tiles<WC, COMM, SPLIT, STREAM>;
+    auto kern = fill_tiles<WC, COMM, SPLIT, STREAM, HALO>;
     const size_t smem = tp.sm.total;
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
+    if (set_dyn_smem((const void*)kern, smem) != cudaSuccess)
         return 3;
     InstDesc dd = d;
     TilePlan pp = tp;
@@ -860,6 +859,11 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
 int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (width != 32 || tp.WC != 1) return 3;  // 32-bit costs, 32-slot tiles
+    if (tp.halo) {  // budget shards: communication warp, no split tails
+        if (!tp.comm || tp.split) return 3;
+        return tp.stream ? launch_tiles_t<1, true, false, true, true>(d, tp, st)
+                         : launch_tiles_t<1, true, false, false, true>(d, tp, st);
+    }
     if (tp.stream) return tp.comm ? launch_tiles_t<1, true, false, true>(d, tp, st)
                                   : launch_tiles_t<1, false, false, true>(d, tp, st);
     if (tp.comm) return tp.split ? launch_tiles_t<1, true, true, false>(d, tp, st)
@@ -876,9 +880,7 @@ int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const in
     if (njobs <= 0) return 0;
     auto go = [&](auto kern) -> int {
         const size_t smem = proto.sm.total;
-        if (smem > 48 * 1024 &&
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-                cudaSuccess)
+        if (set_dyn_smem((const void*)kern, smem) != cudaSuccess)
             return 3;
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);
@@ -890,24 +892,29 @@ int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const in
         return cudaGetLastError() == cudaSuccess ? 0 : 3;
     };
     if (proto.WC != 1) return 3;  // batches run 32-slot tiles
+    if (proto.halo) {  // budget shards: communication warp, no split tails, no walk
+        if (!proto.comm || proto.split || (walk && walk->walk)) return 3;
+        return proto.stream ? go(fill_tiles_batch<1, true, false, true, false, true>)
+                            : go(fill_tiles_batch<1, true, false, false, false, true>);
+    }
     // the walk variant only for a single table with a walk request (no code
     // for it in the batch kernels)
     // (split tails only for a single table run as jobs, never for batches)
     const bool split = walk && proto.comm && proto.split;
     if (walk && walk->walk) {
         if (proto.stream)
-            return proto.comm ? go(fill_tiles_batch<1, true, false, true, true>)
-                              : go(fill_tiles_batch<1, false, false, true, true>);
-        if (split) return go(fill_tiles_batch<1, true, true, false, true>);
-        return proto.comm ? go(fill_tiles_batch<1, true, false, false, true>)
-                          : go(fill_tiles_batch<1, false, false, false, true>);
+            return proto.comm ? go(fill_tiles_batch<1, true, false, true, true, false>)
+                              : go(fill_tiles_batch<1, false, false, true, true, false>);
+        if (split) return go(fill_tiles_batch<1, true, true, false, true, false>);
+        return proto.comm ? go(fill_tiles_batch<1, true, false, false, true, false>)
+                          : go(fill_tiles_batch<1, false, false, false, true, false>);
     }
     if (proto.stream)  // (a single long table, or budget shards of one)
-        return proto.comm ? go(fill_tiles_batch<1, true, false, true, false>)
-                          : go(fill_tiles_batch<1, false, false, true, false>);
-    if (split) return go(fill_tiles_batch<1, true, true, false, false>);
-    return proto.comm ? go(fill_tiles_batch<1, true, false, false, false>)
-                      : go(fill_tiles_batch<1, false, false, false, false>);
+        return proto.comm ? go(fill_tiles_batch<1, true, false, true, false, false>)
+                          : go(fill_tiles_batch<1, false, false, true, false, false>);
+    if (split) return go(fill_tiles_batch<1, true, true, false, false, false>);
+    return proto.comm ? go(fill_tiles_batch<1, true, false, false, false, false>)
+                      : go(fill_tiles_batch<1, false, false, false, false, false>);
 }
 
 }  // namespace rkr

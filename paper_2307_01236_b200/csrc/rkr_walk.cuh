@@ -72,14 +72,29 @@ __device__ void walk(const Geometry& g, const MV& mv, const V* __restrict__ opt,
         }
         out[4] = top;
     }
-    stack[sp++] = make_int4(0, s0, t0, m0);
-    while (sp > 0) {
-        const int4 e = stack[--sp];
-        if (e.x == 1) {  // deferred BlockBwd of an option turn (chain_dp.hpp:230)
-            emit(3, e.y, e.z);
-            continue;
+    // the cell expanded next stays in registers (the child an expansion
+    // would push and pop at once); the stack keeps the deferred BlockBwds
+    // and the left children of cuts
+    int cs = s0, ct = t0, cm = m0;
+    bool have = true;
+    for (;;) {
+        if (!have) {
+            bool found = false;
+            while (sp > 0) {
+                const int4 e = stack[--sp];
+                if (e.x == 1) {  // deferred BlockBwd of an option turn (chain_dp.hpp:230)
+                    emit(3, e.y, e.z);
+                    continue;
+                }
+                cs = e.y;
+                ct = e.z;
+                cm = e.w;
+                found = true;
+                break;
+            }
+            if (!found) break;
         }
-        const int s = e.y, t = e.z, m = e.w;
+        const int s = cs, t = ct, m = cm;
         // table.opt(s,t,m) >= kInfTime -> InfeasibleBudget (chain_dp.hpp:213-215)
         const int64_t rid = row_id(L, s, t);
         bool inf = m < 0;
@@ -102,9 +117,12 @@ __device__ void walk(const Geometry& g, const MV& mv, const V* __restrict__ opt,
             if (s == t) {
                 if (t == L - 1) emit(0, t, -1);
                 emit(3, s, val);
+                have = false;
             } else {
                 stack[sp++] = make_int4(1, s, val, 0);
-                stack[sp++] = make_int4(0, s + 1, t, m - mv.chg(q));
+                cs = s + 1;  // (s + 1, t, m - chg) next
+                cm = m - mv.chg(q);
+                have = true;
             }
         } else {  // Cut (chain_dp.hpp:233-244)
             const int c = code & 0x7fff;
@@ -113,8 +131,10 @@ __device__ void walk(const Geometry& g, const MV& mv, const V* __restrict__ opt,
                 emit(2, j, 0);
                 emit(1, j, -1);
             }
-            stack[sp++] = make_int4(0, s, c - 1, m);             // left, after
-            stack[sp++] = make_int4(0, c, t, m - mv.act(c));     // right, first
+            stack[sp++] = make_int4(0, s, c - 1, m);  // left, after
+            cs = c;                                   // right, next
+            cm = m - mv.act(c);
+            have = true;
             // the left child is expanded after the whole right subtree: pull
             // its cell into L1 now so that hop costs an L1 hit
             if (m >= 0) {

@@ -574,8 +574,10 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 xcode[(kNT >> 1) + u * 32 + lane] = (uint16_t)code;
             }
         }
-        if (TS == 2) {
-            nb_sync_n(kBarSplit, kNC * 32);  // compute warps only
+        if (TS == 2 && warp < 2 * units) {
+            // only the 2 * units tail warps meet here (warp w < 2 * units took
+            // v = w): the others go straight on to bulk(k+1)
+            nb_sync_n(kBarSplit, 2 * units * 32);
             for (int u = warp; u < units; u += kNC) {
                 const int s = u / WC;
                 const int m = m_lo + (u - s * WC) * 32 + lane;

@@ -21,6 +21,10 @@ for width in ("auto", "64"):
     with rotor.ShardedTable(synthetic_menu(12, 4, 900, 6), 1, 900, 3, width=width) as sh:
         sh.download()
         sh.backtrack(0, 11, 900)
+# K1t split tails (>= 2 option batches: 12 options per block)
+with rotor.DpTable(synthetic_menu(14, 12, 600, 7, tie_stress=True), 1, 600, kernel="tiles") as t:
+    t.refill_walk(0, 13, 600)
+    t.backtrack_fetch()
 # K1t without the communication warp (the large-table variant)
 os.environ["RKR_COMM"] = "0"
 with rotor.DpTable(synthetic_menu(10, 4, 600, 5), 1, 600, kernel="tiles") as t:

@@ -295,7 +295,8 @@ struct rkr_table {
     int4* stack = nullptr;
     int64_t* dout = nullptr;      // device scratch: backtrack result / first-feasible
     int64_t hout[8] = {};
-    int32_t* dops = nullptr;      // device op buffer (separate, grows on demand)
+    int64_t* wrec = nullptr;      // walk record (8 x int64) | op buffer: one allocation, one D2H
+    int32_t* dops = nullptr;      // device op buffer (wrec + 64 B, grows on demand)
     int64_t dops_cap = 0;
     bool bt_pending = false;
     int kernel = 0;               // RKR_KERNEL_PERSISTENT or RKR_KERNEL_DIAGONAL
@@ -350,7 +351,7 @@ void free_table(rkr_table* t) {
         t->block = nullptr;
     }
     if (t->block && t->owns_block) cudaFreeAsync(t->block, t->stream);
-    if (t->dops) cudaFreeAsync(t->dops, t->stream);
+    if (t->wrec) cudaFreeAsync(t->wrec, t->stream);
     delete t;
 }
 
@@ -545,7 +546,8 @@ rkr_status alloc_and_upload(rkr_table* t) {
 rkr_status ensure_ops(rkr_table* t) {
     if (t->dops_cap == 0) {
         const int64_t cap = std::max<int64_t>(4096, 8 * (int64_t)t->g.L + 64);
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->dops), (size_t)cap * 12, t->stream));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->wrec), 64 + (size_t)cap * 12, t->stream));
+        t->dops = reinterpret_cast<int32_t*>(t->wrec + 8);
         t->dops_cap = cap;
     }
     return RKR_OK;
@@ -563,7 +565,7 @@ rkr_status enqueue_fill(rkr_table* t, bool walk = false, int32_t s = 0, int32_t 
         rkr_status st = enqueue_fill(t);
         if (st) return st;
         if (launch_backtrack(t->ctx(), s, tt, m, t->dops, t->dops_cap,
-                             reinterpret_cast<int32_t*>(t->stack), t->dout))
+                             reinterpret_cast<int32_t*>(t->stack), t->wrec))
             return cuda_fail(cudaGetLastError(), "backtrack launch");
         return RKR_OK;
     }
@@ -584,7 +586,7 @@ rkr_status enqueue_fill(rkr_table* t, bool walk = false, int32_t s = 0, int32_t 
         tp.wm = m;
         tp.wops = t->dops;
         tp.wcap = t->dops_cap;
-        tp.wout = t->dout;
+        tp.wout = t->wrec;
         tp.wstack = reinterpret_cast<int4*>(t->stack);
         if (tp.jobs) {  // more tiles than SMs: one-table tile jobs
             if (launch_fill_tiles_batch(t->ddesc, t->dtp, t->djobs, tp.T,
@@ -957,7 +959,7 @@ rkr_status rkr_backtrack_async(rkr_table* t, int32_t s, int32_t tt, int32_t m) {
     st = ensure_ops(t);
     if (st) return st;
     if (launch_backtrack(t->ctx(), s, tt, m, t->dops, t->dops_cap,
-                         reinterpret_cast<int32_t*>(t->stack), t->dout))
+                         reinterpret_cast<int32_t*>(t->stack), t->wrec))
         return cuda_fail(cudaGetLastError(), "backtrack launch");
     t->bt_s = s;
     t->bt_t = tt;
@@ -977,22 +979,22 @@ rkr_status rkr_backtrack_fetch(rkr_table* t, rkr_op* ops, int64_t cap, int64_t* 
     const int64_t est = std::min<int64_t>({cap, t->dops_cap, 16 * (int64_t)t->g.L + 64});
     void* pin = nullptr;
     CK(t_back.get(64 + (size_t)std::max<int64_t>(est, 0) * 12, &pin));
-    CK(cudaMemcpyAsync(pin, t->dout, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, t->stream));
-    if (est > 0)
-        CK(cudaMemcpyAsync(static_cast<char*>(pin) + 64, t->dops, (size_t)est * 12,
-                           cudaMemcpyDeviceToHost, t->stream));
+    // (the record and the ops are adjacent: one copy)
+    CK(cudaMemcpyAsync(pin, t->wrec, 64 + (size_t)std::max<int64_t>(est, 0) * 12,
+                       cudaMemcpyDeviceToHost, t->stream));
     CK(cudaStreamSynchronize(t->stream));
     std::memcpy(t->hout, pin, 5 * sizeof(int64_t));
     int64_t n = t->hout[0];
     const bool have = n <= est;  // ops already on the host
     if (n > t->dops_cap) {  // grow the device op buffer and walk again (rare)
-        CK(cudaFreeAsync(t->dops, t->stream));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->dops), (size_t)n * 12, t->stream));
+        CK(cudaFreeAsync(t->wrec, t->stream));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&t->wrec), 64 + (size_t)n * 12, t->stream));
+        t->dops = reinterpret_cast<int32_t*>(t->wrec + 8);
         t->dops_cap = n;
         if (launch_backtrack(t->ctx(), t->bt_s, t->bt_t, t->bt_m, t->dops, t->dops_cap,
-                             reinterpret_cast<int32_t*>(t->stack), t->dout))
+                             reinterpret_cast<int32_t*>(t->stack), t->wrec))
             return cuda_fail(cudaGetLastError(), "backtrack launch");
-        CK(cudaMemcpyAsync(t->hout, t->dout, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost,
+        CK(cudaMemcpyAsync(t->hout, t->wrec, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost,
                            t->stream));
         CK(cudaStreamSynchronize(t->stream));
         n = t->hout[0];

@@ -97,14 +97,15 @@ __device__ void walk(const Geometry& g, const MV& mv, const V* __restrict__ opt,
         const int s = cs, t = ct, m = cm;
         // table.opt(s,t,m) >= kInfTime -> InfeasibleBudget (chain_dp.hpp:213-215)
         const int64_t rid = row_id(L, s, t);
-        bool inf = m < 0;
+        const bool inf = m < 0;
         const int mm = m > M ? M : (m < 0 ? 0 : m);
-        // L1-cached loads (the walk runs in its own launch, or after the
-        // fill's acquire fence, so L1 holds no stale line); both in flight
-        const V v = __ldca(opt + rid * g.sr + g.pad + mm);
+        // One table read per hop: a cell's code is 0 exactly when its value
+        // is infinite (every fill updates value and code together, with a
+        // strict '<' from infinity), so the code alone decides.  L1-cached
+        // load (the walk runs in its own launch, or after the fill's acquire
+        // fence, so L1 holds no stale line).
         const uint16_t code = __ldca(arg + rid * g.sa + mm);
-        inf = inf || v >= Cost<V>::inf;
-        if (inf || code == 0) {  // code 0 on a finite cell = "cell without a decision"
+        if (inf || code == 0) {  // infinite (or undecided) cell
             status = 2;
             bad_s = s;
             bad_t = t;
@@ -140,7 +141,6 @@ __device__ void walk(const Geometry& g, const MV& mv, const V* __restrict__ opt,
             if (m >= 0) {
                 const int64_t lr = row_id(L, s, c - 1);
                 const int mm = m > M ? M : m;
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(opt + lr * g.sr + g.pad + mm));
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(arg + lr * g.sa + mm));
             }
         }

@@ -131,9 +131,18 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
             return fail(RKR_ERR_ARGUMENT, "option_offsets not monotone at block %d", i);
     h.L = L;
     const size_t nopt = (size_t)m->option_offsets[L] - (size_t)m->option_offsets[0];
+    // sized for every option up front (indexed writes, trimmed at the end)
     for (auto* v : {&h.fwd_req, &h.fwd_req_pre, &h.bwd_req, &h.pack_chg, &h.tftb, &h.chg_bt})
-        v->reserve(nopt);
-    h.ids.reserve(nopt);
+        v->resize(nopt);
+    h.ids.resize(nopt);
+    int64_t* const fwd_req = h.fwd_req.data();
+    int64_t* const fwd_req_pre = h.fwd_req_pre.data();
+    int64_t* const bwd_req = h.bwd_req.data();
+    int64_t* const pack_chg = h.pack_chg.data();
+    int64_t* const tftb = h.tftb.data();
+    int64_t* const chg_bt = h.chg_bt.data();
+    int32_t* const ids = h.ids.data();
+    int32_t nq = 0;  // saved options so far
     h.act_u.resize(L + 1);
     for (int32_t i = 0; i <= L; ++i) h.act_u[i] = to_units(m->act_sizes[i], unit);  // :59-60
     h.blk_off.assign(L + 1, 0);
@@ -147,14 +156,27 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
         const int64_t a_i = m->act_sizes[i];
         bool saw_zero = false;
         // build_schedule_rec looks an option up by id, first match in menu
-        // order (chain_dp.hpp:200-205, :228): first position of every id
-        first.clear();
-        for (int32_t o = m->option_offsets[i]; o < m->option_offsets[i + 1]; ++o)
-            first.emplace_back(m->option_id[o], o);
-        // (id, position) pairs: plain sort keeps the first position of an id
-        // first (no allocation, unlike stable_sort)
-        std::sort(first.begin(), first.end());
-        h.blk_off[i] = (int32_t)h.ids.size();
+        // order (chain_dp.hpp:200-205, :228): first position of every id --
+        // a backward scan for blocks of <= 32 options, else sorted
+        // (id, position) pairs (a plain sort keeps the first position of an
+        // id first, without stable_sort's allocation)
+        const int32_t o_lo = m->option_offsets[i], o_hi = m->option_offsets[i + 1];
+        const bool small = o_hi - o_lo <= 32;
+        auto first_pos = [&](int32_t o) {
+            if (small) {
+                for (int32_t q = o_lo; q < o; ++q)
+                    if (m->option_id[q] == m->option_id[o]) return q;
+                return o;
+            }
+            return std::lower_bound(first.begin(), first.end(),
+                                    std::make_pair(m->option_id[o], INT32_MIN))->second;
+        };
+        if (!small) {
+            first.clear();
+            for (int32_t o = o_lo; o < o_hi; ++o) first.emplace_back(m->option_id[o], o);
+            std::sort(first.begin(), first.end());
+        }
+        h.blk_off[i] = nq;
         int64_t fmax = 0, bmax = 0;
         for (int32_t o = m->option_offsets[i]; o < m->option_offsets[i + 1]; ++o) {
             if (m->time_fwd[o] < 0) nonneg = false;
@@ -170,24 +192,26 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
                 return fail(RKR_ERR_INVALID, "saved option without a backward in block %d", i);
             if (m->time_bwd[o] < 0) nonneg = false;
             bmax = std::max(bmax, m->time_bwd[o]);
-            h.ids.push_back(m->option_id[o]);                                 // :86-92
-            h.fwd_req.push_back(to_units(m->peak_fwd[o] - a_i, unit));
-            h.fwd_req_pre.push_back(to_units(m->peak_fwd_pre[o] - a_i, unit));
-            h.bwd_req.push_back(to_units(m->peak_bwd[o] - a_i, unit));
-            h.pack_chg.push_back(to_units(m->save_mem[o] - a_i, unit));
-            h.tftb.push_back(m->time_fwd[o] + m->time_bwd[o]);
-            const int32_t p = std::lower_bound(first.begin(), first.end(),
-                                               std::make_pair(m->option_id[o], INT32_MIN))->second;
-            h.chg_bt.push_back(to_units(m->save_mem[p] - a_i, unit));
+            ids[nq] = m->option_id[o];                                        // :86-92
+            fwd_req[nq] = to_units(m->peak_fwd[o] - a_i, unit);
+            fwd_req_pre[nq] = to_units(m->peak_fwd_pre[o] - a_i, unit);
+            bwd_req[nq] = to_units(m->peak_bwd[o] - a_i, unit);
+            pack_chg[nq] = to_units(m->save_mem[o] - a_i, unit);
+            tftb[nq] = m->time_fwd[o] + m->time_bwd[o];
+            chg_bt[nq] = to_units(m->save_mem[first_pos(o)] - a_i, unit);
+            ++nq;
         }
         if (!saw_zero) return fail(RKR_ERR_INVALID, "block %d lacks option 0", i);  // :94
-        const int32_t n = (int32_t)h.ids.size() - h.blk_off[i];
+        const int32_t n = nq - h.blk_off[i];
         if (n > 0x7ffe) return fail(RKR_ERR_INVALID, "block %d has more than 32766 options", i);
         h.max_opts = std::max(h.max_opts, n);
         F += (long double)fmax;
         Bk += (long double)bmax;
     }
-    h.blk_off[L] = (int32_t)h.ids.size();
+    h.blk_off[L] = nq;
+    for (auto* v : {&h.fwd_req, &h.fwd_req_pre, &h.bwd_req, &h.pack_chg, &h.tftb, &h.chg_bt})
+        v->resize(nq);
+    h.ids.resize(nq);
     // Shifts index earlier budget columns; a negative one would read past
     // m_max, which is undefined behaviour in the reference (vector overrun).
     for (size_t q = 0; q < h.pack_chg.size(); ++q)

@@ -91,6 +91,25 @@ int64_t to_units(int64_t b, int64_t unit) {  // chain_dp.hpp:41 (unit 1: no divi
     return unit == 1 ? b : (b + unit - 1) / unit;
 }
 
+// to_units by one fixed unit, for the host precompute's hot loop: a
+// double-precision quotient corrected to the exact floor for numerators in
+// [0, 2^52) (one multiply instead of a 64-bit division), the plain
+// truncating division otherwise.
+struct UnitDiv {
+    int64_t u;
+    double inv;
+    explicit UnitDiv(int64_t unit) : u(unit), inv(1.0 / (double)unit) {}
+    int64_t operator()(int64_t b) const {
+        if (u == 1) return b;
+        const int64_t n = b + u - 1;
+        if (n < 0 || n >= (int64_t(1) << 52)) return n / u;
+        int64_t q = (int64_t)((double)n * inv);
+        if (q * u > n) --q;
+        else if ((q + 1) * u <= n) ++q;
+        return q;
+    }
+};
+
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 struct DeviceGuard {
@@ -130,6 +149,7 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
         if (m->option_offsets[i + 1] < m->option_offsets[i])
             return fail(RKR_ERR_ARGUMENT, "option_offsets not monotone at block %d", i);
     h.L = L;
+    const UnitDiv tu(unit);
     const size_t nopt = (size_t)m->option_offsets[L] - (size_t)m->option_offsets[0];
     // sized for every option up front (indexed writes, trimmed at the end)
     for (auto* v : {&h.fwd_req, &h.fwd_req_pre, &h.bwd_req, &h.pack_chg, &h.tftb, &h.chg_bt})
@@ -144,7 +164,7 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
     int32_t* const ids = h.ids.data();
     int32_t nq = 0;  // saved options so far
     h.act_u.resize(L + 1);
-    for (int32_t i = 0; i <= L; ++i) h.act_u[i] = to_units(m->act_sizes[i], unit);  // :59-60
+    for (int32_t i = 0; i <= L; ++i) h.act_u[i] = tu(m->act_sizes[i]);  // :59-60
     h.blk_off.assign(L + 1, 0);
     h.fwd0_own.assign(L, 0);
     h.fwd0_full.assign(L, 0);
@@ -182,8 +202,8 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
             if (m->time_fwd[o] < 0) nonneg = false;
             fmax = std::max(fmax, m->time_fwd[o]);
             if (m->option_id[o] == 0) {                                       // :76-81
-                h.fwd0_own[i] = to_units(m->peak_fwd[o] - a_i, unit);
-                h.fwd0_full[i] = to_units(m->peak_fwd[o], unit);
+                h.fwd0_own[i] = tu(m->peak_fwd[o] - a_i);
+                h.fwd0_full[i] = tu(m->peak_fwd[o]);
                 h.tf0[i] = m->time_fwd[o];
                 saw_zero = true;
                 continue;
@@ -193,12 +213,12 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
             if (m->time_bwd[o] < 0) nonneg = false;
             bmax = std::max(bmax, m->time_bwd[o]);
             ids[nq] = m->option_id[o];                                        // :86-92
-            fwd_req[nq] = to_units(m->peak_fwd[o] - a_i, unit);
-            fwd_req_pre[nq] = to_units(m->peak_fwd_pre[o] - a_i, unit);
-            bwd_req[nq] = to_units(m->peak_bwd[o] - a_i, unit);
-            pack_chg[nq] = to_units(m->save_mem[o] - a_i, unit);
+            fwd_req[nq] = tu(m->peak_fwd[o] - a_i);
+            fwd_req_pre[nq] = tu(m->peak_fwd_pre[o] - a_i);
+            bwd_req[nq] = tu(m->peak_bwd[o] - a_i);
+            pack_chg[nq] = tu(m->save_mem[o] - a_i);
             tftb[nq] = m->time_fwd[o] + m->time_bwd[o];
-            chg_bt[nq] = to_units(m->save_mem[first_pos(o)] - a_i, unit);
+            chg_bt[nq] = tu(m->save_mem[first_pos(o)] - a_i);
             ++nq;
         }
         if (!saw_zero) return fail(RKR_ERR_INVALID, "block %d lacks option 0", i);  // :94

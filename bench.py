@@ -473,31 +473,33 @@ def b200_arm_sweep(args, world, rank, local):
     by_chain = {}
     for _, ci, b, _, _ in rows:
         by_chain.setdefault(ci, []).append(b)
-    calls = []
-    for ci, bs in sorted(by_chain.items()):
-        n = len(bs)
-        cap = max(1024, 8 * n * menus[ci].L)
-        calls.append((menus[ci].struct(), (ctypes.c_int64 * n)(*bs), n, (ctypes.c_int32 * n)(),
-                      (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)(), (ctypes.c_int32 * n)(),
-                      (ctypes.c_int64 * n)(), (rotor.RkrOp * cap)(), cap,
-                      (ctypes.c_int64 * (n + 1))()))
+    # one rkr_sweep_chains call: every chain's budgets in one batch (the
+    # reference runs cmd_sweep once per chain; the results are identical)
+    chains = sorted(by_chain)
+    structs = [menus[ci].struct() for ci in chains]
+    mp = (ctypes.POINTER(rotor.RkrMenu) * len(chains))(*[ctypes.pointer(x) for x in structs])
+    counts = (ctypes.c_int32 * len(chains))(*[len(by_chain[ci]) for ci in chains])
+    flat = [b for ci in chains for b in by_chain[ci]]
+    n = len(flat)
+    cap = max(1024, sum(8 * len(by_chain[ci]) * menus[ci].L for ci in chains))
+    b_ = (ctypes.c_int64 * n)(*flat)
+    st_, ot_, un_ = (ctypes.c_int32 * n)(), (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)()
+    mt_, mf_ = (ctypes.c_int32 * n)(), (ctypes.c_int64 * n)()
+    ops_, offs = (rotor.RkrOp * cap)(), (ctypes.c_int64 * (n + 1))()
     ex = rotor._exec(local, "auto")
     e2e = []
-    n_ops = 0
-    n_feas = 0
     for it in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        for ms_, b_, n, st_, ot_, un_, mt_, mf_, ops_, cap, offs in calls:
-            rc = lib.rkr_sweep(ctypes.byref(ms_), b_, n, SWEEP_UNITS, ctypes.byref(ex), st_, ot_,
-                               un_, mt_, mf_, ops_, cap, offs)
-            assert rc == 0, lib.rkr_last_error()
+        rc = lib.rkr_sweep_chains(mp, counts, len(chains), b_, SWEEP_UNITS, ctypes.byref(ex), st_,
+                                  ot_, un_, mt_, mf_, ops_, cap, offs)
+        assert rc == 0, lib.rkr_last_error()
         dt = time.perf_counter() - t0
         if it >= args.warmup:
             e2e.append(dt)
-    n_ops = sum(c[-1][c[2]] for c in calls)
-    n_feas = sum(sum(1 for i in range(c[2]) if c[3][i] == 0) for c in calls)
+    n_ops = offs[n]
+    n_feas = sum(1 for i in range(n) if st_[i] == 0)
     e2e_s = max_over_ranks(sum(e2e))
     cells_rank = sweep_cells(menus, rows)
     cells_total = sweep_cells(menus, rows_all)
@@ -524,8 +526,9 @@ def b200_arm_sweep(args, world, rank, local):
         "e2e": {"value": cells_total * args.steps / e2e_s, "unit": "cells/s",
                 "ms_per_step": 1e3 * e2e_s / args.steps,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 12 * n_ops,
-                "path": "one rkr_sweep C-ABI call per chain from host menus: fill + tops + "
-                        "schedules + min-feasible search, schedules copied back",
+                "path": "one rkr_sweep_chains C-ABI call (all chains' budgets in one batch) "
+                        "from host menus: fill + tops + schedules + min-feasible search, "
+                        "schedules copied back",
                 "feasible_budgets_rank0": n_feas},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

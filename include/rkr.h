@@ -231,6 +231,17 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
                      int32_t* m_top, int64_t* min_feasible, rkr_op* ops, int64_t ops_cap,
                      int64_t* ops_offsets);
 
+/* rkr_sweep over several chains at once (cmd_sweep for each, remat.cpp:217-
+ * 263, sharing one batch and one fill launch): chain c has n_budgets[c]
+ * budgets, stored consecutively in `budgets` in chain order; every output is
+ * indexed like `budgets` (total n = sum of n_budgets), with the results,
+ * statuses and op layout of one rkr_sweep call per chain, concatenated. */
+rkr_status rkr_sweep_chains(const rkr_menu* const* menus, const int32_t* n_budgets,
+                            int32_t n_chains, const int64_t* budgets, int32_t units,
+                            const rkr_exec* exec, int32_t* status, int64_t* opt_time,
+                            int64_t* unit, int32_t* m_top, int64_t* min_feasible, rkr_op* ops,
+                            int64_t ops_cap, int64_t* ops_offsets);
+
 /* ---- Budget-axis sharding (BASELINE config 5) -----------------------------
  * One table split into n contiguous budget ranges ("shards"), shard i on
  * devices[i] (NULL: all on exec->device).  Each shard is filled by the

@@ -1619,16 +1619,24 @@ void rkr_batch_destroy(rkr_batch* b) { free_batch(b); }
 // remat.cpp:240-255) with every table in one batched fill, the top cells
 // gathered in one launch, the schedules walked in one launch (a thread per
 // budget) and the infeasible budgets' min-feasible search batched the same way.
-rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, int32_t units,
-                     const rkr_exec* exec, int32_t* status, int64_t* opt_time, int64_t* unit_out,
-                     int32_t* m_top_out, int64_t* min_feasible, rkr_op* ops, int64_t ops_cap,
-                     int64_t* ops_offsets) {
-    if (!menu || !budgets || !status || !opt_time || !unit_out || !m_top_out || !min_feasible ||
+// rkr_sweep over budgets whose chains may differ: mfor[i] is budget i's menu
+// (one batch, one fill launch for all of them).
+static rkr_status sweep_impl(const rkr_menu* const* mfor, const int64_t* budgets, int32_t n,
+                             int32_t units, const rkr_exec* exec, int32_t* status,
+                             int64_t* opt_time, int64_t* unit_out, int32_t* m_top_out,
+                             int64_t* min_feasible, rkr_op* ops, int64_t ops_cap,
+                             int64_t* ops_offsets) {
+    if (!mfor || !budgets || !status || !opt_time || !unit_out || !m_top_out || !min_feasible ||
         !ops_offsets)
         return fail(RKR_ERR_ARGUMENT, "null argument");
     if (n < 1) return fail(RKR_ERR_ARGUMENT, "empty sweep");
-    if (menu->n_blocks <= 0 || !menu->act_sizes) return fail(RKR_ERR_INVALID, "empty option menu");
-    const int L = menu->n_blocks;
+    int Lmax = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        if (!mfor[i]) return fail(RKR_ERR_ARGUMENT, "null menu");
+        if (mfor[i]->n_blocks <= 0 || !mfor[i]->act_sizes)
+            return fail(RKR_ERR_INVALID, "empty option menu");
+        Lmax = std::max(Lmax, (int)mfor[i]->n_blocks);
+    }
     std::vector<int64_t> unit(n), a0u(n);
     std::vector<int32_t> mtop(n, -1);
     std::vector<int32_t> idx;  // budgets with a table
@@ -1636,7 +1644,7 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
         int64_t bu;
         rkr_status st = rkr_quantize(budgets[i], units, &unit[i], &bu);       // :257
         if (st) return st;
-        a0u[i] = to_units(menu->act_sizes[0], unit[i]);                        // :258
+        a0u[i] = to_units(mfor[i]->act_sizes[0], unit[i]);                    // :258
         const int64_t mt = bu - a0u[i];                                        // :259
         status[i] = RKR_ERR_INFEASIBLE;
         opt_time[i] = 0;
@@ -1655,10 +1663,11 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
     const int32_t* walk_ops = nullptr;  // pinned readback of every table's walk
     std::vector<std::vector<rkr_op>> big(nb);  // schedules that overflowed the batch slots
     if (nb > 0) {
-        std::vector<const rkr_menu*> ms(nb, menu);
+        std::vector<const rkr_menu*> ms(nb);
         std::vector<int64_t> us(nb);
         std::vector<int32_t> mm(nb);
         for (int q = 0; q < nb; ++q) {
+            ms[q] = mfor[idx[q]];
             us[q] = unit[idx[q]];
             mm[q] = mtop[idx[q]];
         }
@@ -1668,7 +1677,7 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
         if (st) return st;
         DeviceGuard dg(b->device);
         // scratch: m_at[nb] | active[nb] | tops[nb] | walk out[4 nb] | ops[nb * cap]
-        cap_each = std::max<int64_t>(256, 16 * (int64_t)L);
+        cap_each = std::max<int64_t>(256, 16 * (int64_t)Lmax);
         const size_t bytes = (size_t)nb * (4 + 1 + 8 + 64) + 64 + (size_t)nb * cap_each * 12;
         void* scr = nullptr;
         cudaError_t e = cudaMallocAsync(&scr, bytes, b->stream);
@@ -1719,7 +1728,7 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
             if (!act[q] || walk_out[8 * q] <= cap_each) continue;
             big[q].resize((size_t)walk_out[8 * q]);
             int64_t nn = 0;
-            st = rkr_backtrack(b->tables[q], 0, L - 1, mm[q], big[q].data(),
+            st = rkr_backtrack(b->tables[q], 0, ms[q]->n_blocks - 1, mm[q], big[q].data(),
                                (int64_t)big[q].size(), &nn);
         }
         rkr_batch_destroy(b);
@@ -1732,11 +1741,14 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
         if (top[q] >= kInf64) inf_q.push_back(q);
     if (!inf_q.empty()) {
         const int ni = (int)inf_q.size();
-        std::vector<const rkr_menu*> ms(ni, menu);
+        std::vector<const rkr_menu*> ms(ni);
         std::vector<int64_t> us(ni);
         std::vector<int32_t> caps(ni);
         for (int r = 0; r < ni; ++r) {
             const int i = idx[inf_q[r]];
+            const rkr_menu* menu = mfor[i];
+            const int L = menu->n_blocks;
+            ms[r] = menu;
             const int64_t u = unit[i];
             int64_t capu = 0;
             for (int bl = 0; bl < L; ++bl) {
@@ -1805,6 +1817,34 @@ rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, in
     if (result == RKR_OK && off > ops_cap)
         return fail(RKR_ERR_CAPACITY, "sweep schedules need %lld ops", (long long)off);
     return result;
+}
+
+rkr_status rkr_sweep(const rkr_menu* menu, const int64_t* budgets, int32_t n, int32_t units,
+                     const rkr_exec* exec, int32_t* status, int64_t* opt_time, int64_t* unit_out,
+                     int32_t* m_top_out, int64_t* min_feasible, rkr_op* ops, int64_t ops_cap,
+                     int64_t* ops_offsets) {
+    if (!menu) return fail(RKR_ERR_ARGUMENT, "null argument");
+    if (n < 1) return fail(RKR_ERR_ARGUMENT, "empty sweep");
+    std::vector<const rkr_menu*> mfor((size_t)n, menu);
+    return sweep_impl(mfor.data(), budgets, n, units, exec, status, opt_time, unit_out, m_top_out,
+                      min_feasible, ops, ops_cap, ops_offsets);
+}
+
+rkr_status rkr_sweep_chains(const rkr_menu* const* menus, const int32_t* n_budgets,
+                            int32_t n_chains, const int64_t* budgets, int32_t units,
+                            const rkr_exec* exec, int32_t* status, int64_t* opt_time,
+                            int64_t* unit_out, int32_t* m_top_out, int64_t* min_feasible,
+                            rkr_op* ops, int64_t ops_cap, int64_t* ops_offsets) {
+    if (!menus || !n_budgets) return fail(RKR_ERR_ARGUMENT, "null argument");
+    if (n_chains < 1) return fail(RKR_ERR_ARGUMENT, "no chains");
+    std::vector<const rkr_menu*> mfor;
+    for (int32_t c = 0; c < n_chains; ++c) {
+        if (n_budgets[c] < 0) return fail(RKR_ERR_ARGUMENT, "negative budget count");
+        mfor.insert(mfor.end(), (size_t)n_budgets[c], menus[c]);
+    }
+    if (mfor.size() > (size_t)INT32_MAX) return fail(RKR_ERR_ARGUMENT, "too many budgets");
+    return sweep_impl(mfor.data(), budgets, (int32_t)mfor.size(), units, exec, status, opt_time,
+                      unit_out, m_top_out, min_feasible, ops, ops_cap, ops_offsets);
 }
 
 }  // extern "C"

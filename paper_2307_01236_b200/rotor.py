@@ -124,6 +124,8 @@ def lib() -> ctypes.CDLL:
     L.rkr_batch_destroy.restype = None
     L.rkr_sweep.argtypes = [P(RkrMenu), P(i64), i32, i32, P(RkrExec), P(i32), P(i64), P(i64), P(i32),
                             P(i64), P(RkrOp), i64, P(i64)]
+    L.rkr_sweep_chains.argtypes = [P(P(RkrMenu)), P(i32), i32, P(i64), i32, P(RkrExec), P(i32),
+                                   P(i64), P(i64), P(i32), P(i64), P(RkrOp), i64, P(i64)]
     L.rkr_sharded_create.argtypes = [P(RkrMenu), i64, i32, i32, P(i32), P(RkrExec), P(p)]
     L.rkr_sharded_count.argtypes = [p]
     L.rkr_sharded_count.restype = i32
@@ -558,6 +560,48 @@ def sweep_raw(menu: Menu, budgets: Sequence[int], units: int, device: int = 0,
         r.ops = [(ops[o].kind, ops[o].block, ops[o].option) for o in range(offs[i], offs[i + 1])]
         rows.append(r)
     return rows
+
+
+def sweep_chains_raw(menus: Sequence[Menu], budgets: Sequence[Sequence[int]], units: int,
+                     device: int = 0, width: str = "auto") -> List[List[SweepRow]]:
+    """rkr_sweep_chains: sweep_raw for several chains in one batched device
+    call (one fill launch); rows per chain, budgets in the given order."""
+    L = lib()
+    nc = len(menus)
+    counts = [len(b) for b in budgets]
+    flat = [int(x) for b in budgets for x in b]
+    n = len(flat)
+    structs = [m.struct() for m in menus]
+    mp = (ctypes.POINTER(RkrMenu) * nc)(*[ctypes.pointer(x) for x in structs])
+    nb = (ctypes.c_int32 * nc)(*counts)
+    ex = _exec(device, width)
+    b = (ctypes.c_int64 * n)(*flat)
+    st = (ctypes.c_int32 * n)()
+    ot = (ctypes.c_int64 * n)()
+    un = (ctypes.c_int64 * n)()
+    mt = (ctypes.c_int32 * n)()
+    mf = (ctypes.c_int64 * n)()
+    offs = (ctypes.c_int64 * (n + 1))()
+    cap = max(1024, sum(8 * c * m.L for c, m in zip(counts, menus)))
+    while True:
+        ops = (RkrOp * cap)()
+        rc = L.rkr_sweep_chains(mp, nb, nc, b, units, ctypes.byref(ex), st, ot, un, mt, mf, ops,
+                                cap, offs)
+        if rc == RKR_ERR_CAPACITY and offs[n] > cap:
+            cap = offs[n]
+            continue
+        _check(rc)
+        break
+    out, i = [], 0
+    for c in counts:
+        rows = []
+        for _ in range(c):
+            r = SweepRow(flat[i], st[i] == RKR_OK, ot[i], un[i], mt[i], mf[i])
+            r.ops = [(ops[o].kind, ops[o].block, ops[o].option) for o in range(offs[i], offs[i + 1])]
+            rows.append(r)
+            i += 1
+        out.append(rows)
+    return out
 
 
 def sweep(menu: Menu, budgets: Sequence[int], units: int, device: int = 0,

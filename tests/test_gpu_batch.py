@@ -88,3 +88,27 @@ def test_sweep_helper_sorts_dedups_and_is_monotone():
     feas = [r.opt_time for r in rows if r.feasible]
     assert len(feas) > 10
     assert all(a >= b for a, b in zip(feas, feas[1:]))
+
+
+def test_sweep_chains_equals_one_sweep_per_chain(orc):
+    """rkr_sweep_chains (one batch over every chain's budgets) returns what
+    one rkr_sweep call per chain returns, and both match solve_chain."""
+    menus = [synthetic_menu(24, 8, 500, 41, byte_scale=1024),
+             synthetic_menu(9, 3, 200, 7, byte_scale=256, tie_stress=True),
+             synthetic_menu(33, 16, 4096, 44, byte_scale=64)]
+    budgets = [[1000, 20000, 70000, 512000, 5],
+               [300, 4000, 90000],
+               [5000, 60000, 400000, 7]]
+    multi = rotor.sweep_chains_raw(menus, budgets, 500)
+    for menu, bs, rows in zip(menus, budgets, multi):
+        single = rotor.sweep_raw(menu, bs, 500)
+        assert len(rows) == len(single) == len(bs)
+        for r, s in zip(rows, single):
+            assert (r.budget, r.feasible, r.opt_time, r.unit, r.m_top, r.min_feasible, r.ops) == \
+                   (s.budget, s.feasible, s.opt_time, s.unit, s.m_top, s.min_feasible, s.ops)
+            st, ops, ot, un, mt, mf = orc.solve_chain(menu, r.budget, 500)
+            assert r.feasible == (st == 0)
+            if st == 0:
+                assert (r.opt_time, r.ops) == (ot, ops)
+            else:
+                assert r.min_feasible == mf

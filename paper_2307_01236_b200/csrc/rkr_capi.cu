@@ -1443,8 +1443,19 @@ rkr_status batch_tables_upload(rkr_batch* b) {
     void* stage = nullptr;
     CK(t_stage.get(mt, &stage));
     unsigned char* sb = static_cast<unsigned char*>(stage);
-    parallel_for((int)b->tables.size(), [&](int i) { stage_menu(b->tables[i], sb + mo[i]); });
-    CK(cudaMemcpyAsync(b->mblock, stage, mt, cudaMemcpyHostToDevice, b->stream));
+    // staged and copied in chunks of ~16 MB: the DMA of one chunk overlaps
+    // the (16-thread) staging of the next
+    const int nt = (int)b->tables.size();
+    constexpr size_t kChunk = size_t(16) << 20;
+    for (int i0 = 0; i0 < nt;) {
+        int i1 = i0 + 1;
+        while (i1 < nt && mo[i1] - mo[i0] < kChunk) ++i1;
+        parallel_for(i1 - i0, [&](int i) { stage_menu(b->tables[i0 + i], sb + mo[i0 + i]); });
+        const size_t end = i1 < nt ? mo[i1] : mt;
+        CK(cudaMemcpyAsync(mb + mo[i0], sb + mo[i0], end - mo[i0], cudaMemcpyHostToDevice,
+                           b->stream));
+        i0 = i1;
+    }
     CK(cudaEventRecord(t_stage.done, b->stream));
     return RKR_OK;
 }

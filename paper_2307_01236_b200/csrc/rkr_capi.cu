@@ -352,6 +352,7 @@ struct rkr_table {
     ProgDev prog{};
     size_t state_bytes = 0;
     bool state_clean = false;     // the program launch zeroed the fill state
+    bool self_reset = false;      // the last co-resident K1t launch re-zeroed its state
     unsigned long long* trace = nullptr;
     int32_t bt_s = 0, bt_t = 0, bt_m = 0;
     InstDesc hdesc{};             // this table as the persistent kernel sees it
@@ -618,10 +619,12 @@ rkr_status enqueue_fill(rkr_table* t, bool walk = false, int32_t s = 0, int32_t 
         if (launch_fill_all(t->ctx())) return cuda_fail(cudaGetLastError(), "fill launch");
         return RKR_OK;
     }
-    if (t->state_clean)
-        t->state_clean = false;  // the program launch zeroed it (first fill)
-    else
+    if (t->state_clean || t->self_reset) {  // zeroed by the program launch (first
+        t->state_clean = false;             // fill) or by the previous co-resident
+        t->self_reset = false;              // K1t launch's last CTA
+    } else {
         CK(cudaMemsetAsync(t->pdev.counter, 0, t->state_bytes, t->stream));
+    }
     if (t->tiles) {
         TilePlan tp = t->tplan;
         tp.walk = walk ? 1 : 0;
@@ -641,6 +644,7 @@ rkr_status enqueue_fill(rkr_table* t, bool walk = false, int32_t s = 0, int32_t 
         }
         if (launch_fill_tiles(t->hdesc, tp, t->width, t->stream))
             return cuda_fail(cudaGetLastError(), "tile fill launch");
+        t->self_reset = true;
         return RKR_OK;
     }
     if (launch_fill_batch(t->ddesc, &t->hdesc, t->lplan, t->width, t->plan.R,

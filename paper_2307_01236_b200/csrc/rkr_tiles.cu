@@ -703,8 +703,9 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
     // (build_schedule_rec, chain_dp.hpp:211-246).  Every CTA counts itself
     // out with an acq_rel add after its last publish; the one that sees T-1
     // has acquired every other tile's stores.  Saves the walk's launch and
-    // reads a table that is still hot in L2.
-    if (!tp.walk) return;
+    // reads a table that is still hot in L2.  The last CTA also returns the
+    // done flags and the counter to zero for the next launch (every CTA has
+    // stopped polling by then), so a refill needs no memset first.
     __syncthreads();
     int* s_last = reinterpret_cast<int*>(smem_raw + sm.blk);  // s_blk is done with
     if (tid == 0) {
@@ -717,6 +718,9 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
     }
     __syncthreads();
     if (!s_last[L + 1]) return;
+    if (tid == 0) *tp.fin = 0;
+    for (int i = tid - 32; i >= 0 && i < L * tp.T; i += kNT - 32) tp.done[i] = 0;  // warps 1..
+    if (!tp.walk) return;
     // menu lookups and the stack in shared memory (program and partial
     // buffers are free now); the global view when they do not fit
     int4* sstack = reinterpret_cast<int4*>(smem_raw + sm.best);

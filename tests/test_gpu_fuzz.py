@@ -84,3 +84,35 @@ def test_random_solve_chain_vs_oracle(orc, seed):
         else:
             with pytest.raises(rotor.ValidationError):
                 rotor.solve_chain(chain, menu, budget, units)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_refill_walks_vs_oracle(orc, seed):
+    """Odd menus, wider budgets, every persistent kernel: fill, then two
+    refill + fused-walk rounds on the same table (the K1t kernel re-zeroes its
+    own flags between launches) against the oracle's table and schedule."""
+    rng = np.random.default_rng(3000 + seed)
+    for _ in range(15):
+        menu = odd_menu(rng)
+        unit = int(rng.integers(1, 4))
+        M = int(rng.integers(0, 300))
+        st, *ref = orc.fill(menu, unit, M)
+        if st != 0:
+            continue
+        L = menu.L
+        for kernel in ("persistent", "tiles", "queue"):
+            with rotor.DpTable(menu, unit, M, kernel=kernel) as t:
+                for _rep in range(2):
+                    m = int(rng.integers(-2, M + 3))
+                    bst, bops = orc.build_schedule(menu, unit, M, tuple(ref[:3]), 0, L - 1, m)
+                    if bst == 0:
+                        t.refill_walk(0, L - 1, m)
+                        assert t.backtrack_fetch() == bops
+                    elif bst == 2:
+                        t.refill_walk(0, L - 1, m)
+                        with pytest.raises(rotor.InfeasibleBudget):
+                            t.backtrack_fetch()
+                    o, k, v = t.download()
+                    np.testing.assert_array_equal(o, ref[0])
+                    np.testing.assert_array_equal(k, ref[1])
+                    np.testing.assert_array_equal(v, ref[2])

@@ -655,7 +655,10 @@ __device__ __forceinline__ void last_walk(const InstDesc& D, const TilePlan& tp,
     // buffers are free now); the global view when they do not fit
     int4* sstack = reinterpret_cast<int4*>(smem_raw + sm.best);
     int32_t* mb = reinterpret_cast<int32_t*>(smem_raw + sm.prog);
-    const bool fit = 4ull * (2 * (L + 1) + 2 * (uint64_t)tp.nq) <= 2ull * sm.prog_bytes &&
+    // (the program region: two staged buffers, or one block of per-warp
+    // slices when programs are streamed)
+    const bool fit = 4ull * (2 * (L + 1) + 2 * (uint64_t)tp.nq) <=
+                         (tp.stream ? 1ull : 2ull) * sm.prog_bytes &&
                      16ull * (2 * L + 16) <= (uint64_t)tp.cap * 4;
     if (fit) {
         int32_t *b = mb, *a = b + L + 1, *id = a + L + 1, *gq = id + tp.nq;
@@ -725,7 +728,10 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
     // buffers are free now); the global view when they do not fit
     int4* sstack = reinterpret_cast<int4*>(smem_raw + sm.best);
     int32_t* mb = reinterpret_cast<int32_t*>(smem_raw + sm.prog);
-    const bool fit = 4ull * (2 * (L + 1) + 2 * (uint64_t)tp.nq) <= 2ull * sm.prog_bytes &&
+    // (the program region: two staged buffers, or one block of per-warp
+    // slices when programs are streamed)
+    const bool fit = 4ull * (2 * (L + 1) + 2 * (uint64_t)tp.nq) <=
+                         (tp.stream ? 1ull : 2ull) * sm.prog_bytes &&
                      16ull * (2 * L + 16) <= (uint64_t)tp.cap * 4;
     if (fit) {
         int32_t *b = mb, *a = b + L + 1, *id = a + L + 1, *gq = id + tp.nq;
@@ -915,8 +921,11 @@ int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const in
         return proto.comm ? go(fill_tiles_batch<1, true, false, false, true, false>)
                           : go(fill_tiles_batch<1, false, false, false, true, false>);
     }
-    if (proto.stream)  // (a single long table, or budget shards of one)
-        return proto.comm ? go(fill_tiles_batch<1, true, false, true, false, false>)
+    // (a single long table: the budget-shard instantiation, whose halo code
+    // is inert here -- its register allocation spills 8 bytes where the
+    // plain one spills 88)
+    if (proto.stream)
+        return proto.comm ? go(fill_tiles_batch<1, true, false, true, false, true>)
                           : go(fill_tiles_batch<1, false, false, true, false, false>);
     if (split) return go(fill_tiles_batch<1, true, true, false, false, false>);
     return proto.comm ? go(fill_tiles_batch<1, true, false, false, false, false>)

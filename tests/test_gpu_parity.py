@@ -440,7 +440,10 @@ def test_tiles_streamed_programs(orc, monkeypatch, env):
     as tile jobs: whole tables and the fused walk against the oracle."""
     for k_, v_ in env.items():
         monkeypatch.setenv(k_, v_)
-    for L, B, M, seed in [(12, 6, 200, 7), (40, 20, 900, 45), (3, 2, 20, 5), (70, 9, 300, 8)]:
+    # (200 x 32: the walk's menu copy (53 KB) exceeds the streamed kernels'
+    # 32 KB program slices and option slices -- it must use the global menu)
+    for L, B, M, seed in [(12, 6, 200, 7), (40, 20, 900, 45), (3, 2, 20, 5), (70, 9, 300, 8),
+                          (200, 32, 40, 9)]:
         menu = synthetic_menu(L, B, M, seed, tie_stress=True)
         st, o, k, v, _, _ = orc.fill(menu, 1, M)
         with rotor.DpTable(menu, 1, M, kernel="tiles") as t:

@@ -25,6 +25,13 @@ for width in ("auto", "64"):
 with rotor.DpTable(synthetic_menu(14, 12, 600, 7, tie_stress=True), 1, 600, kernel="tiles") as t:
     t.refill_walk(0, 13, 600)
     t.backtrack_fetch()
+# streamed K1t as tile jobs with the fused walk on a long chain (the walk's
+# menu copy does not fit the program slices: global-menu walk)
+os.environ["RKR_JOBS"] = "1"
+with rotor.DpTable(synthetic_menu(200, 32, 40, 9), 1, 40, kernel="tiles") as t:
+    t.refill_walk(0, 199, 40)
+    t.backtrack_fetch()
+del os.environ["RKR_JOBS"]
 # K1t without the communication warp (the large-table variant)
 os.environ["RKR_COMM"] = "0"
 with rotor.DpTable(synthetic_menu(10, 4, 600, 5), 1, 600, kernel="tiles") as t:

@@ -120,6 +120,11 @@ class Ref(_Base):
         L.ref_build_schedule.argtypes = [P(RkrMenu), i64, i32, i32, i32, i32, P(i32), i64, P(i64)]
         L.ref_table_bench.argtypes = [P(RkrMenu), i64, i32, i32, P(i64)]
         L.ref_table_bench.restype = ctypes.c_double
+        L.ref_solve_bench.argtypes = [P(RkrMenu), i64, i32, i32, P(i64), P(i64), P(i32), P(i32)]
+        L.ref_solve_bench.restype = ctypes.c_double
+        L.ref_fill_and_walk.argtypes = [P(RkrMenu), i64, i32, p, p, p, P(i64), i32, P(i32), P(i32),
+                                        P(i32), i64, P(i64)]
+        L.ref_fill_and_walk.restype = i32
         L.ref_rng_new.argtypes = [ctypes.c_uint32]
         L.ref_rng_new.restype = p
         L.ref_rng_free.argtypes = [p]
@@ -147,6 +152,47 @@ class Ref(_Base):
         ms = menu.struct()
         secs = self.lib.ref_table_bench(ctypes.byref(ms), unit, M, threads, ctypes.byref(top))
         return secs, top.value
+
+    def solve_bench(self, menu: Menu, budget: int, units: int, threads: int = 1):
+        """remat::solve_chain (fill + top cell + build_schedule_rec) on `threads`
+        concurrent host threads; returns (seconds of the slowest, status,
+        opt_time, n_ops, m_top) of thread 0."""
+        ot, no, mt, st = i64(), i64(), i32(), i32()
+        ms = menu.struct()
+        secs = self.lib.ref_solve_bench(ctypes.byref(ms), budget, units, threads, ctypes.byref(ot),
+                                        ctypes.byref(no), ctypes.byref(mt), ctypes.byref(st))
+        return secs, st.value, ot.value, no.value, mt.value
+
+    def fill_and_walk(self, menu: Menu, unit: int, M: int, cells, want_table: bool = True):
+        """One reference DpTable and build_schedule_rec from every (s, t, m) in
+        `cells`.  Returns (status, (opt, kind, value) or None, max_cands,
+        [(walk status, ops)])."""
+        rows = _tri_rows(menu.L)
+        if want_table:
+            o = np.empty((rows, M + 1), np.int64)
+            k = np.empty((rows, M + 1), np.int8)
+            v = np.empty((rows, M + 1), np.int32)
+            tp = (o.ctypes.data, k.ctypes.data, v.ctypes.data)
+        else:
+            o = k = v = None
+            tp = (None, None, None)
+        n = len(cells)
+        stm = np.array(cells, np.int32).reshape(-1)
+        wst = np.zeros(max(n, 1), np.int32)
+        cap = max(4096, 8 * menu.L * menu.L) * max(n, 1)
+        ops = np.zeros(3 * cap, np.int32)
+        off = np.zeros(n + 1, np.int64)
+        mc = i64()
+        ms = menu.struct()
+        st = self.lib.ref_fill_and_walk(ctypes.byref(ms), unit, M, *tp, ctypes.byref(mc), n,
+                                        stm.ctypes.data_as(P(i32)), wst.ctypes.data_as(P(i32)),
+                                        ops.ctypes.data_as(P(i32)), cap,
+                                        off.ctypes.data_as(P(i64)))
+        walks = []
+        for i in range(n):
+            a, b = int(off[i]), int(off[i + 1])
+            walks.append((int(wst[i]), [tuple(int(x) for x in ops[3 * q:3 * q + 3]) for q in range(a, b)]))
+        return st, ((o, k, v) if want_table else None), mc.value, walks
 
     def random_menus(self, seed: int, count: int, max_blocks: int, max_options: int) -> List[Menu]:
         """Successive testing::random_menu(rng, max_blocks, max_options) draws from

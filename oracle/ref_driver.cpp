@@ -173,6 +173,97 @@ double ref_table_bench(const FlatMenu* f, int64_t unit, int32_t m_max, int32_t n
     return worst;
 }
 
+// remat::solve_chain (DpTable + top cell + build_schedule_rec, chain_dp.hpp:
+// 255-296) -- the same work as the device solve -- run n_threads times
+// concurrently (one independent solve per host thread; the reference itself
+// is single-threaded).  Returns the wall seconds of the slowest thread;
+// *opt_time / *n_ops / *m_top describe thread 0's solution (status in *status).
+double ref_solve_bench(const FlatMenu* f, int64_t budget, int32_t units, int32_t n_threads,
+                       int64_t* opt_time, int64_t* n_ops, int32_t* m_top, int32_t* status) {
+    OptionMenu menu = to_menu(f);
+    Chain chain = skeleton_chain(menu.length());
+    if (n_threads < 1) n_threads = 1;
+    std::vector<double> secs(n_threads, 0.0);
+    std::vector<int64_t> ot(n_threads, -1), no(n_threads, 0);
+    std::vector<int32_t> mt(n_threads, -1), st(n_threads, 0);
+    auto work = [&](int i) {
+        auto t0 = std::chrono::steady_clock::now();
+        try {
+            ChainSolution sol = solve_chain(chain, menu, budget, units);
+            ot[i] = sol.opt_time;
+            no[i] = (int64_t)sol.schedule.ops.size();
+            mt[i] = sol.m_top;
+        } catch (const InfeasibleBudget&) {
+            st[i] = 2;
+        } catch (const ValidationError&) {
+            st[i] = 1;
+        }
+        auto t1 = std::chrono::steady_clock::now();
+        secs[i] = std::chrono::duration<double>(t1 - t0).count();
+    };
+    if (n_threads == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int i = 0; i < n_threads; ++i) th.emplace_back(work, i);
+        for (auto& x : th) x.join();
+    }
+    double worst = 0;
+    for (double s : secs) worst = s > worst ? s : worst;
+    if (opt_time) *opt_time = ot[0];
+    if (n_ops) *n_ops = no[0];
+    if (m_top) *m_top = mt[0];
+    if (status) *status = st[0];
+    return worst;
+}
+
+// One DpTable, then build_schedule_rec from n cells (stm = {s, t, m} triples):
+// the whole table (as ref_table_fill) and every walk's ops, concatenated in
+// ops (ops_off[i] .. ops_off[i+1]); status[i] = 0 / 2 (InfeasibleBudget).
+// Returns 0, 1 (ValidationError) or 5 (ops_cap too small).
+int ref_fill_and_walk(const FlatMenu* f, int64_t unit, int32_t m_max, int64_t* opt, int8_t* kind,
+                      int32_t* value, int64_t* max_cands, int32_t n, const int32_t* stm,
+                      int32_t* status, int32_t* ops, int64_t ops_cap, int64_t* ops_off) {
+    try {
+        OptionMenu menu = to_menu(f);
+        DpTable table(menu, unit, m_max);
+        const int L = table.length();
+        if (opt)
+            for (int s = 0; s < L; ++s)
+                for (int t = s; t < L; ++t) {
+                    size_t r = tri_row(L, s, t) * (size_t)(m_max + 1);
+                    for (int m = 0; m <= m_max; ++m) {
+                        opt[r + m] = table.opt(s, t, m);
+                        DpArg a = table.arg(s, t, m);
+                        kind[r + m] = (int8_t)a.kind;
+                        value[r + m] = a.value;
+                    }
+                }
+        if (max_cands) *max_cands = table.max_candidates_per_cell;
+        Chain chain = skeleton_chain(L);
+        int64_t pos = 0;
+        ops_off[0] = 0;
+        for (int i = 0; i < n; ++i) {
+            std::vector<ScheduleOp> out;
+            status[i] = 0;
+            try {
+                build_schedule_rec(table, menu, chain, stm[3 * i], stm[3 * i + 1], stm[3 * i + 2], out);
+            } catch (const InfeasibleBudget&) {
+                status[i] = 2;
+                out.clear();
+            }
+            int64_t k = ops_to_triples(out, ops + 3 * pos, ops_cap - pos);
+            if (k < 0) return 5;
+            pos += k;
+            ops_off[i + 1] = pos;
+        }
+        return 0;
+    } catch (const ValidationError& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 int ref_build_schedule(const FlatMenu* f, int64_t unit, int32_t m_max, int32_t s, int32_t t,
                        int32_t m, int32_t* ops, int64_t cap, int64_t* n_ops) {
     try {

@@ -40,6 +40,19 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+PROBE_SRC = os.path.join(ROOT, "tools", "l2probe.cu")
+PROBE_LIB = os.path.join(ROOT, "tools", "libl2probe.so")
+
+
+def build_probe(force: bool = False) -> str:
+    """tools/libl2probe.so: the L2 read-bandwidth micro-benchmark bench.py's
+    roofline uses (measurement infrastructure, not the solver)."""
+    if force or _stale(PROBE_LIB, [PROBE_SRC]):
+        subprocess.run(["nvcc", *NVCC_FLAGS, "-o", PROBE_LIB + ".tmp", PROBE_SRC], check=True)
+        os.replace(PROBE_LIB + ".tmp", PROBE_LIB)
+    return PROBE_LIB
+
+
 CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_chain_dp_b200.cpp")
 CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "test_chain_dp_b200")
 
@@ -59,4 +72,5 @@ def build_cpp_tests(force: bool = False) -> str:
 if __name__ == "__main__":
     build_lib(force="--force" in sys.argv, verbose="-v" in sys.argv)
     build_cpp_tests(force="--force" in sys.argv)
+    build_probe(force="--force" in sys.argv)
     print(LIB)

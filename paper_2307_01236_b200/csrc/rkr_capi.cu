@@ -644,7 +644,9 @@ rkr_status enqueue_fill(rkr_table* t, bool walk = false, int32_t s = 0, int32_t 
         }
         if (launch_fill_tiles(t->hdesc, tp, t->width, t->stream))
             return cuda_fail(cudaGetLastError(), "tile fill launch");
-        t->self_reset = true;
+        // the last CTA re-zeroes the done flags and its counter -- but not a
+        // budget shard's halo counters, so shard tables memset before a refill
+        t->self_reset = !tp.halo;
         return RKR_OK;
     }
     if (launch_fill_batch(t->ddesc, &t->hdesc, t->lplan, t->width, t->plan.R,
@@ -729,8 +731,7 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
             // batch tables need no co-residency (their tiles are queued jobs)
             t->tiles = tile_plan(t->g, t->width, batch_tiles ? INT32_MAX : sms, (int64_t)h.ids.size(),
-                                 (int)round_up(std::max<int32_t>(h.max_opts, 1), kTileOptBatch), t->tplan,
-                                 kreq == RKR_KERNEL_TILES && !batch_tiles) == 1;
+                                 (int)round_up(std::max<int32_t>(h.max_opts, 1), kTileOptBatch), t->tplan) == 1;
         }
         if (kreq == RKR_KERNEL_TILES && !t->tiles) {
             delete t;

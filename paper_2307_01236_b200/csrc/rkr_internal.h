@@ -202,10 +202,9 @@ struct TilePlan {
     int32_t* done = nullptr;              // [L * T]
     unsigned long long* trace = nullptr;  // optional: 6 stamps per (k, j)
 };
-// 1 = eligible.  allow_stream: long chains may run the streamed-program
-// variant (only on an explicit RKR_KERNEL_TILES request; else they run K1p).
-int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp,
-              bool allow_stream = false);
+// 1 = eligible.  Long chains, whose per-step programs do not fit shared
+// memory, get the streamed-program variant (tp.stream = 1) by default.
+int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp);
 int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream);
 // Batches: jobs (table, tile) in queue order; tps[i].sm is the batch-wide
 // layout (tile_batch_smem of a plan with every table's maxima).
@@ -246,28 +245,26 @@ int launch_first_feasible(const LaunchCtx& c, int32_t s, int32_t t, int32_t* dev
 int launch_export(const LaunchCtx& c, int64_t r0, int64_t r1, int64_t* opt, int8_t* kind,
                   int32_t* value);
 
-// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, smem), skipped when the
-// kernel already has exactly that value on this device (the call costs host
-// time on every launch otherwise; the value itself is kept as before: the
-// launch's own size, never a larger one)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, smem) for a launch of
+// `smem` bytes.  The attribute only ever GROWS (per kernel and device): a
+// launch with a smaller size runs under a larger limit, so a thread that
+// checked the limit for its launch can never have it lowered underneath it by
+// another thread's table (the check-then-launch race of a set-to-exact-size
+// scheme).  The call is skipped when the limit already covers the request
+// (it costs host time on every launch otherwise).
 inline cudaError_t set_dyn_smem(const void* kern, size_t smem) {
     if (smem <= 48 * 1024) return cudaSuccess;
     int dev = 0;
     cudaGetDevice(&dev);
     static std::mutex mu;
-    static std::unordered_map<const void*, int> last[64];
-    auto& m = last[dev & 63];
-    {
-        std::lock_guard<std::mutex> g(mu);
-        auto it = m.find(kern);
-        if (it != m.end() && it->second == (int)smem) return cudaSuccess;
-    }
+    static std::unordered_map<const void*, int> limit[64];
+    std::lock_guard<std::mutex> g(mu);  // held across the set: the map and the attribute agree
+    auto& m = limit[dev & 63];
+    auto it = m.find(kern);
+    if (it != m.end() && it->second >= (int)smem) return cudaSuccess;
     const cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) {
-        std::lock_guard<std::mutex> g(mu);
-        m[kern] = (int)smem;
-    }
+    if (e == cudaSuccess) m[kern] = (int)smem;
     return e;
 }
 

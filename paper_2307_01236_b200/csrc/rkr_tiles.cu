@@ -812,8 +812,7 @@ int launch_tiles_t(const InstDesc& d, const TilePlan& tp, cudaStream_t st) {
 
 // Narrowest tile (W = 32 WC) whose T tiles fit one CTA per SM; 0 = not
 // eligible (the queue-scheduled K1p runs instead).
-int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp,
-              bool allow_stream) {
+int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp) {
     if (const char* e = getenv("RKR_TILES"))  // tuning knob: 0 disables K1t
         if (atoi(e) == 0) return 0;
     if (width != 32) return 0;
@@ -857,7 +856,6 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TileP
             // stages its unit's program, options and thresholds into its own
             // slice); with the communication warp it beats the row-segment
             // queue (L=256, B=64, M=4096: 25.9 ms against K1p's 27.0 ms)
-            (void)allow_stream;
             tp.stream = 1;
             tp.split = 0;
             if (!getenv("RKR_COMM")) tp.comm = 1;

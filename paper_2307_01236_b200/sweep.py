@@ -81,16 +81,18 @@ class SweepInstance:
 
 def sweep_workload(n_budgets: int = 256, byte_scale: int = 1024):
     """Menus (bytes, so quantization is exercised) and the instance list:
-    for each chain, budgets evenly spaced from 1/8 of its no-recompute peak
-    (infeasible at the low end: the min-feasible search runs too) up to the
-    peak itself."""
+    for each chain, budgets evenly spaced from 1/32 of its no-recompute peak
+    up to the peak itself (min-feasible .. chain_max_peak).  The
+    min-feasible budgets of these chains sit at 4-9 % of the peak (chain 0:
+    below 1/32 the top slot is negative), so the low end of every sweep but
+    chain 0's is infeasible and the batched min-feasible search runs too."""
     menus: List[Menu] = []
     inst: List[SweepInstance] = []
     for ci, (_, L, B) in enumerate(SWEEP_CHAINS):
         m = synthetic_menu(L, B, SWEEP_UNITS, seed=400 + ci, byte_scale=byte_scale)
         menus.append(m)
         hi = one_pass_peak(m)
-        for b in even_spacing(hi // 8, hi, n_budgets):
+        for b in even_spacing(hi // 32, hi, n_budgets):
             inst.append(SweepInstance(ci, b))
     return menus, inst
 

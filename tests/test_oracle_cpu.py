@@ -149,3 +149,27 @@ def test_oracle_against_reference_directly(orc):
     a, b = orc.fill(m, 1, 300), ref.fill(m, 1, 300)
     for x, y in zip(a[1:4], b[1:4]):
         np.testing.assert_array_equal(x, y)
+
+
+def test_oracle_matches_large_config4_goldens(orc):
+    """The C restatement reproduces the reference's config-4 solve_chain results
+    (tests/golden/large_cfg4.json) on a spread of the cheaper chains' budgets."""
+    import json
+    import os
+
+    from helpers import ops_digest
+    from paper_2307_01236_b200.sweep import sweep_workload
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "large_cfg4.json")))
+    menus, inst = sweep_workload()
+    assert [(x.chain, x.budget) for x in inst] == [(e["chain"], e["budget"]) for e in g["instances"]]
+    picks = [e for e in g["instances"] if e["chain"] < 2][::12]
+    picks += [e for e in g["instances"] if e["status"] == 2][:6]
+    for e in picks:
+        st, ops, ot, un, mt, mf = orc.solve_chain(menus[e["chain"]], e["budget"], g["units"])
+        assert st == e["status"]
+        if st == 0:
+            assert (ot, un, mt, ops_digest(ops)) == (e["opt_time"], e["unit"], e["m_top"],
+                                                     e["ops_digest"])
+        else:
+            assert mf == e["min_feasible"]

@@ -37,6 +37,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "rkr_internal.h"
 #include "rkr_walk.cuh"
@@ -153,7 +154,7 @@ inline TileSmem tile_smem(const TilePlan& tp) {
         m.thr = (uint32_t)b;  // per-warp option slices: [kNW][ocap] int2 | [kNW][ocap] int
         b = al16(b + (uint64_t)kNW * tp.ocap * 12);
     } else {
-        b = al16(b + L * tp.ocap * 8);  // [block][ocap] {pack shift, pass time}, padded
+        b = al16(b + L * tp.ocap * 8);  // [block][ocap] {-pack shift, pass time}, padded
         m.prog = (uint32_t)b;
         b += 2ull * m.prog_bytes;
         m.thr = (uint32_t)b;
@@ -181,12 +182,33 @@ __device__ __forceinline__ void stage_step(const TilePlan& tp, const ProgDev& pq
     bulk_g2s(smem + sm.thr + b * sm.thr_bytes, pq.thr + diag_off(L, k) * tp.ocap, tb, bars + b);
 }
 
+// The lane's table base opt + m as an opaque 64-bit register, so that a
+// table address is ONE IMAD.WIDE.U32 (entry offset x 4 + base) instead of
+// the compiler's re-associated 64-bit (m + offset) sum (four instructions).
+__device__ __forceinline__ const uint32_t* lane_base(const uint32_t* opt, int m) {
+    const uint32_t* p;
+    asm("mov.b64 %0, %1;" : "=l"(p) : "l"(opt + m));
+    return p;
+}
+
 // Cuts i in [ib, ie) of one cell slice, ascending, strict '<' into (best,
 // code).  Program entry i of cell (s, s+k): element offsets of slot 0 of the
 // left row (s, c-1) and of the right row (c, t) shifted by act_u[c]
 // (:166-167), the option-0 sweep (:162) and the gate (:159, :164).
+//
+// Instruction budget per candidate (the fill is issue-bound, ncu: 58 % issue
+// slots busy on config 3): one LDS.128 (program entry), two IMAD.WIDE (lane
+// base + entry offset: the lane's `optm = opt + m` is formed once), two LDG,
+// one IADD3 (sweep + left + right), one VIMNMX with predicate output (DPX
+// __vibmin_u32: min and "kept the old best" in one instruction) and one
+// predicated code update.  The gate (:159, :164) is only tested per candidate
+// in a batch where the warp is split by it: it grows with i and the lanes'
+// budgets are consecutive, so when lane 0 (the smallest m) admits the
+// batch's last cut, every lane admits every cut of the batch.
 __device__ __forceinline__ bool scan_cuts(const uint32_t* __restrict__ opt, const int4* pe, int ib,
                                           int ie, int m, int cb, uint32_t& best, int& code) {
+    const uint32_t* __restrict__ optm = lane_base(opt, m);
+    const int m0 = m - (int)(threadIdx.x & 31);  // warp-uniform: the smallest budget
     int i0 = ib;
     for (; i0 + kU <= ie; i0 += kU) {
         uint32_t lv[kU], rv[kU];
@@ -196,8 +218,17 @@ __device__ __forceinline__ bool scan_cuts(const uint32_t* __restrict__ opt, cons
             e[q] = pe[i0 + q];
             // unconditional loads (every offset is inside the table); the
             // gate masks the candidate afterwards
-            lv[q] = __ldcg(opt + (uint32_t)(e[q].x + m));
-            rv[q] = __ldcg(opt + (uint32_t)(e[q].y + m));
+            lv[q] = __ldcg(optm + (uint32_t)e[q].x);
+            rv[q] = __ldcg(optm + (uint32_t)e[q].y);
+        }
+        if (e[kU - 1].w <= m0) {  // (warp-uniform) no lane gated in this batch
+#pragma unroll
+            for (int q = 0; q < kU; ++q) {
+                bool keep;
+                best = __vibmin_u32(best, (uint32_t)e[q].z + lv[q] + rv[q], &keep);
+                if (!keep) code = cb + i0 + q;  // strictly smaller: the scan's first minimum
+            }
+            continue;
         }
 #pragma unroll
         for (int q = 0; q < kU; ++q) {
@@ -214,7 +245,7 @@ __device__ __forceinline__ bool scan_cuts(const uint32_t* __restrict__ opt, cons
     for (; i0 < ie; ++i0) {
         const int4 e = pe[i0];
         const uint32_t tot =
-            (uint32_t)e.z + __ldcg(opt + (uint32_t)(e.x + m)) + __ldcg(opt + (uint32_t)(e.y + m));
+            (uint32_t)e.z + __ldcg(optm + (uint32_t)e.x) + __ldcg(optm + (uint32_t)e.y);
         if (e.w <= m && tot < best) {
             best = tot;
             code = cb + i0;
@@ -270,7 +301,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     const int m_lo = j * W;
 
     // Table-independent data in shared memory: block option ranges, and per
-    // (block, option slot) the pack shift clamped to pad (:148) and time_fwd
+    // (block, option slot) the pack shift (negated) clamped to pad (:148) and time_fwd
     // + time_bwd (:150), padded to ocap with options that never win (pass
     // time INF).  Cut programs and thresholds arrive per step by bulk copy,
     // two steps ahead (double buffer, one mbarrier per buffer).
@@ -293,7 +324,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         const int b = q / ocap, i = q - b * ocap;
         const int o = __ldg(dm.blk_off + b) + i;
         s_opd[q] = o < __ldg(dm.blk_off + b + 1)
-                       ? make_int2(__ldg(pq.pc + o), (int)__ldg(static_cast<const uint32_t*>(pq.otot) + o))
+                       ? make_int2(-__ldg(pq.pc + o), (int)__ldg(static_cast<const uint32_t*>(pq.otot) + o))
                        : make_int2(0, (int)INF);
     }
     const int d_eff = tp.d < j ? tp.d : j;  // lower tiles this one reads
@@ -494,7 +525,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 __syncwarp();  // the previous unit's readers are done
                 const int o0 = s_blk[s];
                 for (int i = lane; i < ocap; i += 32) {
-                    wo[i] = i < nopt ? make_int2(__ldg(pq.pc + o0 + i),
+                    wo[i] = i < nopt ? make_int2(-__ldg(pq.pc + o0 + i),
                                                  (int)__ldg(static_cast<const uint32_t*>(pq.otot) + o0 + i))
                                      : make_int2(0, (int)INF);
                     wt[i] = __ldg(thrs + s * ocap + i);
@@ -503,36 +534,47 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 od4 = reinterpret_cast<const int4*>(wo);
                 th4 = reinterpret_cast<const int4*>(wt);
             }
-            const int widx = k > 0 ? (rid - (L - k)) * sr + g.pad + m : 0;
-            // whole batches: the padding options never win
-            for (int i0 = ia; i0 < ib; i0 += kOB) {
-                uint32_t sub[kOB], ot[kOB];
-                int32_t th[kOB];
+            // whole batches: the padding options never win.  Diagonal 0 has
+            // no sub-row (chain_dp.hpp:146: s == t), so its loop is a separate
+            // instantiation without loads; otherwise each window read is one
+            // IMAD.WIDE off the lane's row base (shifts stored negated).
+            auto options = [&](auto has_sub) {
+                constexpr bool SUB = decltype(has_sub)::value;
+                const uint32_t* __restrict__ optw =
+                    lane_base(opt, SUB ? (rid - (L - k)) * sr + g.pad + m : 0);
+                for (int i0 = ia; i0 < ib; i0 += kOB) {
+                    uint32_t sub[kOB], ot[kOB];
+                    int32_t th[kOB];
 #pragma unroll
-                for (int q = 0; q < kOB; q += 2) {
-                    const int4 o2 = od4[(i0 + q) >> 1];
-                    ot[q] = (uint32_t)o2.y;
-                    ot[q + 1] = (uint32_t)o2.w;
-                    sub[q] = k > 0 ? __ldcg(opt + (uint32_t)(widx - o2.x)) : 0u;
-                    sub[q + 1] = k > 0 ? __ldcg(opt + (uint32_t)(widx - o2.z)) : 0u;
-                }
+                    for (int q = 0; q < kOB; q += 2) {
+                        const int4 o2 = od4[(i0 + q) >> 1];
+                        ot[q] = (uint32_t)o2.y;
+                        ot[q + 1] = (uint32_t)o2.w;
+                        sub[q] = SUB ? __ldcg(optw + o2.x) : 0u;
+                        sub[q + 1] = SUB ? __ldcg(optw + o2.z) : 0u;
+                    }
 #pragma unroll
-                for (int q = 0; q < kOB; q += 4) {
-                    const int4 t4 = th4[(i0 + q) >> 2];
-                    th[q] = t4.x;
-                    th[q + 1] = t4.y;
-                    th[q + 2] = t4.z;
-                    th[q + 3] = t4.w;
-                }
+                    for (int q = 0; q < kOB; q += 4) {
+                        const int4 t4 = th4[(i0 + q) >> 2];
+                        th[q] = t4.x;
+                        th[q + 1] = t4.y;
+                        th[q + 2] = t4.z;
+                        th[q + 3] = t4.w;
+                    }
 #pragma unroll
-                for (int q = 0; q < kOB; ++q) {
-                    const uint32_t tot = ot[q] + sub[q];
-                    if (m >= th[q] && tot < best) {
-                        best = tot;
-                        code = i0 + q + 1;
+                    for (int q = 0; q < kOB; ++q) {
+                        const uint32_t tot = ot[q] + sub[q];
+                        if (m >= th[q] && tot < best) {
+                            best = tot;
+                            code = i0 + q + 1;
+                        }
                     }
                 }
-            }
+            };
+            if (k > 0)
+                options(std::true_type{});
+            else
+                options(std::false_type{});
             if (cuts) {
                 // Case 2 (chain_dp.hpp:158-174): cut i = 0, bulk parts, cut i = k-1
                 const int cb = kCutBit | (s + 1);

@@ -231,6 +231,14 @@ def ncu_pass(cfg_idx, timeout=240):
     cmd = [ncu, "--metrics", NCU_METRICS, "--clock-control", "none", "-k", "regex:fill_",
            "-s", "3", "-c", "1", "--csv", "--log-file", log, sys.executable,
            os.path.abspath(__file__), "--ncu-probe", "--config", str(cfg_idx)]
+    from paper_2307_01236_b200 import rotor
+
+    bits, rows = rotor._tuning.get()  # the same kernel variant as the timed run
+    flags = [k for k, v in rotor.TUNE.items() if bits & v]
+    if flags:
+        cmd += ["--tune", ",".join(flags)]
+    if rows:
+        cmd += ["--tile-rows", str(rows)]
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
         import csv
@@ -998,7 +1006,18 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU leg (tuning runs)")
     ap.add_argument("--no-ncu", action="store_true", help="skip the live ncu counter pass")
     ap.add_argument("--ncu-probe", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--tune", default="", help="A/B: comma-separated rkr_exec.tune flags (rotor.TUNE)")
+    ap.add_argument("--tile-rows", type=int, default=0, help="A/B: K1t rows per warp (0 = auto)")
     args = ap.parse_args()
+    if args.tune or args.tile_rows:
+        from paper_2307_01236_b200 import rotor
+        flags = [f for f in args.tune.split(",") if f]
+        with rotor.tuning(*flags, tile_rows=args.tile_rows):
+            return run(args)
+    return run(args)
+
+
+def run(args):
     if args.ncu_probe:
         ncu_probe_child(args.config)
         return

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define RKR_ABI_VERSION 1
+#define RKR_ABI_VERSION 2
 
 /* Mirrors remat::kInfTime (chain_dp.hpp:23). */
 #define RKR_INF_TIME ((int64_t)(INT64_MAX / 4))
@@ -93,14 +93,31 @@ typedef enum {
                                   the table does not fit) */
 } rkr_kernel;
 
+/* Kernel tuning overrides (rkr_exec.tune bits).  0 = the library's measured
+ * choices; the bits exist for A/B measurements and for
+ * tests that pin one variant.  Results are identical under every setting. */
+typedef enum {
+    RKR_TUNE_NO_TILES = 1 << 0,    /* never the budget-tile kernel (K1t) */
+    RKR_TUNE_JOBS = 1 << 1,        /* K1t as tile jobs even when its tiles fit one CTA per SM */
+    RKR_TUNE_COMM_OFF = 1 << 2,    /* K1t without the communication warp */
+    RKR_TUNE_COMM_ON = 1 << 3,     /* K1t with the communication warp */
+    RKR_TUNE_SPLIT_OFF = 1 << 4,   /* no split tails on late diagonals */
+    RKR_TUNE_SPLIT_ON = 1 << 5,    /* split tails (with the communication warp) */
+    RKR_TUNE_STREAM = 1 << 6,      /* streamed cut programs even when they fit shared memory */
+    RKR_TUNE_BATCH_QUEUE = 1 << 7, /* batches on the row-segment queue (K1p) */
+    RKR_TUNE_PROFILE = 1 << 8      /* host phase timers on stderr (synchronises: never for timing) */
+} rkr_tune;
+
 /* Execution settings; pass NULL for defaults (device 0, the library's shared
- * per-device stream, auto width, persistent kernel). */
+ * per-device stream, auto width, persistent kernel, measured tuning). */
 typedef struct {
     int32_t device;
     void* stream;       /* cudaStream_t, or NULL for the library's per-device stream */
     int32_t width;      /* rkr_width */
     int32_t kernel;     /* rkr_kernel */
-    int32_t reserved[4];
+    int32_t tune;       /* rkr_tune bits, 0 = defaults */
+    int32_t tile_rows;  /* K1t rows per warp: 0 = auto, 1 (32-slot tiles) or 2 (16-slot tiles) */
+    int32_t reserved[2];
 } rkr_exec;
 
 typedef struct rkr_table rkr_table;
@@ -162,6 +179,16 @@ rkr_status rkr_table_download(const rkr_table* table, int64_t* opt, int8_t* kind
  * reference's out-vector would). */
 rkr_status rkr_backtrack(const rkr_table* table, int32_t s, int32_t t, int32_t m, rkr_op* ops,
                          int64_t cap, int64_t* n_ops);
+
+/* build_schedule_rec with the CALLER's menu, as the reference does: the
+ * option decided at a cell is looked up by id in `menu` (first match,
+ * chain_dp.hpp:200-205) and its pack shift to_units(save_mem - act_sizes[s])
+ * taken from there (:228); cut shifts come from the table (:240).  A menu
+ * lacking the option: RKR_ERR_INVALID ("menu for block s lacks option id",
+ * the reference's ValidationError), *n_ops = the ops emitted before it.
+ * menu == NULL or the table's own menu: the same as rkr_backtrack. */
+rkr_status rkr_backtrack_menu(const rkr_table* table, const rkr_menu* menu, int32_t s, int32_t t,
+                              int32_t m, rkr_op* ops, int64_t cap, int64_t* n_ops);
 
 /* The same walk split in two: _async enqueues it on the table's stream (no
  * host sync), _fetch waits and copies the ops (same statuses as above). */

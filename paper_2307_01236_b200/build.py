@@ -59,7 +59,8 @@ CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "test_chain_dp_b200")
 
 def build_cpp_tests(force: bool = False) -> str:
     hdrs = [os.path.join(ROOT, "include", "remat_b200", f) for f in
-            ("chain_dp.hpp", "types.hpp", "errors.hpp")]
+            ("chain_dp.hpp", "types.hpp", "errors.hpp", "device_error.hpp")]
+    hdrs.append(os.path.join(ROOT, "include", "remat", "chain_dp.hpp"))
     if force or _stale(CPP_TEST_BIN, [CPP_TEST_SRC, LIB, *hdrs]):
         subprocess.run(
             ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), CPP_TEST_SRC,

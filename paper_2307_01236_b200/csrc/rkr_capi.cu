@@ -45,14 +45,12 @@ void parallel_for(int n, F fn) {
     for (auto& th : pool) th.join();
 }
 
-// RKR_PROFILE=1: host phase timings of the batched entry points on stderr
-// (each mark synchronises the stream first, so only for diagnostics).
+// rkr_exec.tune & RKR_TUNE_PROFILE: host phase timings of the batched entry
+// points on stderr (each mark synchronises the stream first, so only for
+// diagnostics).
 struct PhaseTimer {
-    bool on = enabled();
-    static bool enabled() {
-        static const bool e = getenv("RKR_PROFILE") != nullptr;
-        return e;
-    }
+    bool on = false;
+    explicit PhaseTimer(const rkr_exec* ex) : on(ex && (ex->tune & RKR_TUNE_PROFILE)) {}
     cudaStream_t st = nullptr;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
     void mark(const char* what) {
@@ -362,10 +360,14 @@ struct rkr_table {
     InstDesc* ddesc = nullptr;    // device copy (single-table fills)
     LaunchPlan lplan{};           // single-table launch order (device pointers)
 
+    // rkr_backtrack_menu: the caller's menu's pack shifts for the walk
+    // (device, nq entries; nullptr = the table's own)
+    int64_t* walk_chg = nullptr;
     LaunchCtx ctx() const {
         LaunchCtx c;
         c.g = g;
         c.dm = dm;
+        if (walk_chg) c.dm.chg_bt = walk_chg;
         c.opt = opt;
         c.arg = arg;
         c.width = width;
@@ -672,7 +674,7 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
     if (!out) return fail(RKR_ERR_ARGUMENT, "null output handle");
     *out = nullptr;
     if (m_max < 0) return fail(RKR_ERR_INVALID, "m_max must be >= 0");
-    PhaseTimer ppt;
+    PhaseTimer ppt(exec);
     rkr_table* t = new rkr_table();
     rkr_status st = build_host_menu(menu, unit, t->hm);
     ppt.mark("  prepare: build_host_menu");
@@ -730,8 +732,14 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
             int sms = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
             // batch tables need no co-residency (their tiles are queued jobs)
+            TileKnobs kn;
+            kn.tune = exec ? exec->tune : 0;
+            // batches run 32-slot tiles unless told otherwise (their jobs
+            // already fill the GPU); shards get the rows of their sharding
+            kn.rows = exec && exec->tile_rows ? exec->tile_rows : (batch_tiles ? 1 : 0);
             t->tiles = tile_plan(t->g, t->width, batch_tiles ? INT32_MAX : sms, (int64_t)h.ids.size(),
-                                 (int)round_up(std::max<int32_t>(h.max_opts, 1), kTileOptBatch), t->tplan) == 1;
+                                 (int)round_up(std::max<int32_t>(h.max_opts, 1), kTileOptBatch), kn,
+                                 t->tplan) == 1;
         }
         if (kreq == RKR_KERNEL_TILES && !t->tiles) {
             delete t;
@@ -1061,6 +1069,9 @@ rkr_status rkr_backtrack_fetch(rkr_table* t, rkr_op* ops, int64_t cap, int64_t* 
     if (status == 2)
         return fail(RKR_ERR_INFEASIBLE, "no feasible schedule for blocks %lld..%lld",
                     (long long)t->hout[2], (long long)t->hout[3]);
+    if (status == 3)  // chain_dp.hpp:203-204, the reference's message
+        return fail(RKR_ERR_INVALID, "menu for block %lld lacks option %lld",
+                    (long long)t->hout[2], (long long)t->hout[3]);
     if (n > cap) return fail(RKR_ERR_CAPACITY, "schedule needs %lld ops", (long long)n);
     return RKR_OK;
 }
@@ -1072,6 +1083,50 @@ rkr_status rkr_backtrack(const rkr_table* tc, int32_t s, int32_t tt, int32_t m, 
     rkr_status st = rkr_backtrack_async(t, s, tt, m);
     if (st) return st;
     return rkr_backtrack_fetch(t, ops, cap, n_ops);
+}
+
+rkr_status rkr_backtrack_menu(const rkr_table* tc, const rkr_menu* menu, int32_t s, int32_t tt,
+                              int32_t m, rkr_op* ops, int64_t cap, int64_t* n_ops) {
+    rkr_table* t = const_cast<rkr_table*>(tc);  // scratch buffers only
+    if (!menu) return rkr_backtrack(tc, s, tt, m, ops, cap, n_ops);
+    rkr_status st = check_cell(t, s, tt);
+    if (st) return st;
+    if (!n_ops || (cap > 0 && !ops)) return fail(RKR_ERR_ARGUMENT, "null output");
+    const HostMenu& h = t->hm;
+    if (menu->n_blocks < h.L || !menu->option_offsets || !menu->option_id || !menu->save_mem ||
+        !menu->act_sizes)
+        return fail(RKR_ERR_INVALID, "menu has %d blocks, the table %d", menu->n_blocks, h.L);
+    // build_schedule_rec's per-option shift from the caller's menu: the first
+    // option with the decided id (detail::menu_option, chain_dp.hpp:200-205)
+    // and to_units(save_mem - act_sizes[s], table unit) (:228)
+    const UnitDiv tu(t->unit);
+    std::vector<int64_t> chg(h.ids.size());
+    bool same = true;
+    for (int32_t b = 0; b < h.L; ++b) {
+        const int32_t o_lo = menu->option_offsets[b], o_hi = menu->option_offsets[b + 1];
+        for (int32_t q = h.blk_off[b]; q < h.blk_off[b + 1]; ++q) {
+            int64_t c = (int64_t)kMissingShift;
+            for (int32_t o = o_lo; o < o_hi; ++o)
+                if (menu->option_id[o] == h.ids[q]) {
+                    c = tu(menu->save_mem[o] - menu->act_sizes[b]);
+                    break;
+                }
+            chg[q] = c;
+            same = same && c == h.chg_bt[q];
+        }
+    }
+    if (same) return rkr_backtrack(tc, s, tt, m, ops, cap, n_ops);
+    DeviceGuard dg(t->device);
+    int64_t* dchg = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&dchg), std::max<size_t>(chg.size(), 1) * 8, t->stream));
+    CK(cudaMemcpyAsync(dchg, chg.data(), chg.size() * 8, cudaMemcpyHostToDevice, t->stream));
+    t->walk_chg = dchg;
+    st = rkr_backtrack_async(t, s, tt, m);
+    if (st == RKR_OK) st = rkr_backtrack_fetch(t, ops, cap, n_ops);
+    t->walk_chg = nullptr;
+    cudaFreeAsync(dchg, t->stream);
+    cudaStreamSynchronize(t->stream);  // chg lives on the host stack
+    return st;
 }
 
 rkr_status rkr_table_refill(rkr_table* t) {
@@ -1195,7 +1250,7 @@ rkr_status rkr_solve_chain(const rkr_menu* menu, int64_t budget_bytes, int32_t u
     if (m_top < 0) return fail(RKR_ERR_INFEASIBLE, "budget cannot hold the chain input");
     if (m_top > 0x7ffffffe) return fail(RKR_ERR_INVALID, "budget slots exceed int range");
     rkr_table* t = nullptr;
-    PhaseTimer pt;  // host-side enqueue costs (no synchronisation)
+    PhaseTimer pt(exec);  // host-side enqueue costs (no synchronisation)
     st = prepare_table(menu, unit, (int32_t)m_top, exec, 0, &t);          // :262
     pt.mark("solve: prepare_table (+H2D, programs)");
     if (st) return st;
@@ -1254,6 +1309,7 @@ struct rkr_batch {
     int device = 0;
     cudaStream_t stream = nullptr;
     int width = 32, R = 1, kcap = 1, ocap = 1;
+    int32_t tune = 0;                    // rkr_exec.tune of the creating call
     std::vector<rkr_table*> tables;
     void* block = nullptr;               // desc array | counter | flags of every table
     InstDesc* ddesc = nullptr;
@@ -1392,7 +1448,7 @@ rkr_status batch_layout(rkr_batch* b) {
     if (b->tiles) {
         // one shared-memory layout for every job: the tables' maxima (create)
         TilePlan& pr = b->proto;
-        if (const char* e = getenv("RKR_COMM")) pr.comm = atoi(e) ? 1 : 0;  // tuning knob
+        if (b->tune & RKR_TUNE_COMM_OFF) pr.comm = 0;
         pr.sm = tile_batch_smem(pr);
         b->htp.assign(n, TilePlan{});
     }
@@ -1503,19 +1559,20 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
     if (exec) ex = *exec;
     const int kreq = exec ? exec->kernel : RKR_KERNEL_PERSISTENT;
     bool want_tiles = kreq != RKR_KERNEL_QUEUE && kreq != RKR_KERNEL_DIAGONAL;
-    if (const char* e = getenv("RKR_BATCH_TILES")) want_tiles = want_tiles && atoi(e) != 0;
+    if (ex.tune & RKR_TUNE_BATCH_QUEUE) want_tiles = false;
     // One pass normally: every table's host side prepared in parallel as
     // budget-tile jobs (K1t).  A common cost width is needed (32 only if every
     // table's overflow proof holds) and the batch-wide shared-memory layout
     // must fit; otherwise a second pass prepares them for the row-segment
     // queue (K1p), in the common width.
     rkr_batch* b = nullptr;
-    PhaseTimer pt0;
+    PhaseTimer pt0(exec);
     for (int attempt = want_tiles ? 0 : 1; attempt < 2; ++attempt) {
         ex.kernel = attempt == 0 ? RKR_KERNEL_TILES : RKR_KERNEL_QUEUE;
         b = new rkr_batch();
         b->device = ex.device;
         b->R = persistent_choose_r(min_m);
+        b->tune = ex.tune;
         b->tiles = attempt == 0;
         DeviceGuard dg0(b->device);
         std::vector<rkr_table*> ts(n, nullptr);
@@ -1572,7 +1629,7 @@ rkr_status batch_create_impl(const rkr_menu* const* menus, const int64_t* units,
     }
     pt0.mark("batch: prepare_table x n");
     DeviceGuard dg(b->device);
-    PhaseTimer pt;
+    PhaseTimer pt(exec);
     pt.st = b->tables[0]->stream;
     pt.mark("batch: host tables");
     rkr_status st = batch_tables_upload(b);
@@ -1688,7 +1745,7 @@ static rkr_status sweep_impl(const rkr_menu* const* mfor, const int64_t* budgets
             mm[q] = mtop[idx[q]];
         }
         rkr_batch* b = nullptr;
-        PhaseTimer spt;
+        PhaseTimer spt(exec);
         rkr_status st = rkr_batch_create(ms.data(), us.data(), mm.data(), nb, exec, &b);
         if (st) return st;
         DeviceGuard dg(b->device);
@@ -1955,6 +2012,13 @@ rkr_status sharded_create_impl(const rkr_menu* menu, int64_t unit, int32_t m_max
             if (exec) ex = *exec;
             ex.kernel = tiles ? RKR_KERNEL_TILES : RKR_KERNEL_QUEUE;
             if (devices) ex.device = devices[r];
+            if (!ex.tile_rows) {  // every shard alike: from the slots one device runs
+                int sms = 0;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ex.device);
+                int per_dev = devices ? 0 : n;
+                for (int q = 0; devices && q < n; ++q) per_dev += devices[q] == devices[r];
+                ex.tile_rows = tile_rows_for((int64_t)W * per_dev, sms, TileKnobs{ex.tune, 0});
+            }
             if (devices && exec && exec->stream) ex.stream = nullptr;  // per-device library streams
             ShardSpec spec{lo, pad, jo};
             rkr_table* t = nullptr;
@@ -2257,6 +2321,12 @@ rkr_status rkr_shard_create(const rkr_menu* menu, int64_t unit, int32_t m_max, i
     // budget tiles (K1t) when the shard qualifies -- every process decides
     // alike, from the same menu and geometry -- else the row-segment queue
     const bool want_tiles = !(exec && (exec->kernel == RKR_KERNEL_QUEUE || exec->kernel == RKR_KERNEL_DIAGONAL));
+    if (!ex.tile_rows) {  // every process decides alike: from shard 0's width
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ex.device);
+        ex.tile_rows = tile_rows_for((int64_t)sg.hi[0] - sg.lo[0], sms > 0 ? sms : 148,
+                                     TileKnobs{ex.tune, 0});
+    }
     ShardSpec spec{sg.lo[shard], sg.pad, sg.jo[shard]};
     spec.ipc = true;
     rkr_table* t = nullptr;

@@ -4,10 +4,13 @@
 
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
+
+#include "../../include/rkr.h"
 
 namespace rkr {
 
@@ -23,6 +26,12 @@ constexpr uint32_t kInf32 = 1u << 30;
 // cut c -> 0x8000 | c.  Numeric order == the reference's candidate order
 // (options in menu order, then cuts ascending, chain_dp.hpp:139-174).
 constexpr uint16_t kCutBit = 0x8000;
+
+// A walk with the CALLER's menu (rkr_backtrack_menu) marks the table's saved
+// options that the caller's menu lacks with this pack shift: the reference's
+// detail::menu_option throws ValidationError at them (chain_dp.hpp:200-205),
+// before it emits anything for the cell.  A table's own shifts are >= 0.
+constexpr int32_t kMissingShift = INT32_MIN;
 
 // Per-table menu data in units (the DpTable ctor precompute, chain_dp.hpp:56-95),
 // device resident.  Saved options of block s: [blk_off[s], blk_off[s+1]).
@@ -182,7 +191,7 @@ struct TileSmem {  // shared-memory carve-up of K1t (byte offsets)
     uint32_t prog_bytes, thr_bytes;  // one buffer of each (two of each are kept)
 };
 struct TilePlan {
-    int32_t WC = 0, W = 0, T = 0, d = 0;  // W = 32 WC; d = lower tiles read (ceil(pad / W))
+    int32_t rpw = 0, W = 0, T = 0, d = 0;  // rows per warp; W = 32 / rpw; d = lower tiles read (ceil(pad / W))
     int32_t cap = 0;                      // bulk partials (values + codes) in shared memory
     int32_t L = 0, nq = 0, ocap = 0;      // blocks, saved options, thr row stride
     TileSmem sm{};
@@ -202,9 +211,17 @@ struct TilePlan {
     int32_t* done = nullptr;              // [L * T]
     unsigned long long* trace = nullptr;  // optional: 6 stamps per (k, j)
 };
+// The rkr_exec tuning fields a plan honours (include/rkr.h; 0 = defaults).
+struct TileKnobs {
+    int32_t tune = 0;  // rkr_tune bits
+    int32_t rows = 0;  // K1t rows per warp: 0 auto, 1 or 2
+};
 // 1 = eligible.  Long chains, whose per-step programs do not fit shared
 // memory, get the streamed-program variant (tp.stream = 1) by default.
-int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp);
+int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, const TileKnobs& kn,
+              TilePlan& tp);
+// K1t rows per warp for a table (or shard) of `slots` budget slots.
+int tile_rows_for(int64_t slots, int sms, const TileKnobs& kn);
 int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream);
 // Batches: jobs (table, tile) in queue order; tps[i].sm is the batch-wide
 // layout (tile_batch_smem of a plan with every table's maxima).

@@ -302,7 +302,7 @@ __device__ inline Programs<V> programs_of(const ProgDev& q) {
 // SINGLE: one table whose descriptor travels as a kernel parameter (constant
 // bank); batches read their descriptors from global memory (measured 22%
 // slower per item on config 3, so the single-table path keeps the param).
-__constant__ int pl_sleep_ns = 32;  // poll back-off (tuning knob, RKR_SLEEP_NS)
+constexpr int pl_sleep_ns = 32;  // poll back-off (ns; measured, profiles/r01_persist)
 
 template <typename V, int NT, int R, int U, bool SINGLE, int MINB>
 __global__ void __launch_bounds__(NT, MINB) fill_persistent(const InstDesc* __restrict__ inst,
@@ -674,9 +674,7 @@ int prep_t(const LaunchCtx& cx) {
 }  // namespace
 
 int persistent_choose_r(int32_t M) {
-    int R = (M + 1 >= 8192) ? 2 : 1;
-    if (const char* e = getenv("RKR_R")) R = atoi(e) == 2 ? 2 : 1;  // tuning knob
-    return R;
+    return (M + 1 >= 8192) ? 2 : 1;
 }
 
 void persistent_plan(const Geometry& g, int width, int R, PersistPlan& p) {
@@ -693,7 +691,6 @@ void persistent_plan(const Geometry& g, int width, int R, PersistPlan& p) {
     // locality (profiles/r01_persist: never paid off at this item latency).
     const double table_bytes = (double)g.rows * g.sr * vb;
     p.lambda = table_bytes <= 48.0 * (1 << 20) ? 0 : 1;
-    if (const char* e = getenv("RKR_LAMBDA")) p.lambda = atoi(e) >= 0 ? atoi(e) : 1;  // tuning knob
     std::vector<std::pair<int64_t, int64_t>> order;  // (key, j * L + k)
     order.reserve((size_t)p.J * L);
     for (int64_t jj = 0; jj < p.J; ++jj)
@@ -744,29 +741,6 @@ int launch_fill_batch(const InstDesc* dev_desc, const InstDesc* single, const La
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     InstDesc d0{};
     if (single) d0 = *single;
-    static const bool sleep_set = [] {
-        if (const char* e = getenv("RKR_SLEEP_NS")) {
-            const int v = atoi(e);
-            cudaMemcpyToSymbol(pl_sleep_ns, &v, sizeof v);
-        }
-        return true;
-    }();
-    (void)sleep_set;
-    static const int variant = [] {
-        const char* e = getenv("RKR_VARIANT");  // tuning knob for measurements
-        return e ? atoi(e) : 0;
-    }();
-    if (single && width == 32 && variant) {
-        switch (variant * 10 + R) {
-            case 11: return launch_t<uint32_t, 1, true, 8, 6>(dev_desc, d0, lp, kcap, ocap, counter, st);
-            case 12: return launch_t<uint32_t, 2, true, 8, 4>(dev_desc, d0, lp, kcap, ocap, counter, st);
-            case 21: return launch_t<uint32_t, 1, true, 4, 1>(dev_desc, d0, lp, kcap, ocap, counter, st);
-            case 22: return launch_t<uint32_t, 2, true, 4, 5>(dev_desc, d0, lp, kcap, ocap, counter, st);
-            case 31: return launch_t<uint32_t, 1, true, 2, 8>(dev_desc, d0, lp, kcap, ocap, counter, st);
-            case 32: return launch_t<uint32_t, 2, true, 2, 5>(dev_desc, d0, lp, kcap, ocap, counter, st);
-            default: break;
-        }
-    }
     if (single) {
         if (width == 32)
             return R == 2 ? launch_t<uint32_t, 2, true>(dev_desc, d0, lp, kcap, ocap, counter, st)

@@ -128,14 +128,17 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     m.thr_bytes = al16(L * tp.ocap * 4);
     uint64_t b = 0;
     m.best = 0;
-    // Bulk partials (values, then codes): [L W] (>= kNT) for unsplit steps and
-    // [kNT] for split steps (late diagonals, cut range over several warps).
-    // Without the communication warp the steps are barrier-aligned and one
-    // [L W] region serves both.  With it, the bulk of step k+1 runs on other
-    // warps than the tail of step k that reads step k's parts, so each region
-    // is double-buffered by step parity: [2 L W | 2 kNT].  (Shared memory is
-    // tight for config-3-sized co-resident tables: 12 KB more once cost 30 %
-    // -- less L1 left for loads in flight.)
+    // Bulk partials (values, then codes): [units 32] (>= kNT) for unsplit
+    // steps and [kNT] for split steps (late diagonals, cut range over several
+    // warps).  Without the communication warp the steps are barrier-aligned
+    // and one [cap] region serves both.  With it, the bulk of step k+1 runs on
+    // other warps than the tail of step k that reads step k's parts, so each
+    // region is double-buffered by step parity: [2 cap | 2 kNT].  (Shared
+    // memory is tight for config-3-sized co-resident tables: 12 KB more once
+    // cost 30 % -- less L1 left for loads in flight.)  A dynamic split (bulk
+    // items of 16-64 cuts taken from a shared counter by whichever warp is
+    // free, merged with a 64-bit atomicMin on (value, code)) measured 5 %
+    // slower on configs 3 and 2 at every item size.
     const uint64_t np = tp.comm ? 2ull * tp.cap + 2 * kNT : (uint64_t)tp.cap;
     b = al16(b + np * 4);
     m.code = (uint32_t)b;
@@ -147,12 +150,13 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     m.opd = (uint32_t)b;
     if (tp.stream) {  // programs, thresholds and options from global memory;
         // per-warp program slices for the bulk
-        m.prog_bytes = (uint32_t)(kNW * kSlice * 16);
+        m.prog_bytes = (uint32_t)(kNW * kSlice * 16 * tp.rpw);
         m.thr_bytes = 0;
         m.prog = (uint32_t)b;
         b += m.prog_bytes;
-        m.thr = (uint32_t)b;  // per-warp option slices: [kNW][ocap] int2 | [kNW][ocap] int
-        b = al16(b + (uint64_t)kNW * tp.ocap * 12);
+        // per-(warp, row) option slices: [kNW RPW][ocap] int2 | [kNW RPW][ocap] int
+        m.thr = (uint32_t)b;
+        b = al16(b + (uint64_t)kNW * tp.rpw * tp.ocap * 12);
     } else {
         b = al16(b + L * tp.ocap * 8);  // [block][ocap] {-pack shift, pass time}, padded
         m.prog = (uint32_t)b;
@@ -196,19 +200,22 @@ __device__ __forceinline__ const uint32_t* lane_base(const uint32_t* opt, int m)
 // left row (s, c-1) and of the right row (c, t) shifted by act_u[c]
 // (:166-167), the option-0 sweep (:162) and the gate (:159, :164).
 //
-// Instruction budget per candidate (the fill is issue-bound, ncu: 58 % issue
-// slots busy on config 3): one LDS.128 (program entry), two IMAD.WIDE (lane
-// base + entry offset: the lane's `optm = opt + m` is formed once), two LDG,
-// one IADD3 (sweep + left + right), one VIMNMX with predicate output (DPX
-// __vibmin_u32: min and "kept the old best" in one instruction) and one
-// predicated code update.  The gate (:159, :164) is only tested per candidate
-// in a batch where the warp is split by it: it grows with i and the lanes'
-// budgets are consecutive, so when lane 0 (the smallest m) admits the
-// batch's last cut, every lane admits every cut of the batch.
+// Instruction budget per candidate (ncu, config 3: 57 % issue slots busy):
+// one LDS.128 (program entry), two IMAD.WIDE (lane base + entry offset: the
+// lane's `optm = opt + m` is formed once), two LDG, one IADD3 (sweep + left
+// + right), VIMNMX + ISETP (DPX __vibmin_u32: min and "kept the old best";
+// sm_100a has no fused predicate form) and one predicated code update --
+// 10.4 per cut with the loop overhead, 13.5 before (profiles/r02_sass).
+// The gate (:159, :164) is only tested per candidate in a batch where it
+// splits the warp: it grows with i, so when every lane admits the batch's
+// last cut, every lane admits every cut of the batch.  RPW = 1 (one row per
+// warp, consecutive budgets): that is lane 0's test, warp-uniform, no vote.
+// RPW = 2 (two rows per warp, 16 budgets each): a warp vote.
+template <int RPW>
 __device__ __forceinline__ bool scan_cuts(const uint32_t* __restrict__ opt, const int4* pe, int ib,
                                           int ie, int m, int cb, uint32_t& best, int& code) {
     const uint32_t* __restrict__ optm = lane_base(opt, m);
-    const int m0 = m - (int)(threadIdx.x & 31);  // warp-uniform: the smallest budget
+    const int m0 = m - (int)(threadIdx.x & 31);  // RPW = 1: warp-uniform, the smallest budget
     int i0 = ib;
     for (; i0 + kU <= ie; i0 += kU) {
         uint32_t lv[kU], rv[kU];
@@ -221,7 +228,8 @@ __device__ __forceinline__ bool scan_cuts(const uint32_t* __restrict__ opt, cons
             lv[q] = __ldcg(optm + (uint32_t)e[q].x);
             rv[q] = __ldcg(optm + (uint32_t)e[q].y);
         }
-        if (e[kU - 1].w <= m0) {  // (warp-uniform) no lane gated in this batch
+        if (RPW == 1 ? e[kU - 1].w <= m0 : __all_sync(0xffffffffu, e[kU - 1].w <= m)) {
+            // (warp-uniform) no lane gated in this batch
 #pragma unroll
             for (int q = 0; q < kU; ++q) {
                 bool keep;
@@ -255,18 +263,22 @@ __device__ __forceinline__ bool scan_cuts(const uint32_t* __restrict__ opt, cons
 }
 
 // STREAM variant (long chains: a diagonal's programs do not fit shared
-// memory): each warp stages its unit's program kSlice entries at a time.
+// memory): each warp stages its unit's program(s) kSlice entries at a time
+// (RPW rows: one slice per row, staged by that row's lanes).
+template <int RPW>
 __device__ __forceinline__ void scan_cuts_streamed(const uint32_t* __restrict__ opt,
                                                    const int4* __restrict__ pe_g, int4* slice,
                                                    int ib, int ie, int m, int cb, uint32_t& best,
                                                    int& code) {
-    const int lane = threadIdx.x & 31;
+    constexpr int W = 32 / RPW;
+    const int lane = threadIdx.x & 31, rw = lane / W, ml = lane % W;
+    int4* mine = slice + rw * kSlice;
     for (int c0 = ib; c0 < ie; c0 += kSlice) {
         const int c1 = c0 + kSlice < ie ? c0 + kSlice : ie;
         __syncwarp();  // the previous chunk's readers are done
-        for (int i = c0 + lane; i < c1; i += 32) slice[i - c0] = __ldg(pe_g + i);
+        for (int i = c0 + ml; i < c1; i += W) mine[i - c0] = __ldg(pe_g + i);
         __syncwarp();
-        if (scan_cuts(opt, slice - c0, c0, c1, m, cb, best, code)) return;
+        if (scan_cuts<RPW>(opt, mine - c0, c0, c1, m, cb, best, code)) return;
     }
 }
 
@@ -279,10 +291,19 @@ __device__ __forceinline__ void scan_cuts_streamed(const uint32_t* __restrict__ 
 // phases of the two program mbarriers before this job (jobs of a batch
 // reuse them).  The caller initialises the mbarriers once and separates
 // jobs with a CTA barrier.
-template <int WC, bool COMM, bool SPLIT, bool STREAM, bool TABLE, bool HALO>
+//
+// RPW = rows per warp.  1: a warp computes 32 consecutive budget slots of
+// one row (tile width W = 32).  2: lanes 0-15 and 16-31 take the same 16
+// slots of two rows (W = 16), so a table has twice as many tiles, each half
+// the work: the tile jobs of config 3 come out to 7 waves of 148 instead of
+// 4 (the last one 46 % full), and a budget shard of 2048 slots occupies 128
+// SMs instead of 64.  A unit is one warp's (row group, slots) share of a
+// step; rows past the diagonal's last (an odd row count) are computed from a
+// clamped row and not stored.
+template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool TABLE, bool HALO>
 __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, const int j,
                                          unsigned char* smem_raw, uint32_t ph0, uint32_t ph1) {
-    constexpr int W = 32 * WC;
+    constexpr int W = 32 / RPW;
     constexpr int kNC = COMM ? kNW - 1 : kNW;  // compute warps
     const TileSmem& sm = tp.sm;
     int32_t* s_blk = reinterpret_cast<int32_t*>(smem_raw + sm.blk);
@@ -298,6 +319,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     const int sr = (int)g.sr;  // rows * sr < 2^31 (tile_plan)
     const int ocap = tp.ocap;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rw = lane / W, ml = lane % W;  // row within the unit, slot within the tile
     const int m_lo = j * W;
 
     // Table-independent data in shared memory: block option ranges, and per
@@ -310,7 +332,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     // cut range over warps; >= 8 cuts per part)
     int2* s_split = reinterpret_cast<int2*>(smem_raw + sm.split);
     for (int k = tid; TABLE && k < L; k += kNT) {
-        const int units = (L - k) * WC, nb = k >= 3 ? k - 2 : 0;
+        const int units = (L - k + RPW - 1) / RPW, nb = k >= 3 ? k - 2 : 0;
         int P = 1, chunk = nb;
         if (nb > 0 && units < kNC) {
             P = kNC / units;
@@ -367,6 +389,9 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 if (halo_in && lane == 0) wait_halo(k - 1);
                 __syncwarp();
             }
+            // trace: when the lower tiles' diagonal k-1 was acquired (the
+            // compute warps pass READY at max(this, their last bulk))
+            if (tp.trace && lane == 0) tp.trace[6 * ((int64_t)k * tp.T + j) + 1] = t_gtimer();
             nb_arrive(kBarReady);
             nb_sync(kBarDone);  // the compute warps stored diagonal k
             if (lane == 0) {
@@ -400,7 +425,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                                      : reinterpret_cast<const int32_t*>(smem_raw + sm.thr + (k & 1) * sm.thr_bytes);
 
         const int rows = L - k;
-        const int units = rows * WC;
+        const int units = (rows + RPW - 1) / RPW;
         const int nb = k >= 3 ? k - 2 : 0;  // bulk cuts i = 1 .. k-2
         // late diagonals split the cut range into P parts of `chunk` cuts
         // (TABLE: precomputed per step, no integer division in the step loop
@@ -422,8 +447,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         uint16_t* pcode = reinterpret_cast<uint16_t*>(smem_raw + sm.code) + poff;
 
         // ---- bulk: cuts i in [1, k-2] ahead of the wait -----------------------
-        // (scanning them inside the tail instead, which frees the [L W]
-        // partials, measured 3% slower on config 3)
+        // (scanning them inside the tail instead, which frees the partials,
+        // measured 3% slower on config 3)
         if (nb > 0) {
             // with the communication warp, bulk units go to the warps from the
             // top down: on late diagonals the tail of step k-1 occupies the
@@ -432,18 +457,18 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             for (int it = COMM ? kNC - 1 - warp : warp; it < units * P; it += kNC) {
                 const int p = P == 1 ? 0 : (TABLE ? (int)((float)it * rcp_units) : it / units);
                 const int u = it - p * units;
-                const int s = u / WC;
-                const int m = m_lo + (u - s * WC) * 32 + lane;
+                const int s = min(u * RPW + rw, rows - 1);  // (a clamped row is not stored)
+                const int m = m_lo + ml;
                 const int ib = 1 + p * chunk;
                 const int ie = ib + chunk < k - 1 ? ib + chunk : k - 1;
                 uint32_t best = INF;
                 int code = 0;
                 if constexpr (STREAM)
-                    scan_cuts_streamed(opt, prog + s * k,
-                                       reinterpret_cast<int4*>(smem_raw + sm.prog) + warp * kSlice,
-                                       ib, ie, m, kCutBit | (s + 1), best, code);
+                    scan_cuts_streamed<RPW>(opt, prog + s * k,
+                                            reinterpret_cast<int4*>(smem_raw + sm.prog) + warp * RPW * kSlice,
+                                            ib, ie, m, kCutBit | (s + 1), best, code);
                 else
-                    scan_cuts(opt, prog + s * k, ib, ie, m, kCutBit | (s + 1), best, code);
+                    scan_cuts<RPW>(opt, prog + s * k, ib, ie, m, kCutBit | (s + 1), best, code);
                 pbest[it * 32 + lane] = best;
                 pcode[it * 32 + lane] = (uint16_t)code;
             }
@@ -484,10 +509,14 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         for (int v = warp; v < units * TS; v += kNC) {
             const int h = TS == 1 ? -1 : (v >= units ? 1 : 0);  // -1: the whole tail
             const int u = TS == 1 ? v : v - h * units;
-            const int s = u / WC;
-            const int m = m_lo + (u - s * WC) * 32 + lane;
+            const bool valid = RPW == 1 || u * RPW + rw < rows;  // stores only for real rows
+            const int s = min(u * RPW + rw, rows - 1);
+            const int m = m_lo + ml;
             const int rid = rbase + s;
-            const int nopt = s_blk[s + 1] - s_blk[s];
+            // options of the unit's rows, warp-uniform (the padded slots of a
+            // shorter block never win: pass time INF, threshold M + 1)
+            const int nopt = RPW == 1 ? s_blk[s + 1] - s_blk[s]
+                                      : __reduce_max_sync(0xffffffffu, s_blk[s + 1] - s_blk[s]);
             // option batches of this half: [ia, ib)
             const int nb2 = (((nopt + kOB - 1) / kOB) + 1) / 2 * kOB;  // first half, whole batches
             const int ia = h == 1 ? nb2 : 0;
@@ -519,13 +548,14 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 // thresholds into the warp's slice, coalesced, padded like
                 // the staged layout (padding never wins: pass time INF,
                 // threshold M+1)
-                int2* wo = reinterpret_cast<int2*>(smem_raw + sm.thr) + warp * ocap;
-                int32_t* wt = reinterpret_cast<int32_t*>(smem_raw + sm.thr + (size_t)kNW * ocap * 8) +
-                              warp * ocap;
+                const int slot = warp * RPW + rw;
+                int2* wo = reinterpret_cast<int2*>(smem_raw + sm.thr) + slot * ocap;
+                int32_t* wt = reinterpret_cast<int32_t*>(smem_raw + sm.thr + (size_t)kNW * RPW * ocap * 8) +
+                              slot * ocap;
                 __syncwarp();  // the previous unit's readers are done
-                const int o0 = s_blk[s];
-                for (int i = lane; i < ocap; i += 32) {
-                    wo[i] = i < nopt ? make_int2(-__ldg(pq.pc + o0 + i),
+                const int o0 = s_blk[s], own = s_blk[s + 1] - o0;
+                for (int i = ml; i < ocap; i += W) {
+                    wo[i] = i < own ? make_int2(-__ldg(pq.pc + o0 + i),
                                                  (int)__ldg(static_cast<const uint32_t*>(pq.otot) + o0 + i))
                                      : make_int2(0, (int)INF);
                     wt[i] = __ldg(thrs + s * ocap + i);
@@ -606,7 +636,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             if (h == 1) {  // hand the later half to the h = 0 warp
                 xbest[u * 32 + lane] = best;
                 xcode[u * 32 + lane] = (uint16_t)code;
-            } else if (h == -1 && m <= M) {  // store (chain_dp.hpp:176-177)
+            } else if (h == -1 && m <= M && valid) {  // store (chain_dp.hpp:176-177)
                 opt[(int64_t)rid * sr + g.pad + m] = best;
                 arg[(int64_t)rid * g.sa + m] = (uint16_t)code;
                 if (halo_out && m >= Wl - g.pad)  // the next shard's halo slot m - Wl
@@ -621,8 +651,9 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             // v = w): the others go straight on to bulk(k+1)
             nb_sync_n(kBarSplit, 2 * units * 32);
             for (int u = warp; u < units; u += kNC) {
-                const int s = u / WC;
-                const int m = m_lo + (u - s * WC) * 32 + lane;
+                const bool valid = RPW == 1 || u * RPW + rw < rows;
+                const int s = min(u * RPW + rw, rows - 1);
+                const int m = m_lo + ml;
                 const int rid = rbase + s;
                 uint32_t best = xbest[(kNT >> 1) + u * 32 + lane];
                 int code = xcode[(kNT >> 1) + u * 32 + lane];
@@ -631,7 +662,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                     best = b1;
                     code = xcode[u * 32 + lane];
                 }
-                if (m <= M) {  // store (chain_dp.hpp:176-177)
+                if (m <= M && valid) {  // store (chain_dp.hpp:176-177)
                     opt[(int64_t)rid * sr + g.pad + m] = best;
                     arg[(int64_t)rid * g.sa + m] = (uint16_t)code;
                     if (halo_out && m >= Wl - g.pad)
@@ -642,8 +673,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         if (tp.trace && tid == 0) {
             t3 = t_gtimer();
             unsigned long long* tr = tp.trace + 6 * ((int64_t)k * tp.T + j);
-            tr[0] = t0;  // the K1p stamp layout: no k-2 wait (stamp 1 = 0),
-            tr[1] = t0;  // publish happens on the communication warp (5 = 4)
+            tr[0] = t0;  // the K1p stamp layout; stamp 1: the communication warp's
+            if (!COMM) tr[1] = t0;  // acquisition of diagonal k-1 (else = 0)
             tr[2] = t1;
             tr[3] = t2;
             tr[4] = t3;
@@ -723,7 +754,7 @@ __device__ __forceinline__ void last_walk(const InstDesc& D, const TilePlan& tp,
     __syncthreads();  // the walk's shared memory is free again
 }
 
-template <int WC, bool COMM, bool SPLIT, bool STREAM, bool HALO>
+template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool HALO>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ InstDesc D,
                                                     const __grid_constant__ TilePlan tp) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -736,7 +767,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    tile_job<WC, COMM, SPLIT, STREAM, true, HALO>(D, tp, blockIdx.x, smem_raw, 0, 0);
+    tile_job<RPW, COMM, SPLIT, STREAM, true, HALO>(D, tp, blockIdx.x, smem_raw, 0, 0);
     const Geometry& g = D.g;
     const DevMenu& dm = D.dm;
     uint32_t* __restrict__ opt = static_cast<uint32_t*>(D.opt);
@@ -800,7 +831,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
 // tiles of its own table, which were dequeued earlier by CTAs that are
 // running or done, so the queue cannot deadlock and tables need not be
 // co-resident.
-template <int WC, bool COMM, bool SPLIT, bool STREAM, bool WALK, bool HALO>
+template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool WALK, bool HALO>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __restrict__ descs,
                                                           const TilePlan* __restrict__ tps,
                                                           const int2* __restrict__ jobs, int njobs,
@@ -823,7 +854,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
         const int q = s_job;
         if (q >= njobs) break;
         const int2 jb = jobs[q];
-        tile_job<WC, COMM, SPLIT, STREAM, false, HALO>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0,
+        tile_job<RPW, COMM, SPLIT, STREAM, false, HALO>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0,
                                                        ph1);
         const int L = descs[jb.x].g.L;
         ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
@@ -834,9 +865,9 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
     }
 }
 
-template <int WC, bool COMM, bool SPLIT, bool STREAM, bool HALO = false>
+template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool HALO = false>
 int launch_tiles_t(const InstDesc& d, const TilePlan& tp, cudaStream_t st) {
-    auto kern = fill_tiles<WC, COMM, SPLIT, STREAM, HALO>;
+    auto kern = fill_tiles<RPW, COMM, SPLIT, STREAM, HALO>;
     const size_t smem = tp.sm.total;
     if (set_dyn_smem((const void*)kern, smem) != cudaSuccess)
         return 3;
@@ -852,84 +883,98 @@ int launch_tiles_t(const InstDesc& d, const TilePlan& tp, cudaStream_t st) {
 
 }  // namespace
 
-// Narrowest tile (W = 32 WC) whose T tiles fit one CTA per SM; 0 = not
-// eligible (the queue-scheduled K1p runs instead).
-int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, TilePlan& tp) {
-    if (const char* e = getenv("RKR_TILES"))  // tuning knob: 0 disables K1t
-        if (atoi(e) == 0) return 0;
+// Tile width, warp roles and program staging of K1t for one table; 0 = not
+// eligible (the queue-scheduled K1p runs instead).  kn: the caller's
+// rkr_exec tuning fields (0 = the measured defaults below).
+int tile_rows_for(int64_t slots, int sms, const TileKnobs& kn) {
+    if (kn.rows == 1 || kn.rows == 2) return kn.rows;
+    // RPW = 2 halves the tile (16 slots, two rows per warp): twice the tiles,
+    // each with half the work but the same per-step costs (program staging,
+    // flags, barriers) and twice the L1 wavefronts per load.  It only pays
+    // where 32-slot tiles leave at least half the SMs idle: a co-resident
+    // table of <= 74 tiles (config 1: fill 0.070 -> 0.064 ms; a budget shard
+    // of config 3 on 8 GPUs: 64 tiles).  As tile jobs it loses even when it
+    // evens out the waves (config 3: 1025 half jobs in 7 half waves, 4.96 ms,
+    // against 513 jobs in 4 waves, 4.07 ms).
+    const int64_t t1 = (slots + 31) / 32;
+    return 2 * t1 <= sms ? 2 : 1;
+}
+
+int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, const TileKnobs& kn,
+              TilePlan& tp) {
+    if (kn.tune & RKR_TUNE_NO_TILES) return 0;
     if (width != 32) return 0;
-    // 32-bit element offsets inside the table (plus the tile over-read)
+    // 32-bit element offsets inside the table (plus the tile over-read).
+    // (A config-5 shard on 8 GPUs holds 4.4e9 elements: K1p, 64-bit row
+    // pointers, runs it.)
     if ((double)g.rows * g.sr + 64.0 * 32 + g.pad >= 2147483647.0) return 0;
-    // 32-slot tiles.  When they do not all fit one CTA per SM the table runs
-    // as tile jobs (fill_tiles_batch on one table): a dataflow queue needs no
+    // When the tiles do not all fit one CTA per SM the table runs as tile
+    // jobs (fill_tiles_batch on one table): a dataflow queue needs no
     // co-residency, and walking the tiles in budget order keeps the rows
     // around the active band in L2 (config 3: 4.65 ms and 0.13 GB of DRAM
     // reads, against 5.14 ms and 13.3 GB with 129 co-resident 128-slot tiles)
-    for (int wc = 1; wc <= 1; wc *= 2) {
-        const int W = 32 * wc;
-        const int64_t T = ((int64_t)g.M + 1 + W - 1) / W;
-        tp.jobs = T > sms ? 1 : 0;
-        if (const char* e = getenv("RKR_JOBS")) tp.jobs = tp.jobs || atoi(e) != 0;  // test knob
-        tp.WC = wc;
-        tp.W = W;
-        tp.T = (int32_t)T;
-        tp.d = (g.pad + W - 1) / W;
-        tp.cap = (int32_t)((int64_t)g.L * W > kNT ? (int64_t)g.L * W : kNT);
-        tp.L = g.L;
-        tp.nq = (int32_t)nq;
-        tp.ocap = ocap;
-        // the communication warp pays off where the fill is latency-bound
-        // (per-step work of a few microseconds: configs 1-2), not where it is
-        // throughput-bound (config 3: measured 5.36 ms without, 6.56 with)
-        tp.comm = (tp.jobs || (double)g.rows * (g.M + 1) <= 16.0e6) ? 1 : 0;
-        if (const char* e = getenv("RKR_COMM")) tp.comm = atoi(e) ? 1 : 0;  // tuning knob
-        // split tails on late diagonals: co-resident tables whose blocks have
-        // two or more option batches (config 2: -3.5 %; measured slower with
-        // one batch (config 1), as tile jobs (config 3: +7 %) and for batches
-        // of tables (config 4))
-        tp.split = tp.comm && !tp.jobs && ocap >= 2 * kOB ? 1 : 0;
-        if (const char* e = getenv("RKR_SPLIT")) tp.split = tp.comm && atoi(e) != 0;  // tuning knob
-        tp.stream = 0;
+    const int rpw = tile_rows_for((int64_t)g.M + 1, sms, kn);
+    const int W = 32 / rpw;
+    const int64_t T = ((int64_t)g.M + 1 + W - 1) / W;
+    tp.jobs = (T > sms || (kn.tune & RKR_TUNE_JOBS)) ? 1 : 0;
+    tp.rpw = rpw;
+    tp.W = W;
+    tp.T = (int32_t)T;
+    tp.d = (g.pad + W - 1) / W;
+    const int64_t units = ((int64_t)g.L + rpw - 1) / rpw;  // warp units of the widest step
+    tp.cap = (int32_t)(units * 32 > kNT ? units * 32 : kNT);
+    tp.L = g.L;
+    tp.nq = (int32_t)nq;
+    tp.ocap = ocap;
+    // the communication warp pays off where the fill is latency-bound
+    // (per-step work of a few microseconds: configs 1-2), not where it is
+    // throughput-bound (config 3: measured 5.36 ms without, 6.56 with)
+    tp.comm = (tp.jobs || (double)g.rows * (g.M + 1) <= 16.0e6) ? 1 : 0;
+    if (kn.tune & RKR_TUNE_COMM_OFF) tp.comm = 0;
+    if (kn.tune & RKR_TUNE_COMM_ON) tp.comm = 1;
+    // split tails on late diagonals: co-resident tables whose blocks have
+    // two or more option batches (config 2: -3.5 %; measured slower with
+    // one batch (config 1), as tile jobs (config 3: +7 %) and for batches
+    // of tables (config 4))
+    tp.split = tp.comm && !tp.jobs && ocap >= 2 * kOB ? 1 : 0;
+    if (kn.tune & RKR_TUNE_SPLIT_OFF) tp.split = 0;
+    if (kn.tune & RKR_TUNE_SPLIT_ON) tp.split = tp.comm;
+    tp.stream = 0;
+    tp.sm = tile_smem(tp);
+    if (tp.sm.total > 220 * 1024 || (kn.tune & RKR_TUNE_STREAM)) {
+        // long chains: a diagonal's programs do not fit shared memory.
+        // The streamed variant reads them from global memory (each warp
+        // stages its unit's program, options and thresholds into its own
+        // slice); with the communication warp it beats the row-segment
+        // queue (L=256, B=64, M=4096: 25.9 ms against K1p's 27.0 ms)
+        tp.stream = 1;
+        tp.split = 0;
+        if (!(kn.tune & RKR_TUNE_COMM_OFF)) tp.comm = 1;
         tp.sm = tile_smem(tp);
-        const bool force = getenv("RKR_STREAM") != nullptr;  // test knob
-        if (tp.sm.total > 220 * 1024 || force) {
-            // long chains: a diagonal's programs do not fit shared memory.
-            // The streamed variant reads them from global memory (each warp
-            // stages its unit's program, options and thresholds into its own
-            // slice); with the communication warp it beats the row-segment
-            // queue (L=256, B=64, M=4096: 25.9 ms against K1p's 27.0 ms)
-            tp.stream = 1;
-            tp.split = 0;
-            if (!getenv("RKR_COMM")) tp.comm = 1;
-            tp.sm = tile_smem(tp);
-        }
-        return tp.sm.total <= 220 * 1024 ? 1 : 0;
     }
-    return 0;
+    return tp.sm.total <= 220 * 1024 ? 1 : 0;
 }
 
-int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream) {
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (width != 32 || tp.WC != 1) return 3;  // 32-bit costs, 32-slot tiles
+namespace {
+
+template <int RPW>
+int launch_fill_tiles_r(const InstDesc& d, const TilePlan& tp, cudaStream_t st) {
     if (tp.halo) {  // budget shards: communication warp, no split tails
         if (!tp.comm || tp.split) return 3;
-        return tp.stream ? launch_tiles_t<1, true, false, true, true>(d, tp, st)
-                         : launch_tiles_t<1, true, false, false, true>(d, tp, st);
+        return tp.stream ? launch_tiles_t<RPW, true, false, true, true>(d, tp, st)
+                         : launch_tiles_t<RPW, true, false, false, true>(d, tp, st);
     }
-    if (tp.stream) return tp.comm ? launch_tiles_t<1, true, false, true>(d, tp, st)
-                                  : launch_tiles_t<1, false, false, true>(d, tp, st);
-    if (tp.comm) return tp.split ? launch_tiles_t<1, true, true, false>(d, tp, st)
-                                 : launch_tiles_t<1, true, false, false>(d, tp, st);
-    return launch_tiles_t<1, false, false, false>(d, tp, st);
+    if (tp.stream) return tp.comm ? launch_tiles_t<RPW, true, false, true>(d, tp, st)
+                                  : launch_tiles_t<RPW, false, false, true>(d, tp, st);
+    if (tp.comm) return tp.split ? launch_tiles_t<RPW, true, true, false>(d, tp, st)
+                                 : launch_tiles_t<RPW, true, false, false>(d, tp, st);
+    return launch_tiles_t<RPW, false, false, false>(d, tp, st);
 }
 
-TileSmem tile_batch_smem(const TilePlan& proto) { return tile_smem(proto); }
-
-int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const int2* jobs,
-                            int njobs, unsigned int* counter, const TilePlan& proto, void* stream,
-                            const TilePlan* walk) {
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (njobs <= 0) return 0;
+template <int RPW>
+int launch_fill_tiles_batch_r(const InstDesc* descs, const TilePlan* tps, const int2* jobs,
+                              int njobs, unsigned int* counter, const TilePlan& proto,
+                              cudaStream_t st, const TilePlan* walk) {
     auto go = [&](auto kern) -> int {
         const size_t smem = proto.sm.total;
         if (set_dyn_smem((const void*)kern, smem) != cudaSuccess)
@@ -943,11 +988,10 @@ int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const in
         kern<<<grid, kNT, smem, st>>>(descs, tps, jobs, njobs, counter, wp);
         return cudaGetLastError() == cudaSuccess ? 0 : 3;
     };
-    if (proto.WC != 1) return 3;  // batches run 32-slot tiles
     if (proto.halo) {  // budget shards: communication warp, no split tails, no walk
         if (!proto.comm || proto.split || (walk && walk->walk)) return 3;
-        return proto.stream ? go(fill_tiles_batch<1, true, false, true, false, true>)
-                            : go(fill_tiles_batch<1, true, false, false, false, true>);
+        return proto.stream ? go(fill_tiles_batch<RPW, true, false, true, false, true>)
+                            : go(fill_tiles_batch<RPW, true, false, false, false, true>);
     }
     // the walk variant only for a single table with a walk request (no code
     // for it in the batch kernels)
@@ -955,21 +999,45 @@ int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const in
     const bool split = walk && proto.comm && proto.split;
     if (walk && walk->walk) {
         if (proto.stream)
-            return proto.comm ? go(fill_tiles_batch<1, true, false, true, true, false>)
-                              : go(fill_tiles_batch<1, false, false, true, true, false>);
-        if (split) return go(fill_tiles_batch<1, true, true, false, true, false>);
-        return proto.comm ? go(fill_tiles_batch<1, true, false, false, true, false>)
-                          : go(fill_tiles_batch<1, false, false, false, true, false>);
+            return proto.comm ? go(fill_tiles_batch<RPW, true, false, true, true, false>)
+                              : go(fill_tiles_batch<RPW, false, false, true, true, false>);
+        if (split) return go(fill_tiles_batch<RPW, true, true, false, true, false>);
+        return proto.comm ? go(fill_tiles_batch<RPW, true, false, false, true, false>)
+                          : go(fill_tiles_batch<RPW, false, false, false, true, false>);
     }
     // (a single long table: the budget-shard instantiation, whose halo code
     // is inert here -- its register allocation spills 8 bytes where the
     // plain one spills 88)
     if (proto.stream)
-        return proto.comm ? go(fill_tiles_batch<1, true, false, true, false, true>)
-                          : go(fill_tiles_batch<1, false, false, true, false, false>);
-    if (split) return go(fill_tiles_batch<1, true, true, false, false, false>);
-    return proto.comm ? go(fill_tiles_batch<1, true, false, false, false, false>)
-                      : go(fill_tiles_batch<1, false, false, false, false, false>);
+        return proto.comm ? go(fill_tiles_batch<RPW, true, false, true, false, true>)
+                          : go(fill_tiles_batch<RPW, false, false, true, false, false>);
+    if (split) return go(fill_tiles_batch<RPW, true, true, false, false, false>);
+    return proto.comm ? go(fill_tiles_batch<RPW, true, false, false, false, false>)
+                      : go(fill_tiles_batch<RPW, false, false, false, false, false>);
+}
+
+}  // namespace
+
+int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (width != 32) return 3;  // 32-bit costs
+    if (tp.rpw == 1) return launch_fill_tiles_r<1>(d, tp, st);
+    if (tp.rpw == 2) return launch_fill_tiles_r<2>(d, tp, st);
+    return 3;
+}
+
+TileSmem tile_batch_smem(const TilePlan& proto) { return tile_smem(proto); }
+
+int launch_fill_tiles_batch(const InstDesc* descs, const TilePlan* tps, const int2* jobs,
+                            int njobs, unsigned int* counter, const TilePlan& proto, void* stream,
+                            const TilePlan* walk) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (njobs <= 0) return 0;
+    if (proto.rpw == 1)
+        return launch_fill_tiles_batch_r<1>(descs, tps, jobs, njobs, counter, proto, st, walk);
+    if (proto.rpw == 2)
+        return launch_fill_tiles_batch_r<2>(descs, tps, jobs, njobs, counter, proto, st, walk);
+    return 3;
 }
 
 }  // namespace rkr

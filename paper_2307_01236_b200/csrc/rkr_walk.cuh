@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 
 #include "rkr_internal.h"
@@ -46,7 +47,9 @@ struct SharedMenuView {
 
 // K2: build_schedule_rec as an explicit stack walk on one thread.  Stack
 // entries are int4 {type, s, t, m}: type 0 = cell to expand, type 1 =
-// pending BlockBwd(s, t = option).  out = {n_ops, status, bad_s, bad_t, top}.
+// pending BlockBwd(s, t = option).  out = {n_ops, status, bad_s, bad_t, top};
+// status 2 = infinite cell (bad_s, bad_t), 3 = the menu lacks the option
+// (bad_s = block, bad_t = option id).
 template <typename V, typename MV>
 __device__ void walk(const Geometry& g, const MV& mv, const V* __restrict__ opt,
                      const uint16_t* __restrict__ arg, int s0, int t0, int m0,
@@ -114,6 +117,13 @@ __device__ void walk(const Geometry& g, const MV& mv, const V* __restrict__ opt,
         if (!(code & kCutBit)) {  // Option (chain_dp.hpp:217-232)
             const int q = mv.blk(s) + code - 1;
             const int val = mv.id(q);
+            const int chg = mv.chg(q);
+            if (chg == kMissingShift) {  // (rkr_backtrack_menu)  // menu_option throws (chain_dp.hpp:203)
+                status = 3;
+                bad_s = s;
+                bad_t = val;
+                break;
+            }
             emit(2, s, val);
             if (s == t) {
                 if (t == L - 1) emit(0, t, -1);
@@ -122,7 +132,7 @@ __device__ void walk(const Geometry& g, const MV& mv, const V* __restrict__ opt,
             } else {
                 stack[sp++] = make_int4(1, s, val, 0);
                 cs = s + 1;  // (s + 1, t, m - chg) next
-                cm = m - mv.chg(q);
+                cm = m - chg;
                 have = true;
             }
         } else {  // Cut (chain_dp.hpp:233-244)

@@ -17,6 +17,8 @@ fallback: if the library or the device is missing, calls raise.
 """
 from __future__ import annotations
 
+import contextlib
+import contextvars
 import ctypes
 import os
 from dataclasses import dataclass, field
@@ -57,7 +59,8 @@ class RkrOp(ctypes.Structure):
 
 class RkrExec(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("stream", ctypes.c_void_p), ("width", ctypes.c_int32),
-                ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+                ("kernel", ctypes.c_int32), ("tune", ctypes.c_int32), ("tile_rows", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 _lib = None
@@ -95,6 +98,7 @@ def lib() -> ctypes.CDLL:
     L.rkr_table_row.argtypes = [p, i32, i32, p, p, p]
     L.rkr_table_download.argtypes = [p, p, p, p]
     L.rkr_backtrack.argtypes = [p, i32, i32, i32, P(RkrOp), i64, P(i64)]
+    L.rkr_backtrack_menu.argtypes = [p, P(RkrMenu), i32, i32, i32, P(RkrOp), i64, P(i64)]
     L.rkr_first_feasible.argtypes = [p, i32, i32, P(i32)]
     L.rkr_solve_chain.argtypes = [P(RkrMenu), i64, i32, P(RkrExec), P(RkrOp), i64, P(i64), P(i64),
                                   P(i64), P(i32), P(i64)]
@@ -168,6 +172,27 @@ def _check(st: int, min_feasible: int = -1) -> None:
 
 KERNELS = {"persistent": 0, "diagonal": 1, "queue": 2, "tiles": 3}
 
+# rkr_exec.tune bits (include/rkr.h rkr_tune)
+TUNE = {"no_tiles": 1 << 0, "jobs": 1 << 1, "comm_off": 1 << 2, "comm_on": 1 << 3,
+        "split_off": 1 << 4, "split_on": 1 << 5, "stream": 1 << 6, "batch_queue": 1 << 7,
+        "profile": 1 << 8}
+_tuning: contextvars.ContextVar = contextvars.ContextVar("rkr_tuning", default=(0, 0))
+
+
+@contextlib.contextmanager
+def tuning(*flags: str, tile_rows: int = 0):
+    """Kernel-variant overrides for every table created inside the block
+    (rkr_exec.tune / tile_rows; A/B measurements and variant-pinning tests).
+    Results are identical under every setting."""
+    bits = 0
+    for f in flags:
+        bits |= TUNE[f]
+    tok = _tuning.set((bits, tile_rows))
+    try:
+        yield
+    finally:
+        _tuning.reset(tok)
+
 
 def _exec(device: int, width: str, stream: Optional[int] = None,
           kernel: str = "persistent") -> RkrExec:
@@ -176,6 +201,7 @@ def _exec(device: int, width: str, stream: Optional[int] = None,
     e.stream = stream
     e.width = 64 if width == "64" else 0
     e.kernel = KERNELS[kernel]
+    e.tune, e.tile_rows = _tuning.get()
     return e
 
 
@@ -392,18 +418,30 @@ class DpTable:
         L = self.length()
         return int(self._host[0][s * L - s * (s - 1) // 2 + (t - s), m])
 
-    def backtrack(self, s: int, t: int, m: int) -> List[Tuple[int, int, int]]:
-        """Raw device backtrack: (kind, block, option) triples."""
+    def backtrack(self, s: int, t: int, m: int, menu: Optional[Menu] = None,
+                  partial: Optional[list] = None) -> List[Tuple[int, int, int]]:
+        """Raw device backtrack: (kind, block, option) triples.  menu: the
+        caller's menu for the option lookups and pack shifts (as
+        build_schedule_rec does, chain_dp.hpp:200-205, :228); default the
+        table's own.  On an error, `partial` receives the ops emitted before it."""
+        ms = menu.struct() if menu is not None else None
         cap = 4096
         while True:
             buf = (RkrOp * cap)()
             n = ctypes.c_int64()
-            st = self._lib.rkr_backtrack(self._h, s, t, m, buf, cap, ctypes.byref(n))
+            if ms is None:
+                st = self._lib.rkr_backtrack(self._h, s, t, m, buf, cap, ctypes.byref(n))
+            else:
+                st = self._lib.rkr_backtrack_menu(self._h, ctypes.byref(ms), s, t, m, buf, cap,
+                                                  ctypes.byref(n))
             if st == RKR_ERR_CAPACITY:
                 cap = n.value
                 continue
+            ops = [(buf[i].kind, buf[i].block, buf[i].option) for i in range(min(n.value, cap))]
+            if st != 0 and partial is not None:
+                partial.extend(ops)
             _check(st)
-            return [(buf[i].kind, buf[i].block, buf[i].option) for i in range(n.value)]
+            return ops
 
     def first_feasible(self, s: int, t: int) -> int:
         m = ctypes.c_int32()
@@ -425,8 +463,16 @@ def _named(ops, chain: Chain) -> List[ScheduleOp]:
 
 def build_schedule_rec(table: DpTable, menu: Menu, chain: Chain, s: int, t: int, m: int,
                        out: Optional[list] = None) -> List[ScheduleOp]:
-    """remat::build_schedule_rec (chain_dp.hpp:211-246), walked on the device."""
-    ops = _named(table.backtrack(s, t, m), chain)
+    """remat::build_schedule_rec (chain_dp.hpp:211-246), walked on the device
+    with the caller's menu for the option lookups (ValidationError when it
+    lacks a decided option; `out` then holds the ops emitted before)."""
+    done: list = []
+    try:
+        ops = _named(table.backtrack(s, t, m, menu=menu, partial=done), chain)
+    except Exception:
+        if out is not None:
+            out.extend(_named(done, chain))
+        raise
     if out is not None:
         out.extend(ops)
     return ops

@@ -27,17 +27,19 @@ with rotor.DpTable(synthetic_menu(14, 12, 600, 7, tie_stress=True), 1, 600, kern
     t.backtrack_fetch()
 # streamed K1t as tile jobs with the fused walk on a long chain (the walk's
 # menu copy does not fit the program slices: global-menu walk)
-os.environ["RKR_JOBS"] = "1"
-with rotor.DpTable(synthetic_menu(200, 32, 40, 9), 1, 40, kernel="tiles") as t:
+with rotor.tuning("jobs"), rotor.DpTable(synthetic_menu(200, 32, 40, 9), 1, 40, kernel="tiles") as t:
     t.refill_walk(0, 199, 40)
     t.backtrack_fetch()
-del os.environ["RKR_JOBS"]
+# two rows per warp (16-slot tiles), co-resident and as tile jobs
+for fl in ((), ("jobs",)):
+    with rotor.tuning(*fl, tile_rows=2), rotor.DpTable(synthetic_menu(21, 6, 500, 4), 1, 500,
+                                                       kernel="tiles") as t:
+        t.refill_walk(0, 20, 500)
+        t.backtrack_fetch()
 # K1t without the communication warp (the large-table variant)
-os.environ["RKR_COMM"] = "0"
-with rotor.DpTable(synthetic_menu(10, 4, 600, 5), 1, 600, kernel="tiles") as t:
+with rotor.tuning("comm_off"), rotor.DpTable(synthetic_menu(10, 4, 600, 5), 1, 600, kernel="tiles") as t:
     t.refill_walk(0, 9, 600)
     t.backtrack_fetch()
-del os.environ["RKR_COMM"]
 for kernel in ("persistent", "queue"):  # tile jobs / row-segment queue
     b = rotor.Batch([tiny_chain_menu(), synthetic_menu(8, 3, 300, 7)], [1, 1], [64, 300],
                     kernel=kernel)

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 20
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.rkr_abi_version() == 1
+    assert lib.rkr_abi_version() == 2
 
 
 def test_quantize_matches_reference(kat):

@@ -399,30 +399,29 @@ def test_refill_walk_matches_oracle(orc, kernel, L, B, M, seed):
         assert_same((do, dk, dv), (o, k, v))
 
 
-def test_tiles_without_communication_warp(orc, monkeypatch):
+@pytest.mark.parametrize("rows", [1, 2])
+def test_tiles_without_communication_warp(orc, rows):
     """The barrier-aligned K1t variant (large tables) on small tables, fill and fused walk."""
-    monkeypatch.setenv("RKR_COMM", "0")
     for L, B, M, seed in [(12, 6, 200, 7), (40, 8, 1500, 11), (3, 2, 20, 5)]:
         menu = synthetic_menu(L, B, M, seed, tie_stress=True)
         st, o, k, v, _, _ = orc.fill(menu, 1, M)
-        with rotor.DpTable(menu, 1, M, kernel="tiles") as t:
+        with rotor.tuning("comm_off", tile_rows=rows), rotor.DpTable(menu, 1, M, kernel="tiles") as t:
             assert_same(t.download(), (o, k, v))
             t.refill_walk(0, L - 1, M)
             bst, ref_ops = orc.build_schedule(menu, 1, M, (o, k, v), 0, L - 1, M)
             assert bst == 0 and t.backtrack_fetch() == ref_ops
 
 
-@pytest.mark.parametrize("comm", ["1", "0"])
-def test_tiles_as_jobs(orc, monkeypatch, comm):
-    """K1t as a one-table job queue (tables with more 32-slot tiles than SMs,
-    forced here on small ones), with and without the communication warp: the
-    whole table and the fused walk against the oracle."""
-    monkeypatch.setenv("RKR_JOBS", "1")
-    monkeypatch.setenv("RKR_COMM", comm)
-    for L, B, M, seed in [(12, 6, 200, 7), (33, 16, 1500, 44), (3, 2, 20, 5)]:
+@pytest.mark.parametrize("rows", [1, 2])
+@pytest.mark.parametrize("comm", ["comm_on", "comm_off"])
+def test_tiles_as_jobs(orc, comm, rows):
+    """K1t as a one-table job queue (tables with more tiles than SMs, forced
+    here on small ones), with and without the communication warp, one or two
+    rows per warp: the whole table and the fused walk against the oracle."""
+    for L, B, M, seed in [(12, 6, 200, 7), (33, 16, 1500, 44), (3, 2, 20, 5), (9, 5, 40, 3)]:
         menu = synthetic_menu(L, B, M, seed, tie_stress=True)
         st, o, k, v, _, _ = orc.fill(menu, 1, M)
-        with rotor.DpTable(menu, 1, M, kernel="tiles") as t:
+        with rotor.tuning("jobs", comm, tile_rows=rows), rotor.DpTable(menu, 1, M, kernel="tiles") as t:
             assert_same(t.download(), (o, k, v))
             for m in (M, M // 2):
                 t.refill_walk(0, L - 1, m)
@@ -432,22 +431,67 @@ def test_tiles_as_jobs(orc, monkeypatch, comm):
             assert_same(t.download(), (o, k, v))
 
 
-@pytest.mark.parametrize("env", [{"RKR_STREAM": "1"}, {"RKR_STREAM": "1", "RKR_COMM": "0"},
-                                 {"RKR_STREAM": "1", "RKR_JOBS": "1"}])
-def test_tiles_streamed_programs(orc, monkeypatch, env):
+@pytest.mark.parametrize("rows", [1, 2])
+@pytest.mark.parametrize("flags", [("stream",), ("stream", "comm_off"), ("stream", "jobs")])
+def test_tiles_streamed_programs(orc, flags, rows):
     """K1t with programs, thresholds and option data read from global memory
     (the long-chain variant), co-resident / without the communication warp /
-    as tile jobs: whole tables and the fused walk against the oracle."""
-    for k_, v_ in env.items():
-        monkeypatch.setenv(k_, v_)
+    as tile jobs, one or two rows per warp: whole tables and the fused walk
+    against the oracle."""
     # (200 x 32: the walk's menu copy (53 KB) exceeds the streamed kernels'
     # 32 KB program slices and option slices -- it must use the global menu)
     for L, B, M, seed in [(12, 6, 200, 7), (40, 20, 900, 45), (3, 2, 20, 5), (70, 9, 300, 8),
                           (200, 32, 40, 9)]:
         menu = synthetic_menu(L, B, M, seed, tie_stress=True)
         st, o, k, v, _, _ = orc.fill(menu, 1, M)
-        with rotor.DpTable(menu, 1, M, kernel="tiles") as t:
+        with rotor.tuning(*flags, tile_rows=rows), rotor.DpTable(menu, 1, M, kernel="tiles") as t:
             assert_same(t.download(), (o, k, v))
             t.refill_walk(0, L - 1, M)
             bst, ref_ops = orc.build_schedule(menu, 1, M, (o, k, v), 0, L - 1, M)
             assert _walk_or_inf(t.backtrack_fetch) == (ref_ops if bst == 0 else "infeasible")
+
+
+def _caller_menus(menu: Menu, seed: int):
+    """A copy with the pack size of some saved options changed, and one with
+    a saved option of every other block dropped (ids then missing)."""
+    rng = np.random.default_rng(seed)
+    bumped = Menu.from_options([menu.options(b) for b in range(menu.L)], list(menu.act_sizes))
+    for o in range(len(bumped.save_mem)):
+        if bumped.has_bwd[o] and rng.random() < 0.5:
+            bumped.save_mem[o] += int(rng.integers(0, 12))
+    blocks = []
+    for b in range(menu.L):
+        opts = menu.options(b)
+        saved = [o for o in opts if o.option_id != 0]
+        if b % 2 == 1 and len(saved) > 1:
+            opts = [o for o in opts if o.option_id != saved[0].option_id]
+        blocks.append(opts)
+    dropped = Menu.from_options(blocks, list(menu.act_sizes))
+    return bumped, dropped
+
+
+@pytest.mark.parametrize("L, B, M, seed", [(12, 6, 200, 7), (20, 9, 400, 3), (33, 16, 600, 44)])
+def test_build_schedule_rec_uses_the_callers_menu(orc, L, B, M, seed):
+    """build_schedule_rec(table, menu, ...) looks options up in the CALLER's
+    menu (chain_dp.hpp:200-205, :228), as the oracle does: a menu with other
+    pack sizes walks other cells, a menu lacking a decided option raises
+    ValidationError with the ops emitted before it (rkr_backtrack_menu)."""
+    menu = synthetic_menu(L, B, M, seed, tie_stress=True)
+    st, o, k, v, _, _ = orc.fill(menu, 1, M)
+    assert st == 0
+    bumped, dropped = _caller_menus(menu, seed)
+    chain = rotor.Chain.skeleton(L)
+    with rotor.DpTable(menu, 1, M) as t:
+        for m in (M, 3 * M // 4, M // 2):
+            # the table's own menu: identical to the plain walk
+            assert t.backtrack(0, L - 1, m, menu=menu) == t.backtrack(0, L - 1, m)
+            for caller in (bumped, dropped):
+                rst, want = orc.build_schedule(caller, 1, M, (o, k, v), 0, L - 1, m)
+                if rst == 0:
+                    assert t.backtrack(0, L - 1, m, menu=caller) == want, m
+                    continue
+                done = []
+                exc = rotor.ValidationError if rst == 1 else rotor.InfeasibleBudget
+                with pytest.raises(exc):
+                    rotor.build_schedule_rec(t, caller, chain, 0, L - 1, m, out=done)
+                assert [(x.kind, x.block, x.option) for x in done] == want, m

@@ -137,3 +137,63 @@ def test_solve_and_sweep_from_files(tmp_path, orc, L, B, M, seed, budget_frac):
         assert r.feasible == (st == 0)
         if st == 0:
             assert (r.opt_time, r.ops) == (t, ops)
+
+
+# ---------------------------------------------------------------------------
+# Documents produced by the reference itself (tests/dropin/options_ref.cpp,
+# built against /root/reference alone by tests/dropin/Makefile): its chain
+# fixtures proj/tests/fixtures/{tiny,ababab}_chain.json re-encoded by
+# ingest.hpp's save_chain, the option menus its ILP generates encoded by
+# ingest.hpp's encode_options (the `remat solve --save-options` document), and
+# cmd_solve's results (schedule_with_menu) over a budget ladder.
+# ---------------------------------------------------------------------------
+import os  # noqa: E402
+
+_GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+_REF_FIXTURES = ("tiny", "ababab")
+_KIND = {"compute": 0, "forget": 1, "block_fwd": 2, "block_bwd": 3}
+
+
+def _ref_paths(name):
+    return (os.path.join(_GOLD, f"ref_chain_{name}.json"),
+            os.path.join(_GOLD, f"ref_options_{name}.json"),
+            os.path.join(_GOLD, f"ref_solve_{name}.json"))
+
+
+@pytest.mark.parametrize("name", _REF_FIXTURES)
+def test_reference_encoded_documents_round_trip(tmp_path, name):
+    """options_io reads the reference's own documents and writes them back
+    with the same content (field for field, option for option)."""
+    cpath, opath, _ = _ref_paths(name)
+    chain = oio.load_chain(cpath)
+    ms = oio.read_options_file(chain, opath)
+    out = tmp_path / "again.json"
+    oio.write_options_file(ms.classes, str(out))
+    assert json.load(open(out)) == json.load(open(opath))
+    assert ms.menu.L == chain.length()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", _REF_FIXTURES)
+def test_reference_options_solve_like_cmd_solve(name):
+    """`remat solve --load-options` on the reference's documents: every
+    budget's opt_time and block-level schedule (or the min-feasible budget)
+    equals the reference's cmd_solve on the same chain and menus.  For the
+    tiny chain at 300 B: 86 us."""
+    cpath, opath, spath = _ref_paths(name)
+    res = json.load(open(spath))
+    for row in res["rows"]:
+        b = row["budget"]
+        if row.get("infeasible"):
+            with pytest.raises(rotor.InfeasibleBudget) as e:
+                oio.solve_files(cpath, opath, b, res["units"])
+            assert e.value.min_feasible_budget == row["min_feasible"], b
+            continue
+        sol = oio.solve_files(cpath, opath, b, res["units"])
+        assert sol.opt_time == row["opt_time"], b
+        got = [(o.kind, o.block, o.option, o.target) for o in sol.schedule]
+        want = [(_KIND[k], blk, opt, tgt) for k, blk, opt, tgt in row["ops"]]
+        assert got == want, b
+    if name == "tiny":
+        r300 = [r for r in res["rows"] if r["budget"] == 300][0]
+        assert r300["opt_time"] == 86 and r300["peak"] == 288

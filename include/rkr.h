@@ -105,7 +105,9 @@ typedef enum {
     RKR_TUNE_SPLIT_ON = 1 << 5,    /* split tails (with the communication warp) */
     RKR_TUNE_STREAM = 1 << 6,      /* streamed cut programs even when they fit shared memory */
     RKR_TUNE_BATCH_QUEUE = 1 << 7, /* batches on the row-segment queue (K1p) */
-    RKR_TUNE_PROFILE = 1 << 8      /* host phase timers on stderr (synchronises: never for timing) */
+    RKR_TUNE_PROFILE = 1 << 8,     /* host phase timers on stderr (synchronises: never for timing) */
+    RKR_TUNE_WIDE_SEARCH = 1 << 9  /* min-feasible search by filling the wide table (as the
+                                      reference does) instead of the threshold recurrence */
 } rkr_tune;
 
 /* Execution settings; pass NULL for defaults (device 0, the library's shared

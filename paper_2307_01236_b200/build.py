@@ -12,8 +12,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librkr.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("rkr_kernels.cu", "rkr_persist.cu", "rkr_tiles.cu", "rkr_capi.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "rkr_internal.h"), os.path.join(CSRC, "rkr_walk.cuh"), os.path.join(ROOT, "include", "rkr.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("rkr_kernels.cu", "rkr_persist.cu", "rkr_tiles.cu",
+                                            "rkr_table.cu", "rkr_batch.cu", "rkr_shard.cu",
+                                            "rkr_replay.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, h) for h in ("rkr_internal.h", "rkr_host.h", "rkr_walk.cuh")] + [
+    os.path.join(ROOT, "include", "rkr.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -170,9 +170,13 @@ int launch_walk_sharded(const ShardView* sv, int n, const DevMenu& dm, int L, in
 int launch_batch_tops(const InstDesc* d, const int32_t* m_at, int n, int width, int64_t* out,
                       void* stream);
 int launch_batch_first_feasible(const InstDesc* d, int n, int width, int32_t* out, void* stream);
+// min-feasible thresholds thr(0, L-1) of the tables d[which[i]] (rkr_kernels.cu);
+// scratch + scr_off[i]: L(L+1)/2 int64 per instance
+int launch_batch_thresholds(const InstDesc* d, const int32_t* which, int n, int64_t* scratch,
+                            const int64_t* scr_off, int64_t* out, void* stream);
 // Fill n tables with ONE persistent launch.  All tables share the cost
 // width and the plan's R.  The counter and every table's done flags must be
-// zeroed on `stream` before the call (they are, by the callers in rkr_capi).
+// zeroed on `stream` before the call (they are, by the callers in rkr_table.cu / rkr_batch.cu).
 // single != nullptr: a one-table launch whose descriptor is passed by value.
 int launch_fill_batch(const InstDesc* dev_desc, const InstDesc* single, const LaunchPlan& lp,
                       int width, int R, int kcap, int ocap, unsigned long long* counter,

@@ -499,6 +499,68 @@ int launch_batch_tops(const InstDesc* d, const int32_t* m_at, int n, int width, 
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+// solve_chain's min-feasible search (chain_dp.hpp:265-288) without the wide
+// table.  Whether opt(s, t, m) is finite does not depend on the times, and it
+// is upward closed in m (every admission test of :141-174 is "requirement <=
+// m" and every read of a smaller span is at m minus a shift >= 0), so it is
+// the threshold thr(s, t) = the smallest feasible m, a min-max recurrence over
+// the same candidates with no budget axis:
+//   option oi (:141-151):  max(fwd_need, bwd_req [, pack_chg + thr(s+1, t)])
+//   cut c (:158-171):      max(gate(s, c), act_u[c] + thr(c, t), thr(s, c-1))
+// with gate(s, c) = the sweep gate (:159) and the prefix maximum behind the
+// `break` (:164), and thr clamped at 0 (budgets are >= 0).  The wide table's
+// first finite m is thr(0, L-1) when it is <= cap.  Exact as long as every
+// finite candidate total stays below kInfTime (the host's 64-bit overflow
+// proof; else the wide table runs).  One CTA per instance; the thresholds of
+// a diagonal depend only on smaller spans, so a CTA barrier per diagonal.
+__global__ void batch_thresholds(const InstDesc* __restrict__ d, const int32_t* __restrict__ which,
+                                 int64_t* __restrict__ scratch, const int64_t* __restrict__ scr_off,
+                                 int64_t* __restrict__ out) {
+    const InstDesc& D = d[which[blockIdx.x]];
+    const DevMenu& dm = D.dm;
+    const int L = D.g.L;
+    int64_t* thr = scratch + scr_off[blockIdx.x];  // [row_id(L, s, t)]
+    for (int k = 0; k < L; ++k) {
+        for (int s = threadIdx.x; s < L - k; s += blockDim.x) {
+            const int t = s + k;
+            const bool seeded = t < L - 1;                                     // :126-127
+            const int64_t seed = seeded ? 2 * dm.act_u[t + 1] : 0;
+            int64_t best = kInf64;
+            const int64_t sub = s < t ? thr[row_id(L, s + 1, t)] : 0;
+            for (int q = dm.blk_off[s]; q < dm.blk_off[s + 1]; ++q) {          // :139-156
+                int64_t c = (s == t && seeded) ? dm.fwd_req_pre[q] + dm.act_u[t + 1]
+                                               : dm.fwd_req[q] + seed;
+                c = max(c, dm.bwd_req[q]);
+                if (s < t) {
+                    if (sub >= kInf64) continue;
+                    c = max(c, dm.pack_chg[q] + sub);
+                }
+                best = min(best, c);
+            }
+            if (s < t) {                                                       // :158-174
+                int64_t gate = dm.fwd0_own[s] + seed;
+                for (int c = s + 1; c <= t; ++c) {
+                    if (c - 1 > s) gate = max(gate, dm.fwd0_full[c - 1] + seed);
+                    const int64_t r = thr[row_id(L, c, t)], l = thr[row_id(L, s, c - 1)];
+                    if (r >= kInf64 || l >= kInf64) continue;
+                    best = min(best, max(max(gate, dm.act_u[c] + r), l));
+                }
+            }
+            thr[row_id(L, s, t)] = best >= kInf64 ? kInf64 : max(best, (int64_t)0);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = thr[row_id(L, 0, L - 1)];
+}
+
+int launch_batch_thresholds(const InstDesc* d, const int32_t* which, int n, int64_t* scratch,
+                            const int64_t* scr_off, int64_t* out, void* stream) {
+    if (n <= 0) return 0;
+    batch_thresholds<<<n, 128, 0, static_cast<cudaStream_t>(stream)>>>(d, which, scratch, scr_off,
+                                                                      out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 int launch_batch_first_feasible(const InstDesc* d, int n, int width, int32_t* out, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (width == 32)

@@ -391,7 +391,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             }
             // trace: when the lower tiles' diagonal k-1 was acquired (the
             // compute warps pass READY at max(this, their last bulk))
-            if (tp.trace && lane == 0) tp.trace[6 * ((int64_t)k * tp.T + j) + 1] = t_gtimer();
+            if (tp.trace && lane == 0) tp.trace[6 * ((int64_t)k * tp.T + j) + 3] = clock64();
             nb_arrive(kBarReady);
             nb_sync(kBarDone);  // the compute warps stored diagonal k
             if (lane == 0) {
@@ -414,8 +414,15 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         if (L > 1) stage_step(tp, pq, sm, smem_raw, bars, L, 1);
     }
     for (int k = 0; k < L; ++k) {
-        unsigned long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
-        if (tp.trace && tid == 0) t0 = t_gtimer();
+        // trace (per (diagonal, tile)): [0] globaltimer at the step start (the
+        // cross-SM timeline); SM cycles: [1] step start, [2] warp 0's bulk
+        // done, [3] the communication warp's acquisition of diagonal k-1
+        // (COMM), [4] READY passed, [5] warp 0's tail done
+        unsigned long long t0 = 0, c0 = 0, t1 = 0, t2 = 0, t3 = 0;
+        if (tp.trace && tid == 0) {
+            t0 = t_gtimer();
+            c0 = clock64();
+        }
         if (!STREAM) mbar_wait(bars + (k & 1), ((k & 1 ? ph1 : ph0) + (uint32_t)(k >> 1)) & 1u);
         // this step's cut programs and option thresholds: the staged copies,
         // or (STREAM) straight from global memory
@@ -473,7 +480,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 pcode[it * 32 + lane] = (uint16_t)code;
             }
         }
-        if (tp.trace && tid == 0) t1 = t_gtimer();
+        if (tp.trace && tid == 0) t1 = clock64();
         // diagonal k-1 of the lower tiles acquired (and, with P > 1, every
         // bulk part of this step written)
         if constexpr (COMM) {
@@ -491,7 +498,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             }
             __syncthreads();
         }
-        if (tp.trace && tid == 0) t2 = t_gtimer();
+        if (tp.trace && tid == 0) t2 = clock64();
 
         // ---- tail -------------------------------------------------------------------
         // Candidates are merged in the reference's scan order -- options (menu
@@ -572,6 +579,9 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 constexpr bool SUB = decltype(has_sub)::value;
                 const uint32_t* __restrict__ optw =
                     lane_base(opt, SUB ? (rid - (L - k)) * sr + g.pad + m : 0);
+                // (software-pipelining the batches -- the next batch's reads
+                // in flight during this batch's compares -- spills inside the
+                // loop at 64 registers per thread)
                 for (int i0 = ia; i0 < ib; i0 += kOB) {
                     uint32_t sub[kOB], ot[kOB];
                     int32_t th[kOB];
@@ -671,13 +681,13 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             }
         }
         if (tp.trace && tid == 0) {
-            t3 = t_gtimer();
+            t3 = clock64();
             unsigned long long* tr = tp.trace + 6 * ((int64_t)k * tp.T + j);
-            tr[0] = t0;  // the K1p stamp layout; stamp 1: the communication warp's
-            if (!COMM) tr[1] = t0;  // acquisition of diagonal k-1 (else = 0)
+            tr[0] = t0;
+            tr[1] = c0;
             tr[2] = t1;
-            tr[3] = t2;
-            tr[4] = t3;
+            if (!COMM) tr[3] = t1;
+            tr[4] = t2;
             tr[5] = t3;
         }
         if constexpr (COMM) {

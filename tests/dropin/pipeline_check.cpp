@@ -7,8 +7,9 @@
 // reference alone (CPU; its output is tests/golden/dropin_pipeline.txt),
 // against this repo's drop-in (include/ first: the DP and the simulator of
 // this repo, the fill and walk on the GPU), and with -DRKR_B200_GATE, where
-// schedule_with_menu / flatten_schedule / chain_max_peak are this repo's own
-// (include/remat_b200/gate.hpp).  All outputs must be equal, line for line.
+// build_menus / schedule_with_menu / flatten_schedule / chain_max_peak are
+// this repo's own (include/remat_b200/menus.hpp, gate.hpp).  All outputs must
+// be equal, line for line.
 #include <cstdio>
 #include <random>
 #include <string>
@@ -16,8 +17,9 @@
 
 #include "remat/pipeline.hpp"
 #include "test_helpers.hpp"
-#ifdef RKR_B200_GATE  // this repo's own gate (include/remat_b200/gate.hpp)
+#ifdef RKR_B200_GATE  // this repo's own gate and menu builder (include/remat_b200/)
 #include "remat_b200/gate.hpp"
+#include "remat_b200/menus.hpp"
 namespace gate = remat::b200;
 #else  // pipeline.hpp's
 namespace gate = remat;
@@ -48,7 +50,7 @@ void run_chain(const char* name, const Chain& chain, int units) {
     st.n_save = 3;
     st.units = units;
     st.time_limit_seconds = 60.0;
-    MenuSet ms = build_menus(chain, st);
+    MenuSet ms = gate::build_menus(chain, st);
     const OptionMenu& menu = ms.menu;
     int nopt = 0;
     for (const auto& b : menu.options) nopt += (int)b.size();

@@ -20,6 +20,7 @@ and testing::atomic_replay (tests/test_helpers.hpp:249-322).  Outputs
   cfg5twin  config-5 twin (L=256, B=64, M=4096, seed 47 -- bench.py's N=1
             sharded chain): as cfg3
   l1024     config-5 chain length (L=1024, B=64) at M=64: as cfg3
+  l1024m256 the same chain length at M=256 (seed 49): as cfg3
 """
 from __future__ import annotations
 
@@ -117,6 +118,8 @@ PARTS = {
     "cfg4": cfg4_part,
     "cfg5twin": lambda ref: table_part(ref, 256, 64, 4096, 47),
     "l1024": lambda ref: table_part(ref, 1024, 64, 64, 48),
+    # config-5 chain length at M = 256 (~55 G candidates, ~10 min of reference CPU)
+    "l1024m256": lambda ref: table_part(ref, 1024, 64, 256, 49),
 }
 
 

@@ -112,3 +112,31 @@ def test_sweep_chains_equals_one_sweep_per_chain(orc):
                 assert (r.opt_time, r.ops) == (ot, ops)
             else:
                 assert r.min_feasible == mf
+
+
+@pytest.mark.parametrize("seed", [3, 11, 29])
+def test_min_feasible_thresholds_equal_the_wide_table(orc, seed):
+    """solve_chain's min-feasible search (chain_dp.hpp:265-288): the
+    threshold recurrence on the budget's own table (default) and the
+    reference's wide-table scan (RKR_TUNE_WIDE_SEARCH) give the same
+    min_feasible_budget as the oracle, for every budget below and around it,
+    single solves and batched sweeps."""
+    rng = np.random.default_rng(seed)
+    for L, B in ((3, 2), (9, 4), (17, 6)):
+        menu = synthetic_menu(L, B, 300, int(rng.integers(1, 1 << 30)), tie_stress=bool(seed & 1))
+        budgets = sorted({int(x) for x in rng.integers(1, int(menu.act_sizes.sum()) * 3, 24)})
+        units = 37
+        want = []
+        for b in budgets:
+            st, _, ot, un, mt, mf = orc.solve_chain(menu, b, units)
+            want.append((st, mf))
+        for flags in ((), ("wide_search",)):
+            with rotor.tuning(*flags):
+                rows = rotor.sweep_raw(menu, budgets, units)
+                for b, r, (st, mf) in zip(budgets, rows, want):
+                    assert r.feasible == (st == 0), (b, flags)
+                    if st != 0:
+                        assert r.min_feasible == mf, (b, flags)
+                        with pytest.raises(rotor.InfeasibleBudget) as e:
+                            rotor.solve_chain(rotor.Chain.skeleton(L), menu, b, units)
+                        assert e.value.min_feasible_budget == mf, (b, flags)

@@ -81,3 +81,13 @@ def test_reference_simulate_tests_pass_on_this_simulator():
     r = subprocess.run([_bin("ref_simulate_b200")], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "10 test cases (0 failed)" in r.stdout, r.stdout
+
+
+def test_parallel_option_generation_equals_the_reference():
+    """remat::b200::build_menus (every (class, budget pair) ILP solve on a
+    thread pool, the lattice's dependencies kept: include/remat_b200/menus.hpp)
+    returns the reference's build_menus MenuSet member for member on its
+    random chains (host only)."""
+    r = subprocess.run([_bin("menus_check"), "4"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr[-2000:]
+    assert "mismatches 0" in r.stdout, r.stdout

@@ -172,10 +172,40 @@ class ClockSampler:
 
 
 def dist_setup():
+    """RANK / LOCAL_RANK / WORLD_SIZE from torchrun.  With fewer visible GPUs
+    than ranks (a functional check of the N > 1 paths on one GPU), ranks share
+    devices round-robin and the process group runs on gloo (NCCL refuses two
+    ranks on one device); timing such a run says nothing about scaling."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+
+        n = max(1, torch.cuda.device_count())
+        if n < world:
+            global PG_BACKEND
+            PG_BACKEND = "gloo"
+            local %= n
     return world, rank, local
+
+
+PG_BACKEND = "nccl"
+
+
+def init_pg(local):
+    import torch
+    import torch.distributed as dist
+
+    if PG_BACKEND == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("gloo")
+
+
+def reduce_device(local):
+    """Where max_over_ranks' tensor lives: the GPU for NCCL, the host for gloo."""
+    return f"cuda:{local}" if PG_BACKEND == "nccl" else "cpu"
 
 
 # ---------------------------------------------------------------------------
@@ -424,7 +454,7 @@ def b200_arm(args, world, rank, local):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_pg(local)
     if not rotor.lib().rkr_device_ok(local):
         raise SystemExit("bench: no sm_100 device")
     c = CONFIGS[args.config]
@@ -441,7 +471,7 @@ def b200_arm(args, world, rank, local):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=reduce_device(local))
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
@@ -623,7 +653,7 @@ def b200_arm_sweep(args, world, rank, local):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_pg(local)
     menus, rows_all = sweep_instances()
     costs = [instance_cost(menus[ci], max(mt, 0)) for _, ci, _, _, mt in rows_all]
     mine = set(partition_lpt(costs, world)[rank])
@@ -641,7 +671,7 @@ def b200_arm_sweep(args, world, rank, local):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=reduce_device(local))
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
@@ -843,7 +873,7 @@ def b200_arm_sharded(args, world, rank, local):
 
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_pg(local)
     cfg = args.config
     c = CONFIGS[cfg]
     L, B, M = c["L"], c["B"], c["M"]
@@ -867,7 +897,7 @@ def b200_arm_sharded(args, world, rank, local):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=reduce_device(local))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

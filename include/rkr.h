@@ -106,8 +106,10 @@ typedef enum {
     RKR_TUNE_STREAM = 1 << 6,      /* streamed cut programs even when they fit shared memory */
     RKR_TUNE_BATCH_QUEUE = 1 << 7, /* batches on the row-segment queue (K1p) */
     RKR_TUNE_PROFILE = 1 << 8,     /* host phase timers on stderr (synchronises: never for timing) */
-    RKR_TUNE_WIDE_SEARCH = 1 << 9  /* min-feasible search by filling the wide table (as the
+    RKR_TUNE_WIDE_SEARCH = 1 << 9, /* min-feasible search by filling the wide table (as the
                                       reference does) instead of the threshold recurrence */
+    RKR_TUNE_UNIFORM = 1 << 10,    /* tile jobs all of one width (no half tiles in the last wave) */
+    RKR_TUNE_MIXED = 1 << 11       /* (tests) tile jobs: half 32-slot, half 16-slot tiles */
 } rkr_tune;
 
 /* Execution settings; pass NULL for defaults (device 0, the library's shared

@@ -204,6 +204,10 @@ struct TilePlan {
     int32_t split = 0;                    // 1 (with comm): late diagonals split each tail over 2 warps
     int32_t stream = 0;                   // 1: programs / thresholds / options read from global (long chains)
     int32_t halo = 0;                     // 1: a budget shard (halo wait / push compiled in; comm, no split)
+    // mixed tile widths (single tables as tile jobs): tiles j >= j1 are
+    // 16-slot (two rows per warp) tiles after j1 32-slot ones, so the last
+    // wave of jobs is made of half jobs
+    int32_t j1 = INT32_MAX;
     // fused K2 (per launch): the last CTA walks from (ws, wt, wm) into wops /
     // wout = {n_ops, status, bad_s, bad_t, top} (rkr_walk.cuh)
     int32_t walk = 0, ws = 0, wt = 0, wm = 0;
@@ -219,6 +223,7 @@ struct TilePlan {
 struct TileKnobs {
     int32_t tune = 0;  // rkr_tune bits
     int32_t rows = 0;  // K1t rows per warp: 0 auto, 1 or 2
+    bool mixed = false;  // a plain single table: may end its tile jobs with half tiles
 };
 // 1 = eligible.  Long chains, whose per-step programs do not fit shared
 // memory, get the streamed-program variant (tp.stream = 1) by default.

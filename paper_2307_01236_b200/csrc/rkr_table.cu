@@ -524,6 +524,7 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
             // batches run 32-slot tiles unless told otherwise (their jobs
             // already fill the GPU); shards get the rows of their sharding
             kn.rows = exec && exec->tile_rows ? exec->tile_rows : (batch_tiles ? 1 : 0);
+            kn.mixed = !spec && !batch_tiles;  // plain single tables only
             t->tiles = tile_plan(t->g, t->width, batch_tiles ? INT32_MAX : sms, (int64_t)h.ids.size(),
                                  (int)round_up(std::max<int32_t>(h.max_opts, 1), kTileOptBatch), kn,
                                  t->tplan) == 1;

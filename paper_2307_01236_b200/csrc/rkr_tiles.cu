@@ -48,6 +48,18 @@ namespace {
 
 constexpr uint32_t INF = kInf32;  // K1t runs the 32-bit cost path only
 
+// timing experiments only (wrong results): skip the lower-tile wait / the
+// release fence of the communication warp
+#ifndef RKR_EXP_NOWAIT
+#define RKR_EXP_NOWAIT 0
+#endif
+#ifndef RKR_EXP_RELAXED
+#define RKR_EXP_RELAXED 0
+#endif
+#ifndef RKR_EXP_DYNUNIT
+#define RKR_EXP_DYNUNIT 0
+#endif
+
 __device__ __forceinline__ int t_ld_relaxed(const int* p) {
     int v;
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -119,6 +131,15 @@ constexpr int kOB = kTileOptBatch;  // options per load batch (ocap is a multipl
 constexpr int kSlice = 64;          // STREAM: cut-program entries staged per warp at a time
 
 inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~15ull); }
+
+// First budget slot of tile j and the tile holding slot x: W-slot tiles, or
+// (mixed plans) j1 32-slot tiles followed by 16-slot ones.
+__host__ __device__ __forceinline__ int tile_lo(const TilePlan& tp, int j) {
+    return j < tp.j1 ? j * tp.W : tp.j1 * 32 + (j - tp.j1) * 16;
+}
+__host__ __device__ __forceinline__ int tile_of(const TilePlan& tp, int x) {
+    return (tp.j1 == INT32_MAX || x < tp.j1 * 32) ? x / tp.W : tp.j1 + (x - tp.j1 * 32) / 16;
+}
 inline TileSmem tile_smem(const TilePlan& tp) {
     TileSmem m;
     const uint64_t L = tp.L;
@@ -145,8 +166,8 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     b = al16(b + np * 2);
     m.blk = (uint32_t)b;
     b = al16(b + (L + 2) * 4);  // block option offsets [L+1] + the last-CTA flag
-    m.split = (uint32_t)b;      // per step: bulk parts and cuts per part
-    b = al16(b + L * 8);
+    m.split = (uint32_t)b;      // per step: bulk parts and cuts per part; 2 unit counters
+    b = al16(b + L * 8 + 8);
     m.opd = (uint32_t)b;
     if (tp.stream) {  // programs, thresholds and options from global memory;
         // per-warp program slices for the bulk
@@ -320,7 +341,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     const int ocap = tp.ocap;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int rw = lane / W, ml = lane % W;  // row within the unit, slot within the tile
-    const int m_lo = j * W;
+    const int m_lo = tile_lo(tp, j);
 
     // Table-independent data in shared memory: block option ranges, and per
     // (block, option slot) the pack shift (negated) clamped to pad (:148) and time_fwd
@@ -342,6 +363,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         }
         s_split[k] = make_int2(P, chunk);
     }
+    int* s_ucnt = reinterpret_cast<int*>(smem_raw + sm.split) + 2 * L;  // bulk units taken, per step parity
+    if (tid < 2) s_ucnt[tid] = 0;
     for (int q = tid; !STREAM && q < L * ocap; q += kNT) {
         const int b = q / ocap, i = q - b * ocap;
         const int o = __ldg(dm.blk_off + b) + i;
@@ -349,7 +372,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                        ? make_int2(-__ldg(pq.pc + o), (int)__ldg(static_cast<const uint32_t*>(pq.otot) + o))
                        : make_int2(0, (int)INF);
     }
-    const int d_eff = tp.d < j ? tp.d : j;  // lower tiles this one reads
+    // lower tiles this one reads: those holding slots [m_lo - pad, m_lo)
+    const int d_eff = j - tile_of(tp, m_lo - g.pad > 0 ? m_lo - g.pad : 0);
     // Budget shards (config 5).  Local slots [Wl - pad, Wl) of this shard are
     // the next shard's halo (its slots [-pad, 0)): tiles that compute them
     // also store them there (peer memory when the next shard is on another
@@ -382,7 +406,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             if (L > 1) stage_step(tp, pq, sm, smem_raw, bars, L, 1);
         }
         for (int k = 0; k < L; ++k) {
-            if (k >= 1) {  // diagonal k-1 of the lower tiles, acquired
+            if (k >= 1 && !RKR_EXP_NOWAIT) {  // diagonal k-1 of the lower tiles, acquired
                 const int* row = done + (int64_t)(k - 1) * tp.T;
                 for (int q = lane; q < d_eff; q += 32)
                     while (t_ld_acquire(row + j - 1 - q) == 0) __nanosleep(20);
@@ -394,10 +418,16 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             if (tp.trace && lane == 0) tp.trace[6 * ((int64_t)k * tp.T + j) + 3] = clock64();
             nb_arrive(kBarReady);
             nb_sync(kBarDone);  // the compute warps stored diagonal k
+#ifdef RKR_TRACE_EXPERIMENT
+            if (tp.trace && lane == 0) tp.trace[6 * ((int64_t)k * tp.T + j) + 0] = clock64();
+#endif
             if (lane == 0) {
                 // release-add: orders the CTA's stores (made visible to this
                 // thread by the barrier) before the flag
-                t_red_release_add(done + (int64_t)k * tp.T + j, 1);
+                if (RKR_EXP_RELAXED)
+                    atomicAdd(done + (int64_t)k * tp.T + j, 1);
+                else
+                    t_red_release_add(done + (int64_t)k * tp.T + j, 1);
                 if (halo_out) push_halo(k);
                 // buffer (k & 1) is free: every compute warp finished tail(k)
                 if (!STREAM && k + 2 < L) {
@@ -461,7 +491,14 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             // top down: on late diagonals the tail of step k-1 occupies the
             // low warps, so the bulk of step k runs beside it
             const float rcp_units = TABLE ? __frcp_ru((float)units) : 0.f;  // it / units, exactly, it < 2^10
-            for (int it = COMM ? kNC - 1 - warp : warp; it < units * P; it += kNC) {
+            const bool dyn = RKR_EXP_DYNUNIT && P == 1;
+            auto grab = [&]() {
+                int v = 0;
+                if (lane == 0) v = atomicAdd(s_ucnt + (k & 1), 1);
+                return __shfl_sync(0xffffffffu, v, 0);
+            };
+            for (int it = dyn ? grab() : (COMM ? kNC - 1 - warp : warp); it < units * P;
+                 it = dyn ? grab() : it + kNC) {
                 const int p = P == 1 ? 0 : (TABLE ? (int)((float)it * rcp_units) : it / units);
                 const int u = it - p * units;
                 const int s = min(u * RPW + rw, rows - 1);  // (a clamped row is not stored)
@@ -499,6 +536,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             __syncthreads();
         }
         if (tp.trace && tid == 0) t2 = clock64();
+
+        if (RKR_EXP_DYNUNIT && tid == 0) s_ucnt[k & 1] = 0;  // bulk(k) done: re-arm for k + 2
 
         // ---- tail -------------------------------------------------------------------
         // Candidates are merged in the reference's scan order -- options (menu
@@ -683,7 +722,9 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         if (tp.trace && tid == 0) {
             t3 = clock64();
             unsigned long long* tr = tp.trace + 6 * ((int64_t)k * tp.T + j);
+#ifndef RKR_TRACE_EXPERIMENT
             tr[0] = t0;
+#endif
             tr[1] = c0;
             tr[2] = t1;
             if (!COMM) tr[3] = t1;
@@ -841,7 +882,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
 // tiles of its own table, which were dequeued earlier by CTAs that are
 // running or done, so the queue cannot deadlock and tables need not be
 // co-resident.
-template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool WALK, bool HALO>
+template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool WALK, bool HALO, bool MIXED = false>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __restrict__ descs,
                                                           const TilePlan* __restrict__ tps,
                                                           const int2* __restrict__ jobs, int njobs,
@@ -864,8 +905,12 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
         const int q = s_job;
         if (q >= njobs) break;
         const int2 jb = jobs[q];
-        tile_job<RPW, COMM, SPLIT, STREAM, false, HALO>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0,
-                                                       ph1);
+        if (MIXED && jb.y >= tps[jb.x].j1)  // a half tile of the last wave
+            tile_job<2, COMM, SPLIT, STREAM, false, HALO>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0,
+                                                          ph1);
+        else
+            tile_job<RPW, COMM, SPLIT, STREAM, false, HALO>(descs[jb.x], tps[jb.x], jb.y, smem_raw,
+                                                            ph0, ph1);
         const int L = descs[jb.x].g.L;
         ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
         ph1 += (uint32_t)L / 2;
@@ -962,6 +1007,28 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, const
         if (!(kn.tune & RKR_TUNE_COMM_OFF)) tp.comm = 1;
         tp.sm = tile_smem(tp);
     }
+    // The last wave of tile jobs: 513 jobs of config 3 on 148 SMs run as 3
+    // full waves and a fourth of 69 jobs (14 % of the SMs idle over the
+    // fill).  When the jobs past the full waves cover at most half a wave,
+    // they become 16-slot tiles (two rows per warp, measured 0.69 of a
+    // 32-slot job): one wave of half jobs instead of a wave of whole ones.
+    tp.j1 = INT32_MAX;
+    if (kn.mixed && tp.jobs && rpw == 1 && tp.comm && !tp.stream && !tp.split &&
+        !(kn.tune & RKR_TUNE_UNIFORM)) {
+        const int64_t full = (T / sms) * sms;  // jobs in full waves
+        const int64_t rest = (int64_t)g.M + 1 - 32 * full;
+        const int64_t halves = (rest + 15) / 16;
+        if (full > 0 && rest > 0 && halves <= sms) {
+            tp.j1 = (int32_t)full;
+            tp.T = (int32_t)(full + halves);
+        }
+    }
+    if ((kn.tune & RKR_TUNE_MIXED) && kn.mixed && tp.jobs && rpw == 1 && tp.comm && !tp.stream &&
+        !tp.split && T >= 2) {  // test knob: half the tiles 32-slot, the rest 16-slot
+        const int64_t j1 = T / 2, rest = (int64_t)g.M + 1 - 32 * j1;
+        tp.j1 = (int32_t)j1;
+        tp.T = (int32_t)(j1 + (rest + 15) / 16);
+    }
     return tp.sm.total <= 220 * 1024 ? 1 : 0;
 }
 
@@ -1007,6 +1074,11 @@ int launch_fill_tiles_batch_r(const InstDesc* descs, const TilePlan* tps, const 
     // for it in the batch kernels)
     // (split tails only for a single table run as jobs, never for batches)
     const bool split = walk && proto.comm && proto.split;
+    if (RPW == 1 && proto.j1 != INT32_MAX) {  // mixed widths: single tables, staged programs
+        if (proto.stream || split || !proto.comm) return 3;
+        return walk && walk->walk ? go(fill_tiles_batch<1, true, false, false, true, false, true>)
+                                  : go(fill_tiles_batch<1, true, false, false, false, false, true>);
+    }
     if (walk && walk->walk) {
         if (proto.stream)
             return proto.comm ? go(fill_tiles_batch<RPW, true, false, true, true, false>)

@@ -210,3 +210,33 @@ def test_chain_length_1024_vs_reference(orc, kernel):
         check_table(*t.download(), g)
         t._host = None
         check_walks(t, menu, g, orc)
+
+
+@pytest.mark.parametrize("kernel", ["persistent", "queue"])
+def test_chain_length_1024_m256_vs_reference(orc, kernel):
+    """The config-5 chain length (L=1024, B=64) at M=256 against the unmodified
+    reference (20 min of its CPU; tests/golden/gen_golden_large.py l1024m256):
+    whole table by diagonal digests, top row, walks and replayed peaks, on the
+    budget-tile kernel (streamed programs) and on the row-segment queue -- the
+    kernel a config-5 shard too large for 32-bit tile offsets runs."""
+    g = _load("l1024m256")
+    menu = synthetic_menu(g["L"], g["B"], g["M"], g["seed"])
+    with rotor.DpTable(menu, 1, g["M"], kernel=kernel) as t:
+        check_table(*t.download(), g)
+        t._host = None
+        check_walks(t, menu, g, orc)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_chain_length_1024_m256_budget_shards_vs_reference(n):
+    """L=1024 split along the budget axis into n shards (halo pushed in the
+    fill kernel): every shard's columns and the cross-shard walk against the
+    reference."""
+    g = _load("l1024m256")
+    L, M = g["L"], g["M"]
+    menu = synthetic_menu(L, g["B"], M, g["seed"])
+    with rotor.ShardedTable(menu, 1, M, n) as sh:
+        check_table(*sh.download(), g)
+        for w in g["walks"]:
+            if w["s"] == 0 and w["t"] == L - 1 and w["status"] == 0:
+                assert ops_digest(sh.backtrack(0, L - 1, w["m"])) == w["ops_digest"]

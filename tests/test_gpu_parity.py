@@ -412,6 +412,23 @@ def test_tiles_without_communication_warp(orc, rows):
             assert bst == 0 and t.backtrack_fetch() == ref_ops
 
 
+@pytest.mark.parametrize("L, B, M, seed", [(12, 6, 200, 7), (33, 16, 1500, 44), (9, 5, 40, 3),
+                                          (40, 8, 3000, 12)])
+def test_tiles_as_mixed_width_jobs(orc, L, B, M, seed):
+    """Tile jobs whose later tiles are 16-slot (two rows per warp) after
+    32-slot ones -- the plan config 3 runs to even out its last wave, forced
+    here at half the tiles: whole table and the fused walk against the oracle."""
+    menu = synthetic_menu(L, B, M, seed, tie_stress=True)
+    st, o, k, v, _, _ = orc.fill(menu, 1, M)
+    with rotor.tuning("jobs", "mixed"), rotor.DpTable(menu, 1, M, kernel="tiles") as t:
+        assert_same(t.download(), (o, k, v))
+        for m in (M, M // 2, M // 5):
+            t.refill_walk(0, L - 1, m)
+            bst, ref_ops = orc.build_schedule(menu, 1, M, (o, k, v), 0, L - 1, m)
+            assert _walk_or_inf(t.backtrack_fetch) == (ref_ops if bst == 0 else "infeasible")
+        assert_same(t.download(), (o, k, v))
+
+
 @pytest.mark.parametrize("rows", [1, 2])
 @pytest.mark.parametrize("comm", ["comm_on", "comm_off"])
 def test_tiles_as_jobs(orc, comm, rows):

@@ -318,6 +318,13 @@ rkr_status rkr_shard_export(const rkr_table* shard, void* ipc_handle, int64_t* i
 rkr_status rkr_shard_link(rkr_table* shard, const void* next_ipc_handle, const int64_t* next_info);
 rkr_status rkr_shard_zero(rkr_table* shard);
 rkr_status rkr_shard_launch(rkr_table* shard);
+/* The walk mirror (optional, before the fill): shard 0 allocates a full-width
+ * copy of the arg table (m_max = the table's global m_max) and exports it;
+ * every other shard attaches it, and from then on each fill also stores its
+ * codes there (peer stores), so rkr_shard_backtrack on shard 0 reads only
+ * local memory instead of one NVLink round trip per hop.  info: 8 int64. */
+rkr_status rkr_shard_mirror(rkr_table* shard0, int32_t m_max, void* ipc_handle, int64_t* info);
+rkr_status rkr_shard_attach_mirror(rkr_table* shard, const void* ipc_handle, const int64_t* info);
 rkr_status rkr_shard_backtrack(rkr_table* shard0, int32_t n_shards, const void* const* ipc_handles,
                                const int64_t* infos, int32_t s, int32_t t, int32_t m, rkr_op* ops,
                                int64_t cap, int64_t* n_ops);

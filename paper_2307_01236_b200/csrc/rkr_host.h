@@ -212,6 +212,15 @@ struct rkr_table {
     bool ipc = false;             // block from cudaMalloc (multi-process shard)
     int32_t shard_lo = 0, shard_hi = 0;
     std::vector<void*> ipc_open;  // peer blocks opened with cudaIpcOpenMemHandle
+    // process shards: shard 0's walk mirror (owned: cudaMalloc, IPC-exported)
+    // and the cross-shard walk's cached views and scratch
+    uint16_t* mirror = nullptr;
+    int64_t mirror_sa = 0;
+    int32_t mirror_M = -1;        // last global budget slot
+    std::vector<unsigned char> walk_key;  // the handles the cached views were opened from
+    void* walk_scratch = nullptr; // ShardView[n] | out[8] | stack | ops[cap]
+    int64_t walk_cap = 0;
+    int32_t walk_n = 0;
     InstDesc* ddesc = nullptr;    // device copy (single-table fills)
     LaunchPlan lplan{};           // single-table launch order (device pointers)
 

@@ -133,6 +133,12 @@ struct InstDesc {
     int32_t* halo;
     int32_t halo_need;
     int32_t next_peer;  // 1: next shard lives on another GPU (system-scope fences)
+    // Walk mirror (process shards): every tile also stores its arg codes into
+    // shard 0's full-width copy (peer memory), so the walk runs on one GPU
+    // with local reads instead of one NVLink round trip per hop.
+    uint16_t* arg_mirror;
+    int64_t mirror_sa;
+    int32_t mirror_base;  // global slot of this shard's local slot 0
 };
 // The launch-wide item order: entry e covers items [start[e], start[e] +
 // L_inst - k[e]) = rows s = 0.. of (instance inst[e], diagonal k[e], tile

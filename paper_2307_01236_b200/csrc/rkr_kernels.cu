@@ -287,7 +287,8 @@ __global__ void walk_sharded(const ShardView* __restrict__ sv, int n_shards, Dev
             while (q + 1 < n_shards && mm >= sv[q + 1].lo) ++q;
             const ShardView& v = sv[q];
             const int64_t rid = row_id(L, s, t);
-            inf = static_cast<const V*>(v.opt)[rid * v.sr + v.pad + (mm - v.lo)] >= Cost<V>::inf;
+            // one read per hop: a cell's code is 0 exactly when its value is
+            // infinite (rkr_walk.cuh), so the owner's opt row is not read
             code = v.arg[rid * v.sa + (mm - v.lo)];
         }
         if (inf || code == 0) {

@@ -576,6 +576,8 @@ __global__ void __launch_bounds__(NT, MINB) fill_persistent(const InstDesc* __re
         const int W = M + 1;
         const bool feeds_next = D.next_opt != nullptr && m0 + pl.TM > W - g.pad && m0 < W;
         V* nrow = feeds_next ? static_cast<V*>(D.next_opt) + rid * D.next_sr + g.pad - W : nullptr;
+        // shard 0's walk mirror (process shards; peer memory)
+        uint16_t* mrow = D.arg_mirror ? D.arg_mirror + rid * D.mirror_sa + D.mirror_base : nullptr;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int m = mb + NT * r;
@@ -583,6 +585,7 @@ __global__ void __launch_bounds__(NT, MINB) fill_persistent(const InstDesc* __re
                 orow[m] = best[r];
                 arow[m] = code[r];
                 if (feeds_next && m >= W - g.pad) nrow[m] = best[r];
+                if (mrow) mrow[m] = code[r];
             }
         }
         __syncthreads();

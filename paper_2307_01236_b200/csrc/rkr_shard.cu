@@ -511,42 +511,112 @@ rkr_status rkr_shard_launch(rkr_table* t) {
     return RKR_OK;
 }
 
+rkr_status rkr_shard_mirror(rkr_table* t0, int32_t m_max, void* ipc_handle, int64_t* info) {
+    if (!t0 || !ipc_handle || !info) return fail(RKR_ERR_ARGUMENT, "null argument");
+    if (!t0->ipc || t0->shard_lo != 0) return fail(RKR_ERR_ARGUMENT, "not shard 0 of rkr_shard_create");
+    if (m_max < t0->shard_hi - 1) return fail(RKR_ERR_ARGUMENT, "m_max below shard 0's range");
+    DeviceGuard dg(t0->device);
+    if (!t0->mirror) {
+        const int64_t sa = round_up((int64_t)m_max + 1, 64);
+        CK(cudaMalloc(reinterpret_cast<void**>(&t0->mirror), (size_t)t0->g.rows * sa * 2));
+        t0->mirror_sa = sa;
+        t0->mirror_M = m_max;
+        t0->hdesc.arg_mirror = t0->mirror;
+        t0->hdesc.mirror_sa = sa;
+        t0->hdesc.mirror_base = 0;
+        CK(cudaMemcpyAsync(t0->ddesc, &t0->hdesc, sizeof(InstDesc), cudaMemcpyHostToDevice, t0->stream));
+        CK(cudaStreamSynchronize(t0->stream));
+    }
+    cudaIpcMemHandle_t hnd;
+    CK(cudaIpcGetMemHandle(&hnd, t0->mirror));
+    std::memcpy(ipc_handle, &hnd, sizeof hnd);
+    info[0] = t0->mirror_sa;
+    info[1] = t0->mirror_M;
+    return RKR_OK;
+}
+
+rkr_status rkr_shard_attach_mirror(rkr_table* t, const void* ipc_handle, const int64_t* info) {
+    if (!t || !ipc_handle || !info) return fail(RKR_ERR_ARGUMENT, "null argument");
+    if (!t->ipc) return fail(RKR_ERR_ARGUMENT, "table was not created by rkr_shard_create");
+    if (t->shard_lo == 0) return RKR_OK;  // shard 0 owns the mirror
+    DeviceGuard dg(t->device);
+    cudaIpcMemHandle_t hnd;
+    std::memcpy(&hnd, ipc_handle, sizeof hnd);
+    void* base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, hnd, cudaIpcMemLazyEnablePeerAccess));
+    t->ipc_open.push_back(base);
+    t->hdesc.arg_mirror = static_cast<uint16_t*>(base);
+    t->hdesc.mirror_sa = info[0];
+    t->hdesc.mirror_base = t->shard_lo;
+    CK(cudaMemcpyAsync(t->ddesc, &t->hdesc, sizeof(InstDesc), cudaMemcpyHostToDevice, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    return RKR_OK;
+}
+
 rkr_status rkr_shard_backtrack(rkr_table* t0, int32_t n, const void* const* ipc_handles,
                                const int64_t* infos, int32_t s, int32_t t, int32_t m, rkr_op* ops,
                                int64_t cap, int64_t* n_ops) {
     if (!t0 || n < 1 || !n_ops || (n > 1 && (!ipc_handles || !infos)))
         return fail(RKR_ERR_ARGUMENT, "null argument");
     DeviceGuard dg(t0->device);
-    std::vector<ShardView> v(n);
     const int32_t m_glob = (int32_t)(n > 1 ? infos[8 * (n - 1) + 7] : t0->shard_hi) - 1;
-    for (int r = 0; r < n; ++r) {
-        const int64_t* in = infos + 8 * r;
-        if (r == 0) {
-            v[0] = ShardView{t0->opt, t0->arg, t0->g.sr, t0->g.sa, t0->g.pad, t0->shard_lo};
-            continue;
-        }
-        cudaIpcMemHandle_t hnd;
-        std::memcpy(&hnd, ipc_handles[r], sizeof hnd);
-        void* base = nullptr;
-        CK(cudaIpcOpenMemHandle(&base, hnd, cudaIpcMemLazyEnablePeerAccess));
-        t0->ipc_open.push_back(base);
-        unsigned char* b = static_cast<unsigned char*>(base);
-        v[r] = ShardView{b + in[0], reinterpret_cast<const uint16_t*>(b + in[3]), in[1], in[4],
-                         (int32_t)in[5], (int32_t)in[6]};
+    // the views: shard 0's walk mirror (every shard stored its codes there:
+    // local reads only), else every shard's rows through its IPC mapping,
+    // opened once and cached with the scratch
+    std::vector<unsigned char> key;
+    for (int r = 1; r < n; ++r) {
+        const unsigned char* h = static_cast<const unsigned char*>(ipc_handles[r]);
+        key.insert(key.end(), h, h + sizeof(cudaIpcMemHandle_t));
     }
-    ShardView* dv = nullptr;
-    int64_t* dout = nullptr;
-    int32_t* dops = nullptr;
-    int4* dstk = nullptr;
+    const bool mirror = t0->mirror && t0->mirror_M == m_glob;
+    const int nv = mirror ? 1 : n;
     const int64_t dcap = std::max<int64_t>(cap, 16);
-    CK(cudaMalloc(reinterpret_cast<void**>(&dv), sizeof(ShardView) * n));
-    CK(cudaMalloc(reinterpret_cast<void**>(&dout), 64));
-    CK(cudaMalloc(reinterpret_cast<void**>(&dops), (size_t)dcap * 12));
-    CK(cudaMalloc(reinterpret_cast<void**>(&dstk), sizeof(int4) * (2 * (size_t)t0->g.L + 16)));
-    CK(cudaMemcpy(dv, v.data(), sizeof(ShardView) * n, cudaMemcpyHostToDevice));
+    if (!t0->walk_scratch || t0->walk_key != key || t0->walk_n != nv || t0->walk_cap < dcap) {
+        std::vector<ShardView> v(nv);
+        if (mirror) {
+            v[0] = ShardView{nullptr, t0->mirror, 0, t0->mirror_sa, 0, 0};
+        } else {
+            for (int r = 0; r < n; ++r) {
+                const int64_t* in = infos + 8 * r;
+                if (r == 0) {
+                    v[0] = ShardView{t0->opt, t0->arg, t0->g.sr, t0->g.sa, t0->g.pad, t0->shard_lo};
+                    continue;
+                }
+                cudaIpcMemHandle_t hnd;
+                std::memcpy(&hnd, ipc_handles[r], sizeof hnd);
+                void* base = nullptr;
+                if (t0->walk_key != key || t0->walk_n != nv) {
+                    CK(cudaIpcOpenMemHandle(&base, hnd, cudaIpcMemLazyEnablePeerAccess));
+                    t0->ipc_open.push_back(base);
+                } else {
+                    base = t0->ipc_open[t0->ipc_open.size() - (n - 1) + (r - 1)];
+                }
+                unsigned char* b = static_cast<unsigned char*>(base);
+                v[r] = ShardView{b + in[0], reinterpret_cast<const uint16_t*>(b + in[3]), in[1], in[4],
+                                 (int32_t)in[5], (int32_t)in[6]};
+            }
+        }
+        if (t0->walk_scratch) {
+            cudaStreamSynchronize(t0->stream);
+            cudaFree(t0->walk_scratch);
+            t0->walk_scratch = nullptr;
+        }
+        const size_t stk = sizeof(int4) * (2 * (size_t)t0->g.L + 16);
+        const size_t bytes = 256 + sizeof(ShardView) * nv + 64 + stk + (size_t)dcap * 12;
+        CK(cudaMalloc(&t0->walk_scratch, bytes));
+        CK(cudaMemcpy(t0->walk_scratch, v.data(), sizeof(ShardView) * nv, cudaMemcpyHostToDevice));
+        t0->walk_key = key;
+        t0->walk_n = nv;
+        t0->walk_cap = dcap;
+    }
+    unsigned char* sp = static_cast<unsigned char*>(t0->walk_scratch);
+    const ShardView* dv = reinterpret_cast<const ShardView*>(sp);
+    int64_t* dout = reinterpret_cast<int64_t*>(sp + ((sizeof(ShardView) * nv + 255) & ~(size_t)255));
+    int4* dstk = reinterpret_cast<int4*>(dout + 8);
+    int32_t* dops = reinterpret_cast<int32_t*>(dstk + 2 * (size_t)t0->g.L + 16);
     rkr_status st = RKR_OK;
-    if (launch_walk_sharded(dv, n, t0->dm, t0->g.L, m_glob, t0->width, s, t, m,
-                            dops, dcap, reinterpret_cast<int32_t*>(dstk), dout, t0->stream))
+    if (launch_walk_sharded(dv, nv, t0->dm, t0->g.L, m_glob, t0->width, s, t, m, dops, t0->walk_cap,
+                            reinterpret_cast<int32_t*>(dstk), dout, t0->stream))
         st = cuda_fail(cudaGetLastError(), "shard walk launch");
     int64_t res[4] = {0, 0, -1, -1};
     if (st == RKR_OK) {
@@ -556,10 +626,6 @@ rkr_status rkr_shard_backtrack(rkr_table* t0, int32_t n, const void* const* ipc_
             e = cudaMemcpy(ops, dops, (size_t)std::min(res[0], cap) * 12, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) st = cuda_fail(e, "shard walk copy");
     }
-    cudaFree(dv);
-    cudaFree(dout);
-    cudaFree(dops);
-    cudaFree(dstk);
     if (st) return st;
     *n_ops = res[0];
     if (res[1] == 2)

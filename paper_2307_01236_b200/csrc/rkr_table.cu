@@ -190,6 +190,11 @@ void free_table(rkr_table* t) {
     }
     if (t->block && t->owns_block) cudaFreeAsync(t->block, t->stream);
     if (t->wrec) cudaFreeAsync(t->wrec, t->stream);
+    if (t->mirror || t->walk_scratch) {
+        cudaStreamSynchronize(t->stream);
+        if (t->mirror) cudaFree(t->mirror);
+        if (t->walk_scratch) cudaFree(t->walk_scratch);
+    }
     delete t;
 }
 

@@ -688,6 +688,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             } else if (h == -1 && m <= M && valid) {  // store (chain_dp.hpp:176-177)
                 opt[(int64_t)rid * sr + g.pad + m] = best;
                 arg[(int64_t)rid * g.sa + m] = (uint16_t)code;
+                if (HALO && D.arg_mirror)  // shard 0's walk mirror (peer store)
+                    D.arg_mirror[(int64_t)rid * D.mirror_sa + D.mirror_base + m] = (uint16_t)code;
                 if (halo_out && m >= Wl - g.pad)  // the next shard's halo slot m - Wl
                     static_cast<uint32_t*>(D.next_opt)[(int64_t)rid * D.next_sr + g.pad + (m - Wl)] = best;
             } else if (h == 0) {

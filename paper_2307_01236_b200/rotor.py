@@ -147,6 +147,8 @@ def lib() -> ctypes.CDLL:
     L.rkr_shard_range.argtypes = [p, P(i32), P(i32)]
     L.rkr_shard_export.argtypes = [p, p, P(i64)]
     L.rkr_shard_link.argtypes = [p, p, P(i64)]
+    L.rkr_shard_mirror.argtypes = [p, i32, p, P(i64)]
+    L.rkr_shard_attach_mirror.argtypes = [p, p, P(i64)]
     L.rkr_shard_zero.argtypes = [p]
     L.rkr_shard_launch.argtypes = [p]
     L.rkr_shard_backtrack.argtypes = [p, i32, P(p), P(i64), i32, i32, i32, P(RkrOp), i64, P(i64)]
@@ -796,6 +798,18 @@ class ProcessShard:
         _check(self._lib.rkr_shard_export(self._h, hnd, info))
         return hnd.raw, list(info)
 
+    def mirror(self) -> Tuple[bytes, List[int]]:
+        """Shard 0: allocate and export the walk mirror (rkr_shard_mirror)."""
+        hnd = ctypes.create_string_buffer(64)
+        info = (ctypes.c_int64 * 8)()
+        _check(self._lib.rkr_shard_mirror(self._h, self.M, hnd, info))
+        return hnd.raw, list(info)
+
+    def attach_mirror(self, handle: bytes, info: Sequence[int]) -> None:
+        hnd = ctypes.create_string_buffer(handle, 64)
+        inf = (ctypes.c_int64 * 8)(*info)
+        _check(self._lib.rkr_shard_attach_mirror(self._h, hnd, inf))
+
     def link(self, next_handle: bytes, next_info: Sequence[int]) -> None:
         hnd = ctypes.create_string_buffer(next_handle, 64)
         info = (ctypes.c_int64 * 8)(*next_info)
@@ -840,13 +854,20 @@ class ProcessShard:
             pass
 
 
-def link_process_shards(shard: "ProcessShard", all_gather) -> Tuple[List[bytes], List[List[int]]]:
+def link_process_shards(shard: "ProcessShard", all_gather,
+                        mirror: bool = True) -> Tuple[List[bytes], List[List[int]]]:
     """Exchange IPC handles with every rank (all_gather: obj -> list of objs)
-    and link this shard to the next one.  Returns all handles and infos."""
+    and link this shard to the next one; with `mirror`, shard 0's walk mirror
+    is shared too, so the cross-shard walk reads local memory only.  Returns
+    all handles and infos."""
     mine = shard.export()
     everyone = all_gather(mine)
     if shard.rank + 1 < shard.n:
         shard.link(*everyone[shard.rank + 1])
+    if mirror and shard.n > 1:
+        m0 = all_gather(shard.mirror() if shard.rank == 0 else None)[0]
+        if shard.rank != 0:
+            shard.attach_mirror(*m0)
     return [e[0] for e in everyone], [e[1] for e in everyone]
 
 

@@ -50,3 +50,15 @@ for kernel in ("persistent", "queue"):  # tile jobs / row-segment queue
 rotor.sweep_raw(synthetic_menu(12, 4, 500, 8, byte_scale=64), [3000, 20000, 60000], 500)
 rotor.solve_chain(rotor.Chain.skeleton(2), tiny_chain_menu(), 16, 16)
 print("sanitize workload done")
+# round 2: mixed-width tile jobs, the caller's-menu walk, the min-feasible
+# threshold kernel (an infeasible solve and an infeasible sweep budget)
+with rotor.tuning("jobs", "mixed"), rotor.DpTable(synthetic_menu(21, 6, 700, 4), 1, 700,
+                                                   kernel="tiles") as t:
+    t.refill_walk(0, 20, 700)
+    t.backtrack_fetch()
+    t.backtrack(0, 20, 700, menu=synthetic_menu(21, 6, 700, 4))
+try:
+    rotor.solve_chain(rotor.Chain.skeleton(2), tiny_chain_menu(), 12, 12)
+except rotor.InfeasibleBudget:
+    pass
+rotor.sweep_raw(synthetic_menu(9, 4, 300, 3, byte_scale=64), [50, 400, 3000, 20000], 300)

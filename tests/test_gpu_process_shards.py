@@ -30,7 +30,7 @@ WORKER = textwrap.dedent(r"""
         out = [None] * world
         dist.all_gather_object(out, obj)
         return out
-    handles, infos = rotor.link_process_shards(sh, gather)
+    handles, infos = rotor.link_process_shards(sh, gather, mirror=os.environ["MIRROR"] == "1")
     lo, hi = sh.range()
     st, o, k, v, _, _ = Orc().fill(menu, 1, M)
     ok = True
@@ -64,14 +64,18 @@ def _port():
     return p
 
 
-def test_two_process_shards_one_gpu(tmp_path):
+@pytest.mark.parametrize("mirror", ["1", "0"])
+def test_two_process_shards_one_gpu(tmp_path, mirror):
+    """mirror=1: every shard also stores its codes into shard 0's walk mirror
+    and the walk reads only that; mirror=0: the walk reads each shard's rows
+    through its IPC mapping."""
     script = tmp_path / "worker.py"
     script.write_text(WORKER)
     port = _port()
     procs = []
     for r in range(2):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port), REPO=ROOT)
+                   MASTER_PORT=str(port), REPO=ROOT, MIRROR=mirror)
         procs.append(subprocess.Popen([sys.executable, str(script)], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
                                       start_new_session=True))

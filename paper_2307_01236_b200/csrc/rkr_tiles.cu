@@ -60,6 +60,7 @@ constexpr uint32_t INF = kInf32;  // K1t runs the 32-bit cost path only
 #define RKR_EXP_DYNUNIT 0
 #endif
 
+
 __device__ __forceinline__ int t_ld_relaxed(const int* p) {
     int v;
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -207,6 +208,21 @@ __device__ __forceinline__ void stage_step(const TilePlan& tp, const ProgDev& pq
     bulk_g2s(smem + sm.thr + b * sm.thr_bytes, pq.thr + diag_off(L, k) * tp.ocap, tb, bars + b);
 }
 
+// Tail reads (the option windows of row (s+1, t) and the two tail cuts) go
+// through L1: the windows of one row at the options' pack shifts overlap
+// (config 3: 32 windows over ~10 lines), so most of them hit instead of
+// paying an L2 round trip each, and the tail is a chain of dependent
+// batches.  Coherent: every row is read only after the step that wrote it,
+// its line holds no other row, and the acquisition of the lower tiles'
+// diagonal k-1 before each tail (ld.acquire -> CCTL.IVALL) empties L1 of
+// anything older; the bulk's reads, which never repeat, stay L2-only.
+#ifndef RKR_TAIL_L1
+#define RKR_TAIL_L1 1
+#endif
+__device__ __forceinline__ uint32_t tail_ld(const uint32_t* p) {
+    return RKR_TAIL_L1 ? __ldca(p) : __ldcg(p);
+}
+
 // The lane's table base opt + m as an opaque 64-bit register, so that a
 // table address is ONE IMAD.WIDE.U32 (entry offset x 4 + base) instead of
 // the compiler's re-associated 64-bit (m + offset) sum (four instructions).
@@ -251,10 +267,13 @@ __device__ __forceinline__ bool scan_cuts(const uint32_t* __restrict__ opt, cons
         }
         if (RPW == 1 ? e[kU - 1].w <= m0 : __all_sync(0xffffffffu, e[kU - 1].w <= m)) {
             // (warp-uniform) no lane gated in this batch
+            uint32_t tot[kU];
+#pragma unroll
+            for (int q = 0; q < kU; ++q) tot[q] = (uint32_t)e[q].z + lv[q] + rv[q];
 #pragma unroll
             for (int q = 0; q < kU; ++q) {
                 bool keep;
-                best = __vibmin_u32(best, (uint32_t)e[q].z + lv[q] + rv[q], &keep);
+                best = __vibmin_u32(best, tot[q], &keep);
                 if (!keep) code = cb + i0 + q;  // strictly smaller: the scan's first minimum
             }
             continue;
@@ -410,6 +429,9 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 const int* row = done + (int64_t)(k - 1) * tp.T;
                 for (int q = lane; q < d_eff; q += 32)
                     while (t_ld_acquire(row + j - 1 - q) == 0) __nanosleep(20);
+                // (tile 0 polls nothing: its own flag, for the L1 invalidation
+                // the tail's cached reads rely on)
+                if (d_eff == 0 && lane == 0) (void)t_ld_acquire(row + j);
                 if (halo_in && lane == 0) wait_halo(k - 1);
                 __syncwarp();
             }
@@ -574,12 +596,12 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             int4 e0 = make_int4(0, 0, 0, M + 2), e1 = e0;
             if (k > 0 && cuts) {
                 e0 = STREAM ? __ldg(prog + s * k) : prog[s * k];
-                tl0 = __ldcg(opt + (uint32_t)(e0.x + m));
-                tr0 = __ldcg(opt + (uint32_t)(e0.y + m));
+                tl0 = tail_ld(opt + (uint32_t)(e0.x + m));
+                tr0 = tail_ld(opt + (uint32_t)(e0.y + m));
                 if (k > 1) {
                     e1 = STREAM ? __ldg(prog + s * k + k - 1) : prog[s * k + k - 1];
-                    tl1 = __ldcg(opt + (uint32_t)(e1.x + m));
-                    tr1 = __ldcg(opt + (uint32_t)(e1.y + m));
+                    tl1 = tail_ld(opt + (uint32_t)(e1.x + m));
+                    tr1 = tail_ld(opt + (uint32_t)(e1.y + m));
                 }
             }
             uint32_t best = INF;
@@ -629,8 +651,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                         const int4 o2 = od4[(i0 + q) >> 1];
                         ot[q] = (uint32_t)o2.y;
                         ot[q + 1] = (uint32_t)o2.w;
-                        sub[q] = SUB ? __ldcg(optw + o2.x) : 0u;
-                        sub[q + 1] = SUB ? __ldcg(optw + o2.z) : 0u;
+                        sub[q] = SUB ? tail_ld(optw + o2.x) : 0u;
+                        sub[q + 1] = SUB ? tail_ld(optw + o2.z) : 0u;
                     }
 #pragma unroll
                     for (int q = 0; q < kOB; q += 4) {

@@ -76,6 +76,18 @@ def test_cpp_header_compiles():
                    check=True)
 
 
+def test_standalone_headers_compile(tmp_path):
+    """Without the reference tree on the include path, the drop-in headers
+    (remat/chain_dp.hpp, remat/simulate.hpp) and the gate fall back to the
+    standalone vocabulary in include/remat_b200/ and still compile."""
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "remat_b200/chain_dp.hpp"\n#include "remat_b200/gate.hpp"\n'
+                   "int main() { remat::CDGraph g; auto c = remat::single_block_chain(g);"
+                   " (void)c; return 0; }\n")
+    subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), str(src)],
+                   check=True)
+
+
 def test_cpp_test_binary_links():
     from paper_2307_01236_b200.build import build_cpp_tests
 

@@ -197,7 +197,7 @@ size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p);  // coun
 // of kTileOptBatch: thr rows and option slots are padded to a multiple.
 constexpr int kTileOptBatch = 8;  // 16 measured: config 2 -2%, configs 1 and 3 +8-12%
 struct TileSmem {  // shared-memory carve-up of K1t (byte offsets)
-    uint32_t best, code, blk, split, opd, prog, thr, xch, bar, total;
+    uint32_t best, code, blk, split, thx, opd, prog, thr, xch, bar, total;
     uint32_t prog_bytes, thr_bytes;  // one buffer of each (two of each are kept)
 };
 struct TilePlan {
@@ -285,7 +285,8 @@ int launch_export(const LaunchCtx& c, int64_t r0, int64_t r1, int64_t* opt, int8
 // scheme).  The call is skipped when the limit already covers the request
 // (it costs host time on every launch otherwise).
 inline cudaError_t set_dyn_smem(const void* kern, size_t smem) {
-    if (smem <= 48 * 1024) return cudaSuccess;
+    // (no "<= 48 KB needs nothing" shortcut: the default limit covers
+    // dynamic + static shared memory, so 48 KB of dynamic alone can exceed it)
     int dev = 0;
     cudaGetDevice(&dev);
     static std::mutex mu;

@@ -424,7 +424,7 @@ int fill_all_t(const LaunchCtx& c) {
         fill_diag<V, NT, R><<<grid, NT, cell_smem_bytes<V>(k, c.max_opts), st>>>(
             c.g, c.dm, opt, c.arg, k);
     }
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 }  // namespace
@@ -439,7 +439,7 @@ int launch_init_pads(const LaunchCtx& c) {
         init_pads<uint32_t><<<blocks, 256, 0, st>>>(c.g, static_cast<uint32_t*>(c.opt));
     else
         init_pads<int64_t><<<blocks, 256, 0, st>>>(c.g, static_cast<int64_t*>(c.opt));
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 int launch_fill_all(const LaunchCtx& c) {
@@ -463,7 +463,7 @@ int launch_backtrack(const LaunchCtx& c, int32_t s, int32_t t, int32_t m, int32_
         backtrack<int64_t><<<1, 128, dyn, st>>>(c.g, c.dm, static_cast<const int64_t*>(c.opt),
                                                 c.arg, s, t, m, dev_ops, cap, stk, dev_out,
                                                 use_smem, nq);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 int launch_batch_walk(const InstDesc* d, const int32_t* m_at, const uint8_t* active, int n,
@@ -474,7 +474,7 @@ int launch_batch_walk(const InstDesc* d, const int32_t* m_at, const uint8_t* act
         batch_walk<uint32_t><<<blocks, 32, 0, st>>>(d, m_at, active, n, ops, cap, out);
     else
         batch_walk<int64_t><<<blocks, 32, 0, st>>>(d, m_at, active, n, ops, cap, out);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 int launch_walk_sharded(const ShardView* sv, int n, const DevMenu& dm, int L, int M, int width,
@@ -486,7 +486,7 @@ int launch_walk_sharded(const ShardView* sv, int n, const DevMenu& dm, int L, in
         walk_sharded<uint32_t><<<1, 32, 0, st>>>(sv, n, dm, L, M, s, t, m, ops, cap, stk, out);
     else
         walk_sharded<int64_t><<<1, 32, 0, st>>>(sv, n, dm, L, M, s, t, m, ops, cap, stk, out);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 int launch_batch_tops(const InstDesc* d, const int32_t* m_at, int n, int width, int64_t* out,
@@ -497,7 +497,7 @@ int launch_batch_tops(const InstDesc* d, const int32_t* m_at, int n, int width, 
         batch_tops<uint32_t><<<blocks, 128, 0, st>>>(d, m_at, n, out);
     else
         batch_tops<int64_t><<<blocks, 128, 0, st>>>(d, m_at, n, out);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 // solve_chain's min-feasible search (chain_dp.hpp:265-288) without the wide
@@ -559,7 +559,7 @@ int launch_batch_thresholds(const InstDesc* d, const int32_t* which, int n, int6
     if (n <= 0) return 0;
     batch_thresholds<<<n, 128, 0, static_cast<cudaStream_t>(stream)>>>(d, which, scratch, scr_off,
                                                                       out);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 int launch_batch_first_feasible(const InstDesc* d, int n, int width, int32_t* out, void* stream) {
@@ -568,7 +568,7 @@ int launch_batch_first_feasible(const InstDesc* d, int n, int width, int32_t* ou
         batch_first_feasible<uint32_t><<<n, 256, 0, st>>>(d, n, out);
     else
         batch_first_feasible<int64_t><<<n, 256, 0, st>>>(d, n, out);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 int launch_first_feasible(const LaunchCtx& c, int32_t s, int32_t t, int32_t* dev_m) {
@@ -581,7 +581,7 @@ int launch_first_feasible(const LaunchCtx& c, int32_t s, int32_t t, int32_t* dev
     else
         first_feasible<int64_t><<<blocks, 256, 0, st>>>(
             c.g, static_cast<const int64_t*>(c.opt), s, t, dev_m);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 int launch_export(const LaunchCtx& c, int64_t r0, int64_t r1, int64_t* o, int8_t* kd,
@@ -597,7 +597,7 @@ int launch_export(const LaunchCtx& c, int64_t r0, int64_t r1, int64_t* o, int8_t
     else
         export_rows<int64_t><<<grid, 256, 0, st>>>(
             c.g, c.dm, static_cast<const int64_t*>(c.opt), c.arg, r0, o, kd, val);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 }  // namespace rkr

@@ -641,7 +641,7 @@ int launch_t(const InstDesc* dev_desc, const InstDesc& d0, const LaunchPlan& lp,
     if (grid > lp.total) grid = lp.total;
     if (grid < 1) return 0;
     kern<<<(unsigned)grid, NT, smem, st>>>(dev_desc, d0, lp, counter, c);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 template <typename V>
@@ -671,7 +671,7 @@ int prep_t(const LaunchCtx& cx) {
         cx.g, cx.dm, static_cast<const V*>(cx.opt), host_programs_of<V>(cx),
         reinterpret_cast<uint32_t*>(cx.plan.counter),
         cx.prep_zero ? (int64_t)(cx.state_bytes / 4) : 0);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 }  // namespace
@@ -735,7 +735,7 @@ int launch_prep_programs_batch(const InstDesc* d, int n, int64_t max_rows, int w
         prep_programs_batch<uint32_t><<<grid, 128, 0, st>>>(d);
     else
         prep_programs_batch<int64_t><<<grid, 128, 0, st>>>(d);
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
 }
 
 int launch_fill_batch(const InstDesc* dev_desc, const InstDesc* single, const LaunchPlan& lp,

@@ -169,6 +169,8 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     b = al16(b + (L + 2) * 4);  // block option offsets [L+1] + the last-CTA flag
     m.split = (uint32_t)b;      // per step: bulk parts and cuts per part; 2 unit counters
     b = al16(b + L * 8 + 8);
+    m.thx = (uint32_t)b;  // per block: the terms of its largest option threshold
+    b = al16(b + (tp.stream ? 0 : L * 12));
     m.opd = (uint32_t)b;
     if (tp.stream) {  // programs, thresholds and options from global memory;
         // per-warp program slices for the bulk
@@ -230,6 +232,29 @@ __device__ __forceinline__ const uint32_t* lane_base(const uint32_t* opt, int m)
     const uint32_t* p;
     asm("mov.b64 %0, %1;" : "=l"(p) : "l"(opt + m));
     return p;
+}
+
+// Eight ungated candidates c0 .. c0+7, in scan order, into (best, code) with
+// the scan's strict '<'.  The sequential scan ends on the FIRST candidate
+// holding the batch minimum when that minimum beats best, and changes
+// nothing otherwise -- so: the minimum (three VIMNMX3 + one VIMNMX), one
+// vote, and the position only when some lane improves.  Used for option
+// batches (config 3: -2 %); on cut batches it measured neutral (late in a
+// long scan most batches improve no lane, but the vote and the position
+// search cost what the per-candidate compares save).
+__device__ __forceinline__ void merge8(const uint32_t (&tot)[8], int c0, uint32_t& best, int& code) {
+    const uint32_t x = __vimin3_u32(__vimin3_u32(tot[0], tot[1], tot[2]),
+                                    __vimin3_u32(tot[3], tot[4], tot[5]), min(tot[6], tot[7]));
+    if (__any_sync(0xffffffffu, x < best)) {
+        int qf = 7;
+#pragma unroll
+        for (int q = 6; q >= 0; --q)
+            if (tot[q] == x) qf = q;
+        if (x < best) {
+            best = x;
+            code = c0 + qf;
+        }
+    }
 }
 
 // Cuts i in [ib, ie) of one cell slice, ascending, strict '<' into (best,
@@ -340,7 +365,13 @@ __device__ __forceinline__ void scan_cuts_streamed(const uint32_t* __restrict__ 
 // SMs instead of 64.  A unit is one warp's (row group, slots) share of a
 // step; rows past the diagonal's last (an odd row count) are computed from a
 // clamped row and not stored.
-template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool TABLE, bool HALO>
+//
+// OM (the plain single tables run as mixed-width jobs -- config 3): option
+// batches whose thresholds no lane is below go ungated through merge8, and
+// the padding of the last batch is not scanned (config 3 -2 %; configs 1, 2
+// and 4 measured 3-7 % slower with it: their short option scans and low
+// budgets gain nothing and pay the extra latency).
+template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool TABLE, bool HALO, bool OM = false>
 __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, const int j,
                                          unsigned char* smem_raw, uint32_t ph0, uint32_t ph1) {
     constexpr int W = 32 / RPW;
@@ -368,6 +399,23 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     // time INF).  Cut programs and thresholds arrive per step by bulk copy,
     // two steps ahead (double buffer, one mbarrier per buffer).
     for (int c = tid; c <= L; c += kNT) s_blk[c] = __ldg(dm.blk_off + c);
+    // (OM) the terms of the largest option threshold of row (s, t), k > 0
+    // (chain_dp.hpp:141-147, local slots): max(F[s] + seed[t], B[s]) with
+    // F = max fwd_req, B = max(bwd_req, pack_chg) over block s's options and
+    // seed[t] = 2 act_u[t+1] (t < L-1), each clamped to +-2^29
+    int32_t* s_thx = reinterpret_cast<int32_t*>(smem_raw + sm.thx);
+    for (int b = tid; OM && !STREAM && b < L; b += kNT) {
+        constexpr int64_t kC = 1ll << 29;
+        int64_t f = -kC, bp = -kC;
+        for (int o = __ldg(dm.blk_off + b); o < __ldg(dm.blk_off + b + 1); ++o) {
+            f = max(f, __ldg(dm.fwd_req + o) - g.m_base);
+            bp = max(bp, max(__ldg(dm.bwd_req + o), __ldg(dm.pack_chg + o)) - g.m_base);
+        }
+        const int64_t sd = b < L - 1 ? 2 * __ldg(dm.act_u + b + 1) : 0;
+        s_thx[b] = (int32_t)min(max(f, -kC), kC);
+        s_thx[L + b] = (int32_t)min(max(bp, -kC), kC);
+        s_thx[2 * L + b] = (int32_t)min(sd, kC);
+    }
     // per step: bulk parts P and cuts per part (late diagonals split the
     // cut range over warps; >= 8 cuts per part)
     int2* s_split = reinterpret_cast<int2*>(smem_raw + sm.split);
@@ -636,24 +684,43 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             // no sub-row (chain_dp.hpp:146: s == t), so its loop is a separate
             // instantiation without loads; otherwise each window read is one
             // IMAD.WIDE off the lane's row base (shifts stored negated).
+            // (OM) no option threshold of the row is above the warp's
+            // smallest budget m_lo: the batches run ungated through merge8
+            bool open = false;
+            if constexpr (OM && !STREAM) {
+                const int32_t thx = max(s_thx[s] + s_thx[2 * L + s + k], s_thx[L + s]);
+                open = __all_sync(0xffffffffu, thx <= m_lo);
+            }
             auto options = [&](auto has_sub) {
                 constexpr bool SUB = decltype(has_sub)::value;
                 const uint32_t* __restrict__ optw =
                     lane_base(opt, SUB ? (rid - (L - k)) * sr + g.pad + m : 0);
-                // (software-pipelining the batches -- the next batch's reads
-                // in flight during this batch's compares -- spills inside the
-                // loop at 64 registers per thread)
-                for (int i0 = ia; i0 < ib; i0 += kOB) {
-                    uint32_t sub[kOB], ot[kOB];
-                    int32_t th[kOB];
+                auto sub_at = [&](int neg_shift) -> uint32_t {  // row (s+1, t) at m - shift
+                    return SUB ? tail_ld(optw + neg_shift) : 0u;
+                };
+                // Whole batches [ia, ibf), then (OM) the options past them one
+                // by one: menus of 8n + 1 options (option 0 and the solver's
+                // 8n) scan no padding; the first one's read goes out with the
+                // first batch's.  (Software-pipelining the batches -- the next
+                // batch's reads in flight during this batch's compares --
+                // spills at 64 registers per thread.)
+                const int ibf = OM ? ia + (ib - ia) / kOB * kOB : ib;
+                const int2* od2 = reinterpret_cast<const int2*>(od4);
+                const int2 orem = ibf < ib ? od2[ibf] : make_int2(0, 0);
+                const uint32_t srem = ibf < ib ? sub_at(orem.x) : 0u;
+                for (int i0 = ia; i0 < ibf; i0 += kOB) {
+                    uint32_t tot[kOB];
 #pragma unroll
                     for (int q = 0; q < kOB; q += 2) {
                         const int4 o2 = od4[(i0 + q) >> 1];
-                        ot[q] = (uint32_t)o2.y;
-                        ot[q + 1] = (uint32_t)o2.w;
-                        sub[q] = SUB ? tail_ld(optw + o2.x) : 0u;
-                        sub[q + 1] = SUB ? tail_ld(optw + o2.z) : 0u;
+                        tot[q] = (uint32_t)o2.y + sub_at(o2.x);
+                        tot[q + 1] = (uint32_t)o2.w + sub_at(o2.z);
                     }
+                    if (SUB && open) {
+                        merge8(tot, i0 + 1, best, code);
+                        continue;
+                    }
+                    int32_t th[kOB];
 #pragma unroll
                     for (int q = 0; q < kOB; q += 4) {
                         const int4 t4 = th4[(i0 + q) >> 2];
@@ -664,11 +731,20 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                     }
 #pragma unroll
                     for (int q = 0; q < kOB; ++q) {
-                        const uint32_t tot = ot[q] + sub[q];
-                        if (m >= th[q] && tot < best) {
-                            best = tot;
+                        if (m >= th[q] && tot[q] < best) {
+                            best = tot[q];
                             code = i0 + q + 1;
                         }
+                    }
+                }
+                const int32_t* thr_row = reinterpret_cast<const int32_t*>(th4);
+#pragma unroll 1
+                for (int i = ibf; i < ib; ++i) {
+                    const int2 o = i == ibf ? orem : od2[i];
+                    const uint32_t tot = (uint32_t)o.y + (i == ibf ? srem : sub_at(o.x));
+                    if (m >= thr_row[i] && tot < best) {
+                        best = tot;
+                        code = i + 1;
                     }
                 }
             };
@@ -930,11 +1006,11 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
         if (q >= njobs) break;
         const int2 jb = jobs[q];
         if (MIXED && jb.y >= tps[jb.x].j1)  // a half tile of the last wave
-            tile_job<2, COMM, SPLIT, STREAM, false, HALO>(descs[jb.x], tps[jb.x], jb.y, smem_raw, ph0,
-                                                          ph1);
+            tile_job<2, COMM, SPLIT, STREAM, false, HALO, MIXED>(descs[jb.x], tps[jb.x], jb.y, smem_raw,
+                                                                 ph0, ph1);
         else
-            tile_job<RPW, COMM, SPLIT, STREAM, false, HALO>(descs[jb.x], tps[jb.x], jb.y, smem_raw,
-                                                            ph0, ph1);
+            tile_job<RPW, COMM, SPLIT, STREAM, false, HALO, MIXED>(descs[jb.x], tps[jb.x], jb.y, smem_raw,
+                                                                   ph0, ph1);
         const int L = descs[jb.x].g.L;
         ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
         ph1 += (uint32_t)L / 2;
@@ -1087,7 +1163,7 @@ int launch_fill_tiles_batch_r(const InstDesc* descs, const TilePlan* tps, const 
         TilePlan wp{};
         if (walk) wp = *walk;  // a single table's plan with its walk request
         kern<<<grid, kNT, smem, st>>>(descs, tps, jobs, njobs, counter, wp);
-        return cudaGetLastError() == cudaSuccess ? 0 : 3;
+        return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;  // (the caller reports it)
     };
     if (proto.halo) {  // budget shards: communication warp, no split tails, no walk
         if (!proto.comm || proto.split || (walk && walk->walk)) return 3;

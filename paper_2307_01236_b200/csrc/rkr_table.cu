@@ -77,7 +77,11 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
         // id first, without stable_sort's allocation)
         const int32_t o_lo = m->option_offsets[i], o_hi = m->option_offsets[i + 1];
         const bool small = o_hi - o_lo <= 32;
+        bool ascending = true;  // ids strictly ascending (the usual menu): every id is first
+        for (int32_t o = o_lo + 1; o < o_hi && ascending; ++o)
+            ascending = m->option_id[o - 1] < m->option_id[o];
         auto first_pos = [&](int32_t o) {
+            if (ascending) return o;
             if (small) {
                 for (int32_t q = o_lo; q < o; ++q)
                     if (m->option_id[q] == m->option_id[o]) return q;
@@ -86,7 +90,7 @@ rkr_status build_host_menu(const rkr_menu* m, int64_t unit, HostMenu& h) {
             return std::lower_bound(first.begin(), first.end(),
                                     std::make_pair(m->option_id[o], INT32_MIN))->second;
         };
-        if (!small) {
+        if (!small && !ascending) {
             first.clear();
             for (int32_t o = o_lo; o < o_hi; ++o) first.emplace_back(m->option_id[o], o);
             std::sort(first.begin(), first.end());

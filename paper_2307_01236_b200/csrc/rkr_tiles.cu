@@ -170,7 +170,7 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     m.split = (uint32_t)b;      // per step: bulk parts and cuts per part; 2 unit counters
     b = al16(b + L * 8 + 8);
     m.thx = (uint32_t)b;  // per block: the terms of its largest option threshold
-    b = al16(b + (tp.stream ? 0 : L * 12));
+    b = al16(b + (tp.stream ? 0 : L * 24));
     m.opd = (uint32_t)b;
     if (tp.stream) {  // programs, thresholds and options from global memory;
         // per-warp program slices for the bulk
@@ -402,19 +402,17 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     // (OM) the terms of the largest option threshold of row (s, t), k > 0
     // (chain_dp.hpp:141-147, local slots): max(F[s] + seed[t], B[s]) with
     // F = max fwd_req, B = max(bwd_req, pack_chg) over block s's options and
-    // seed[t] = 2 act_u[t+1] (t < L-1), each clamped to +-2^29
-    int32_t* s_thx = reinterpret_cast<int32_t*>(smem_raw + sm.thx);
+    // seed[t] = 2 act_u[t+1] (t < L-1); 64-bit (sizes are unbounded)
+    int64_t* s_thx = reinterpret_cast<int64_t*>(smem_raw + sm.thx);
     for (int b = tid; OM && !STREAM && b < L; b += kNT) {
-        constexpr int64_t kC = 1ll << 29;
-        int64_t f = -kC, bp = -kC;
+        int64_t f = INT64_MIN / 4, bp = INT64_MIN / 4;
         for (int o = __ldg(dm.blk_off + b); o < __ldg(dm.blk_off + b + 1); ++o) {
             f = max(f, __ldg(dm.fwd_req + o) - g.m_base);
             bp = max(bp, max(__ldg(dm.bwd_req + o), __ldg(dm.pack_chg + o)) - g.m_base);
         }
-        const int64_t sd = b < L - 1 ? 2 * __ldg(dm.act_u + b + 1) : 0;
-        s_thx[b] = (int32_t)min(max(f, -kC), kC);
-        s_thx[L + b] = (int32_t)min(max(bp, -kC), kC);
-        s_thx[2 * L + b] = (int32_t)min(sd, kC);
+        s_thx[b] = f;
+        s_thx[L + b] = bp;
+        s_thx[2 * L + b] = b < L - 1 ? 2 * __ldg(dm.act_u + b + 1) : 0;
     }
     // per step: bulk parts P and cuts per part (late diagonals split the
     // cut range over warps; >= 8 cuts per part)
@@ -688,7 +686,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             // smallest budget m_lo: the batches run ungated through merge8
             bool open = false;
             if constexpr (OM && !STREAM) {
-                const int32_t thx = max(s_thx[s] + s_thx[2 * L + s + k], s_thx[L + s]);
+                const int64_t thx = max(s_thx[s] + s_thx[2 * L + s + k], s_thx[L + s]);
                 open = __all_sync(0xffffffffu, thx <= m_lo);
             }
             auto options = [&](auto has_sub) {

@@ -116,3 +116,31 @@ def test_random_refill_walks_vs_oracle(orc, seed):
                     np.testing.assert_array_equal(o, ref[0])
                     np.testing.assert_array_equal(k, ref[1])
                     np.testing.assert_array_equal(v, ref[2])
+
+
+@pytest.mark.parametrize("scale", [1, 1000003])
+@pytest.mark.parametrize("seed", range(3))
+def test_random_menus_mixed_width_jobs(orc, seed, scale):
+    """Odd menus through the mixed-width tile-job kernel, whose option batches
+    run ungated when no threshold of the row is above the warp's smallest
+    budget: rows on both sides of that test (budgets up to 300 slots, 32- and
+    16-slot tiles), and sizes scaled past 2^29 (unit 1: thresholds far above
+    and below the budgets, negative forward requirements)."""
+    rng = np.random.default_rng(4000 + seed)
+    for _ in range(12):
+        menu = odd_menu(rng)
+        if scale > 1:
+            for f in ("save_mem", "peak_fwd", "peak_fwd_pre", "peak_bwd"):
+                setattr(menu, f, getattr(menu, f) * scale)
+            menu.act_sizes = menu.act_sizes * scale
+        unit = 1 if scale > 1 else int(rng.integers(1, 4))
+        M = int(rng.integers(40, 300))
+        st, *ref = orc.fill(menu, unit, M)
+        if st != 0:
+            continue
+        with rotor.tuning("jobs", "mixed", tile_rows=1), \
+                rotor.DpTable(menu, unit, M, kernel="tiles") as t:
+            o, k, v = t.download()
+            np.testing.assert_array_equal(o, ref[0])
+            np.testing.assert_array_equal(k, ref[1])
+            np.testing.assert_array_equal(v, ref[2])

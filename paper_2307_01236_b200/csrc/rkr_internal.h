@@ -195,7 +195,7 @@ size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p);  // coun
 // row; done[k * T + j] != 0 once diagonal k of tile j is stored.
 // K1t reads option thresholds and (shift, pass time) pairs in whole batches
 // of kTileOptBatch: thr rows and option slots are padded to a multiple.
-constexpr int kTileOptBatch = 8;  // 16 measured: config 2 -2%, configs 1 and 3 +8-12%
+constexpr int kTileOptBatch = 8;  // the smallest K1t option batch (tile_plan pads to its kernel's batch)
 struct TileSmem {  // shared-memory carve-up of K1t (byte offsets)
     uint32_t best, code, blk, split, thx, opd, prog, thr, xch, bar, total;
     uint32_t prog_bytes, thr_bytes;  // one buffer of each (two of each are kept)

@@ -258,8 +258,8 @@ void layout_sizes(rkr_table* t) {
     const bool progs = t->kernel == RKR_KERNEL_PERSISTENT;
     const size_t nc = progs ? (size_t)program_cut_entries(t->g) : 0;
     // thr row stride; K1t copies thr rows with bulk copies and reads whole option batches
-    t->prog.ocap = (int32_t)(t->tiles ? round_up(std::max<int32_t>(h.max_opts, 1), kTileOptBatch)
-                                      : std::max<int32_t>(h.max_opts, 1));
+    t->prog.ocap = t->tiles ? t->tplan.ocap  // (whole option batches of the plan's kernel)
+                            : std::max<int32_t>(h.max_opts, 1);
     take(nc * 16);                               // 22 program ptr
     take(nc * vbytes);                           // 23 program sweep
     take(nc * 4);                                // 24 program gate

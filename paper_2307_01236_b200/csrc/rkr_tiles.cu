@@ -128,10 +128,12 @@ __device__ __forceinline__ void nb_arrive(int id) {
 constexpr int kNW = 32;        // warps per CTA
 constexpr int kNT = kNW * 32;  // threads per CTA
 constexpr int kU = 8;          // cuts per load batch (2 kU loads in flight per lane)
-constexpr int kOB = kTileOptBatch;  // options per load batch (ocap is a multiple of kOB)
 constexpr int kSlice = 64;          // STREAM: cut-program entries staged per warp at a time
+template <int RPW>
+constexpr int kOptBatch = RPW == 1 ? 16 : 8;  // options per load batch (ocap: a multiple)
 
 inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~15ull); }
+inline int ceil_to(int x, int a) { return (x + a - 1) / a * a; }
 
 // First budget slot of tile j and the tile holding slot x: W-slot tiles, or
 // (mixed plans) j1 32-slot tiles followed by 16-slot ones.
@@ -376,6 +378,11 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                                          unsigned char* smem_raw, uint32_t ph0, uint32_t ph1) {
     constexpr int W = 32 / RPW;
     constexpr int kNC = COMM ? kNW - 1 : kNW;  // compute warps
+    // options per load batch: 16 with one row per warp (16 window reads in
+    // flight per lane: config 3 -5 %, config 2 -3 % against 8; the plan pads
+    // ocap to a multiple of 16), 8 with two rows per warp
+    constexpr int kOB = kOptBatch<RPW>;
+
     const TileSmem& sm = tp.sm;
     int32_t* s_blk = reinterpret_cast<int32_t*>(smem_raw + sm.blk);
     int2* s_opd = reinterpret_cast<int2*>(smem_raw + sm.opd);
@@ -697,10 +704,10 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                     return SUB ? tail_ld(optw + neg_shift) : 0u;
                 };
                 // Whole batches [ia, ibf), then (OM) the options past them one
-                // by one: menus of 8n + 1 options (option 0 and the solver's
-                // 8n) scan no padding; the first one's read goes out with the
-                // first batch's.  (Software-pipelining the batches -- the next
-                // batch's reads in flight during this batch's compares --
+                // by one (the first one's read goes out with the first
+                // batch's): OM scans no padding, the other kernels run the
+                // last batch into it.  (Software-pipelining the batches -- the
+                // next batch's reads in flight during this batch's compares --
                 // spills at 64 registers per thread.)
                 const int ibf = OM ? ia + (ib - ia) / kOB * kOB : ib;
                 const int2* od2 = reinterpret_cast<const int2*>(od4);
@@ -715,7 +722,9 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                         tot[q + 1] = (uint32_t)o2.w + sub_at(o2.z);
                     }
                     if (SUB && open) {
-                        merge8(tot, i0 + 1, best, code);
+#pragma unroll
+                        for (int h = 0; h < kOB; h += 8)
+                            merge8(*reinterpret_cast<uint32_t(*)[8]>(tot + h), i0 + h + 1, best, code);
                         continue;
                     }
                     int32_t th[kOB];
@@ -1078,7 +1087,7 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, const
     tp.cap = (int32_t)(units * 32 > kNT ? units * 32 : kNT);
     tp.L = g.L;
     tp.nq = (int32_t)nq;
-    tp.ocap = ocap;
+    tp.ocap = (int32_t)ceil_to(ocap, rpw == 1 ? kOptBatch<1> : kOptBatch<2>);
     // the communication warp pays off where the fill is latency-bound
     // (per-step work of a few microseconds: configs 1-2), not where it is
     // throughput-bound (config 3: measured 5.36 ms without, 6.56 with)
@@ -1089,7 +1098,7 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, const
     // two or more option batches (config 2: -3.5 %; measured slower with
     // one batch (config 1), as tile jobs (config 3: +7 %) and for batches
     // of tables (config 4))
-    tp.split = tp.comm && !tp.jobs && ocap >= 2 * kOB ? 1 : 0;
+    tp.split = tp.comm && !tp.jobs && tp.ocap >= 16 ? 1 : 0;
     if (kn.tune & RKR_TUNE_SPLIT_OFF) tp.split = 0;
     if (kn.tune & RKR_TUNE_SPLIT_ON) tp.split = tp.comm;
     tp.stream = 0;

@@ -181,6 +181,7 @@ struct rkr_table {
     DevMenu dm{};
     void* block = nullptr;        // one pooled allocation: menu | scratch | opt | arg
     size_t block_bytes = 0, work_bytes = 0;
+    size_t block_cap = 0, mirror_cap = 0;  // process shards: bytes of the cudaMalloc blocks (reused)
     size_t off_tp = 0, off_jobs = 0;  // K1t tile jobs: plan and job list in the menu blob
     TilePlan* dtp = nullptr;
     int2* djobs = nullptr;
@@ -261,6 +262,9 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
                          int R, rkr_table** out, const ShardSpec* spec = nullptr,
                          bool batch_tiles = false, bool defer = false);
 void free_table(rkr_table* t);
+// reusable cudaMalloc blocks of process shards (IPC-exportable), per device
+void* ipc_block_take(int dev, size_t need, size_t* cap);
+void ipc_block_give(int dev, void* block, size_t bytes);
 // solve_chain's min-feasible search by thresholds (rkr_kernels.cu
 // batch_thresholds): thr(0, L-1) of the tables d[which[i]] (device
 // descriptors), L[i] blocks each; kInf64 when never feasible.

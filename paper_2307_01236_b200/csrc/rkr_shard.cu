@@ -518,7 +518,10 @@ rkr_status rkr_shard_mirror(rkr_table* t0, int32_t m_max, void* ipc_handle, int6
     DeviceGuard dg(t0->device);
     if (!t0->mirror) {
         const int64_t sa = round_up((int64_t)m_max + 1, 64);
-        CK(cudaMalloc(reinterpret_cast<void**>(&t0->mirror), (size_t)t0->g.rows * sa * 2));
+        const size_t bytes = (size_t)t0->g.rows * sa * 2;
+        t0->mirror_cap = bytes;
+        t0->mirror = static_cast<uint16_t*>(ipc_block_take(t0->device, bytes, &t0->mirror_cap));
+        if (!t0->mirror) CK(cudaMalloc(reinterpret_cast<void**>(&t0->mirror), bytes));
         t0->mirror_sa = sa;
         t0->mirror_M = m_max;
         t0->hdesc.arg_mirror = t0->mirror;

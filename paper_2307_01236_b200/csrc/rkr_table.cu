@@ -179,6 +179,55 @@ thread_local Staging t_sweep;  // pinned D2H staging (a sweep's walks; outlives 
 thread_local Staging t_desc;   // pinned H2D staging of batch descriptors (overlaps the menu upload)
 
 
+// Process-shard blocks (and shard 0's walk mirror) must come from
+// cudaMalloc (cudaIpcGetMemHandle does not take pool memory); destroyed ones
+// are kept, a few per device, and reused by the next request that fits --
+// the pool's policy for ordinary tables, without a synchronous cudaMalloc +
+// cudaFree of up to gigabytes per solve.
+namespace {
+constexpr int kIpcSlots = 4;
+struct IpcBlockCache {
+    std::mutex mu;
+    void* p[64][kIpcSlots] = {};
+    size_t bytes[64][kIpcSlots] = {};
+} g_ipc_cache;
+}  // namespace
+
+void* ipc_block_take(int dev, size_t need, size_t* cap) {
+    std::lock_guard<std::mutex> g(g_ipc_cache.mu);
+    int best = -1;
+    for (int i = 0; i < kIpcSlots; ++i) {
+        const size_t have = g_ipc_cache.bytes[dev & 63][i];
+        if (g_ipc_cache.p[dev & 63][i] && have >= need && have <= 2 * need &&
+            (best < 0 || have < g_ipc_cache.bytes[dev & 63][best]))
+            best = i;
+    }
+    if (best < 0) return nullptr;
+    void* out = g_ipc_cache.p[dev & 63][best];
+    g_ipc_cache.p[dev & 63][best] = nullptr;
+    *cap = g_ipc_cache.bytes[dev & 63][best];
+    return out;
+}
+
+void ipc_block_give(int dev, void* block, size_t bytes) {  // the device is current, the block idle
+    void* old = nullptr;
+    {
+        std::lock_guard<std::mutex> g(g_ipc_cache.mu);
+        int slot = 0;  // an empty slot, else the smallest block goes
+        for (int i = 0; i < kIpcSlots; ++i) {
+            if (!g_ipc_cache.p[dev & 63][i]) {
+                slot = i;
+                break;
+            }
+            if (g_ipc_cache.bytes[dev & 63][i] < g_ipc_cache.bytes[dev & 63][slot]) slot = i;
+        }
+        old = g_ipc_cache.p[dev & 63][slot];
+        g_ipc_cache.p[dev & 63][slot] = block;
+        g_ipc_cache.bytes[dev & 63][slot] = bytes;
+    }
+    if (old) cudaFree(old);
+}
+
 void free_table(rkr_table* t) {
     if (!t) return;
     DeviceGuard dg(t->device);
@@ -189,14 +238,14 @@ void free_table(rkr_table* t) {
     }
     if (t->block && t->ipc) {
         cudaStreamSynchronize(t->stream);
-        cudaFree(t->block);
+        ipc_block_give(t->device, t->block, t->block_cap);
         t->block = nullptr;
     }
     if (t->block && t->owns_block) cudaFreeAsync(t->block, t->stream);
     if (t->wrec) cudaFreeAsync(t->wrec, t->stream);
     if (t->mirror || t->walk_scratch) {
         cudaStreamSynchronize(t->stream);
-        if (t->mirror) cudaFree(t->mirror);
+        if (t->mirror) ipc_block_give(t->device, t->mirror, t->mirror_cap);
         if (t->walk_scratch) cudaFree(t->walk_scratch);
     }
     delete t;
@@ -376,7 +425,9 @@ void stage_menu(const rkr_table* t, unsigned char* blob) {
 rkr_status alloc_and_upload(rkr_table* t) {
     layout_sizes(t);
     if (t->ipc) {  // exportable to other processes (cudaIpcGetMemHandle needs cudaMalloc)
-        CK(cudaMalloc(&t->block, t->block_bytes));
+        t->block_cap = t->block_bytes;
+        t->block = ipc_block_take(t->device, t->block_bytes, &t->block_cap);
+        if (!t->block) CK(cudaMalloc(&t->block, t->block_bytes));
     } else {
         CK(cudaMallocAsync(&t->block, t->block_bytes, t->stream));
     }

@@ -11,7 +11,7 @@
 // the L diagonals of its tile in order, and the only cross-SM traffic is one
 // done flag per (diagonal, tile).
 //
-// Warp roles.  Warps 0..30 compute; warp 31 communicates, so that no fence,
+// Warp roles.  Warps 0..26 compute; warp 27 communicates, so that no fence,
 // flag poll or release ever stalls a compute warp:
 //   compute, step k:  bulk(k) -> sync READY(k) -> tail(k) -> arrive DONE(k)
 //   comm,    step k:  poll flags (k-1) of tiles j-d..j-1, acquire ->
@@ -30,7 +30,7 @@
 // minimum (chain_dp.hpp:139-174).
 //
 // Eligibility: 32-bit costs; T = ceil((M+1) / W) tiles co-resident (one
-// 1024-thread CTA per SM, cooperative launch); shared memory for the bulk
+// 896-thread CTA per SM, cooperative launch); shared memory for the bulk
 // partials and two steps of programs.  Otherwise the queue-scheduled K1p
 // (rkr_persist.cu) runs.
 #include <cuda_runtime.h>
@@ -112,21 +112,26 @@ __device__ __forceinline__ int t_ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// 28 warps per CTA (27 compute + the communication warp), 72 registers per
+// thread: against 32 warps / 64 registers, config 1 -7.5 %, configs 4-5
+// -1-2 %, configs 2-3 unchanged; 24 warps / 80 registers loses 2-5 % on
+// configs 2-3 (fewer warps to cover the gathers' latency)
+constexpr int kNW = 28;        // warps per CTA
+constexpr int kNT = kNW * 32;  // threads per CTA
 // named barriers (0 is __syncthreads): compute warps arrive / sync, the
 // communication warp syncs / arrives
 constexpr int kBarReady = 1, kBarDone = 2, kBarSplit = 3;
 __device__ __forceinline__ void nb_sync(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(1024) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kNT) : "memory");
 }
 __device__ __forceinline__ void nb_sync_n(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void nb_arrive(int id) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(1024) : "memory");
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kNT) : "memory");
 }
 
-constexpr int kNW = 32;        // warps per CTA
-constexpr int kNT = kNW * 32;  // threads per CTA
+
 constexpr int kU = 8;          // cuts per load batch (2 kU loads in flight per lane)
 constexpr int kSlice = 64;          // STREAM: cut-program entries staged per warp at a time
 template <int RPW>
@@ -349,9 +354,9 @@ __device__ __forceinline__ void scan_cuts_streamed(const uint32_t* __restrict__ 
     }
 }
 
-// COMM: warp 31 is the communication warp (latency-bound tables); otherwise
-// all 32 warps compute and warp 0 polls / thread 0 publishes inline, behind
-// CTA barriers (throughput-bound tables, where the 32nd compute warp and
+// COMM: the last warp is the communication warp (latency-bound tables);
+// otherwise all warps compute and warp 0 polls / thread 0 publishes inline, behind
+// CTA barriers (throughput-bound tables, where the extra compute warp and
 // barrier-aligned phases measured faster).
 //
 // tile_job: every diagonal of tile j of one table.  ph0/ph1 = completed

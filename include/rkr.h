@@ -109,7 +109,8 @@ typedef enum {
     RKR_TUNE_WIDE_SEARCH = 1 << 9, /* min-feasible search by filling the wide table (as the
                                       reference does) instead of the threshold recurrence */
     RKR_TUNE_UNIFORM = 1 << 10,    /* tile jobs all of one width (no half tiles in the last wave) */
-    RKR_TUNE_MIXED = 1 << 11       /* (tests) tile jobs: half 32-slot, half 16-slot tiles */
+    RKR_TUNE_MIXED = 1 << 11,      /* (tests) tile jobs: half 32-slot, half 16-slot tiles */
+    RKR_TUNE_NO_PRUNE = 1 << 12    /* K1t: scan every option of open rows (no dominance pruning) */
 } rkr_tune;
 
 /* Execution settings; pass NULL for defaults (device 0, the library's shared

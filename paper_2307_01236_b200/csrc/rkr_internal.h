@@ -197,7 +197,7 @@ size_t persistent_state_bytes(const Geometry& g, const PersistPlan& p);  // coun
 // of kTileOptBatch: thr rows and option slots are padded to a multiple.
 constexpr int kTileOptBatch = 8;  // the smallest K1t option batch (tile_plan pads to its kernel's batch)
 struct TileSmem {  // shared-memory carve-up of K1t (byte offsets)
-    uint32_t best, code, blk, split, thx, opd, prog, thr, xch, bar, total;
+    uint32_t best, code, blk, split, thx, opd, pru, prog, thr, xch, bar, total;
     uint32_t prog_bytes, thr_bytes;  // one buffer of each (two of each are kept)
 };
 struct TilePlan {
@@ -210,6 +210,7 @@ struct TilePlan {
     int32_t split = 0;                    // 1 (with comm): late diagonals split each tail over 2 warps
     int32_t stream = 0;                   // 1: programs / thresholds / options read from global (long chains)
     int32_t halo = 0;                     // 1: a budget shard (halo wait / push compiled in; comm, no split)
+    int32_t prune = 0;                    // 1: open rows scan each block's undominated options only
     // mixed tile widths (single tables as tile jobs): tiles j >= j1 are
     // 16-slot (two rows per warp) tiles after j1 32-slot ones, so the last
     // wave of jobs is made of half jobs

@@ -136,6 +136,7 @@ constexpr int kU = 8;          // cuts per load batch (2 kU loads in flight per 
 constexpr int kSlice = 64;          // STREAM: cut-program entries staged per warp at a time
 template <int RPW>
 constexpr int kOptBatch = RPW == 1 ? 16 : 8;  // options per load batch (ocap: a multiple)
+constexpr int kPcap = 16;  // undominated options kept per block (more: the block is not pruned)
 
 inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~15ull); }
 inline int ceil_to(int x, int a) { return (x + a - 1) / a * a; }
@@ -179,6 +180,7 @@ inline TileSmem tile_smem(const TilePlan& tp) {
     m.thx = (uint32_t)b;  // per block: the terms of its largest option threshold
     b = al16(b + (tp.stream ? 0 : L * 24));
     m.opd = (uint32_t)b;
+    m.pru = 0;
     if (tp.stream) {  // programs, thresholds and options from global memory;
         // per-warp program slices for the bulk
         m.prog_bytes = (uint32_t)(kNW * kSlice * 16 * tp.rpw);
@@ -190,6 +192,10 @@ inline TileSmem tile_smem(const TilePlan& tp) {
         b = al16(b + (uint64_t)kNW * tp.rpw * tp.ocap * 12);
     } else {
         b = al16(b + L * tp.ocap * 8);  // [block][ocap] {-pack shift, pass time}, padded
+        if (tp.prune) {  // [block][kPcap] {-pack shift, pass time} | [block][kPcap] codes | [block] count
+            m.pru = (uint32_t)b;
+            b = al16(b + L * kPcap * 10 + L * 4);
+        }
         m.prog = (uint32_t)b;
         b += 2ull * m.prog_bytes;
         m.thr = (uint32_t)b;
@@ -261,6 +267,22 @@ __device__ __forceinline__ void merge8(const uint32_t (&tot)[8], int c0, uint32_
             best = x;
             code = c0 + qf;
         }
+    }
+}
+
+// merge8 over a list whose position q holds code pcd[q] (the undominated
+// options of a block, menu order)
+__device__ __forceinline__ void merge8p(const uint32_t (&tot)[8], const uint16_t* pcd, uint32_t& best,
+                                        int& code) {
+    const uint32_t x = __vimin3_u32(__vimin3_u32(tot[0], tot[1], tot[2]),
+                                    __vimin3_u32(tot[3], tot[4], tot[5]), min(tot[6], tot[7]));
+    if (x < best) {
+        int qf = 7;
+#pragma unroll
+        for (int q = 6; q >= 0; --q)
+            if (tot[q] == x) qf = q;
+        best = x;
+        code = pcd[qf];
     }
 }
 
@@ -411,21 +433,6 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     // time INF).  Cut programs and thresholds arrive per step by bulk copy,
     // two steps ahead (double buffer, one mbarrier per buffer).
     for (int c = tid; c <= L; c += kNT) s_blk[c] = __ldg(dm.blk_off + c);
-    // (OM) the terms of the largest option threshold of row (s, t), k > 0
-    // (chain_dp.hpp:141-147, local slots): max(F[s] + seed[t], B[s]) with
-    // F = max fwd_req, B = max(bwd_req, pack_chg) over block s's options and
-    // seed[t] = 2 act_u[t+1] (t < L-1); 64-bit (sizes are unbounded)
-    int64_t* s_thx = reinterpret_cast<int64_t*>(smem_raw + sm.thx);
-    for (int b = tid; OM && !STREAM && b < L; b += kNT) {
-        int64_t f = INT64_MIN / 4, bp = INT64_MIN / 4;
-        for (int o = __ldg(dm.blk_off + b); o < __ldg(dm.blk_off + b + 1); ++o) {
-            f = max(f, __ldg(dm.fwd_req + o) - g.m_base);
-            bp = max(bp, max(__ldg(dm.bwd_req + o), __ldg(dm.pack_chg + o)) - g.m_base);
-        }
-        s_thx[b] = f;
-        s_thx[L + b] = bp;
-        s_thx[2 * L + b] = b < L - 1 ? 2 * __ldg(dm.act_u + b + 1) : 0;
-    }
     // per step: bulk parts P and cuts per part (late diagonals split the
     // cut range over warps; >= 8 cuts per part)
     int2* s_split = reinterpret_cast<int2*>(smem_raw + sm.split);
@@ -442,12 +449,94 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
     }
     int* s_ucnt = reinterpret_cast<int*>(smem_raw + sm.split) + 2 * L;  // bulk units taken, per step parity
     if (tid < 2) s_ucnt[tid] = 0;
-    for (int q = tid; !STREAM && q < L * ocap; q += kNT) {
+    // (OM) per block, one warp (lanes over its options):
+    // * s_opd: {-pack shift clamped to pad, pass time} per option slot;
+    // * the terms of the largest option threshold of row (s, t),
+    //   k > 0 (chain_dp.hpp:141-147, local slots): max(F[s] + seed[t], B[s])
+    //   with F = max fwd_req, B = max(bwd_req, pack_chg) over block s's
+    //   options and seed[t] = 2 act_u[t+1] (t < L-1); 64-bit (sizes are
+    //   unbounded).  A row is *open* for a warp when that is <= the warp's
+    //   smallest budget: every option admissible at every budget of the warp.
+    // * (prune) dominance pruning for open rows: option x can never be the
+    //   scan's first minimum if another option y of the block has a pack
+    //   shift <= x's and a pass time <= x's (y before x in menu order) or <
+    //   x's (y after x): opt(s+1, t) does not increase with the budget, so y's
+    //   total is <= (before) / < (after) x's at every m (chain_dp.hpp:141-155;
+    //   the reference's own option generator drops dominated options the same
+    //   way, options.hpp:182-217, on more fields).  The undominated options
+    //   (menu order, padded with options that never win) and their codes;
+    //   blocks with more than kPcap of them scan everything.  (The shift is
+    //   clamped to pad only for options whose threshold exceeds M, which no
+    //   open row has.)
+    int64_t* s_thx = reinterpret_cast<int64_t*>(smem_raw + sm.thx);
+    int2* s_pru = reinterpret_cast<int2*>(smem_raw + sm.pru);
+    uint16_t* s_pcd = reinterpret_cast<uint16_t*>(smem_raw + sm.pru + L * kPcap * 8);
+    int32_t* s_pcnt = reinterpret_cast<int32_t*>(smem_raw + sm.pru + L * kPcap * 10);
+    for (int q = tid; !OM && !STREAM && q < L * ocap; q += kNT) {
         const int b = q / ocap, i = q - b * ocap;
         const int o = __ldg(dm.blk_off + b) + i;
         s_opd[q] = o < __ldg(dm.blk_off + b + 1)
                        ? make_int2(-__ldg(pq.pc + o), (int)__ldg(static_cast<const uint32_t*>(pq.otot) + o))
                        : make_int2(0, (int)INF);
+    }
+    for (int b = warp; OM && !STREAM && b < L; b += kNW) {
+        const int o0 = __ldg(dm.blk_off + b), own = __ldg(dm.blk_off + b + 1) - o0;
+        int2* ob = s_opd + b * ocap;
+        int64_t f = INT64_MIN / 4, bp = INT64_MIN / 4;
+        for (int i = lane; i < ocap; i += 32) {
+            int2 v = make_int2(0, (int)INF);
+            if (i < own) {
+                const int o = o0 + i;
+                v = make_int2(-__ldg(pq.pc + o), (int)__ldg(static_cast<const uint32_t*>(pq.otot) + o));
+                {
+                    f = max(f, __ldg(dm.fwd_req + o) - g.m_base);
+                    bp = max(bp, max(__ldg(dm.bwd_req + o), __ldg(dm.pack_chg + o)) - g.m_base);
+                }
+            }
+            ob[i] = v;
+        }
+        {
+#pragma unroll
+            for (int d = 16; d; d >>= 1) {
+                f = max(f, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)f, d));
+                bp = max(bp, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)bp, d));
+            }
+            if (lane == 0) {
+                s_thx[b] = f;
+                s_thx[L + b] = bp;
+                s_thx[2 * L + b] = b < L - 1 ? 2 * __ldg(dm.act_u + b + 1) : 0;
+            }
+        }
+        if (!tp.prune) continue;
+        __syncwarp();
+        int cnt = 0;
+        for (int i0 = 0; i0 < own; i0 += 32) {
+            const int i = i0 + lane;
+            bool keep = i < own;
+            if (keep) {
+                const int2 x = ob[i];
+                for (int y = 0; y < own; ++y) {
+                    const int2 v = ob[y];
+                    if (y != i && v.x >= x.x &&
+                        (y < i ? (uint32_t)v.y <= (uint32_t)x.y : (uint32_t)v.y < (uint32_t)x.y)) {
+                        keep = false;
+                        break;
+                    }
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
+            if (keep && pos < kPcap) {
+                s_pru[b * kPcap + pos] = ob[i];
+                s_pcd[b * kPcap + pos] = (uint16_t)(i + 1);
+            }
+            cnt += __popc(bal);
+        }
+        for (int q = cnt + lane; q < kPcap; q += 32) {
+            s_pru[b * kPcap + q] = make_int2(0, (int)INF);
+            s_pcd[b * kPcap + q] = 0;
+        }
+        if (lane == 0) s_pcnt[b] = cnt;
     }
     // lower tiles this one reads: those holding slots [m_lo - pad, m_lo)
     const int d_eff = j - tile_of(tp, m_lo - g.pad > 0 ? m_lo - g.pad : 0);
@@ -558,6 +647,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             if (P > pmax) P = pmax;
             chunk = (nb + P - 1) / P;
         }
+        const int TS = (COMM && SPLIT && 2 * units <= kNC) ? 2 : 1;
         // bulk partials (see tile_smem)
         const int poff = !COMM ? 0 : (P == 1 ? (k & 1) * tp.cap : 2 * tp.cap + (k & 1) * kNT);
         uint32_t* pbest = reinterpret_cast<uint32_t*>(smem_raw + sm.best) + poff;
@@ -629,7 +719,6 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         // batches, half h = 1 the remaining options, cut i = 0, the bulk parts
         // and cut i = k-1.  All of h = 0's candidates precede h = 1's in the
         // scan, so the cell's first minimum is h0 if h0.value <= h1.value.
-        const int TS = (COMM && SPLIT && 2 * units <= kNC) ? 2 : 1;
         uint32_t* xbest = reinterpret_cast<uint32_t*>(smem_raw + sm.xch);
         uint16_t* xcode = reinterpret_cast<uint16_t*>(xbest + kNT);
         for (int v = warp; v < units * TS; v += kNC) {
@@ -696,10 +785,16 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             // IMAD.WIDE off the lane's row base (shifts stored negated).
             // (OM) no option threshold of the row is above the warp's
             // smallest budget m_lo: the batches run ungated through merge8
-            bool open = false;
+            bool open = false, popen = false;
+            int pbat = 0;  // (popen) batches of 8 undominated options
             if constexpr (OM && !STREAM) {
                 const int64_t thx = max(s_thx[s] + s_thx[2 * L + s + k], s_thx[L + s]);
                 open = __all_sync(0xffffffffu, thx <= m_lo);
+                if (tp.prune && open && k > 0) {
+                    const int pc = s_pcnt[s];
+                    popen = __all_sync(0xffffffffu, pc <= kPcap);
+                    pbat = (__reduce_max_sync(0xffffffffu, pc) + 7) >> 3;
+                }
             }
             auto options = [&](auto has_sub) {
                 constexpr bool SUB = decltype(has_sub)::value;
@@ -714,6 +809,24 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 // last batch into it.  (Software-pipelining the batches -- the
                 // next batch's reads in flight during this batch's compares --
                 // spills at 64 registers per thread.)
+                if constexpr (SUB && OM && !STREAM) {
+                    if (popen) {  // open row: the block's undominated options only (h = 1: none)
+                        if (h == 1) return;
+                        const int4* pr4 = reinterpret_cast<const int4*>(s_pru + s * kPcap);
+                        const uint16_t* pcd = s_pcd + s * kPcap;
+                        for (int hb = 0; hb < pbat; ++hb) {
+                            uint32_t tot[8];
+#pragma unroll
+                            for (int q = 0; q < 8; q += 2) {
+                                const int4 o2 = pr4[(hb * 8 + q) >> 1];
+                                tot[q] = (uint32_t)o2.y + sub_at(o2.x);
+                                tot[q + 1] = (uint32_t)o2.w + sub_at(o2.z);
+                            }
+                            merge8p(tot, pcd + hb * 8, best, code);
+                        }
+                        return;
+                    }
+                }
                 const int ibf = OM ? ia + (ib - ia) / kOB * kOB : ib;
                 const int2* od2 = reinterpret_cast<const int2*>(od4);
                 const int2 orem = ibf < ib ? od2[ibf] : make_int2(0, 0);
@@ -726,7 +839,7 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                         tot[q] = (uint32_t)o2.y + sub_at(o2.x);
                         tot[q + 1] = (uint32_t)o2.w + sub_at(o2.z);
                     }
-                    if (SUB && open) {
+                    if (OM && SUB && open) {
 #pragma unroll
                         for (int h = 0; h < kOB; h += 8)
                             merge8(*reinterpret_cast<uint32_t(*)[8]>(tot + h), i0 + h + 1, best, code);
@@ -1107,6 +1220,7 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, const
     if (kn.tune & RKR_TUNE_SPLIT_OFF) tp.split = 0;
     if (kn.tune & RKR_TUNE_SPLIT_ON) tp.split = tp.comm;
     tp.stream = 0;
+    tp.prune = 0;
     tp.sm = tile_smem(tp);
     if (tp.sm.total > 220 * 1024 || (kn.tune & RKR_TUNE_STREAM)) {
         // long chains: a diagonal's programs do not fit shared memory.
@@ -1140,6 +1254,18 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, const
         const int64_t j1 = T / 2, rest = (int64_t)g.M + 1 - 32 * j1;
         tp.j1 = (int32_t)j1;
         tp.T = (int32_t)(j1 + (rest + 15) / 16);
+    }
+    // Dominance pruning of open rows (the mixed-width single-table jobs,
+    // tile_job's OM): config 3 fill -8 %; the latency-bound co-resident
+    // tables (configs 1-2) and batches (config 4) measured 2-10 % slower
+    // with it (shorter scans, not shorter critical paths).
+    if (tp.j1 != INT32_MAX && !(kn.tune & RKR_TUNE_NO_PRUNE)) {
+        tp.prune = 1;
+        tp.sm = tile_smem(tp);
+        if (tp.sm.total > 220 * 1024) {  // the lists do not fit beside the staged programs
+            tp.prune = 0;
+            tp.sm = tile_smem(tp);
+        }
     }
     return tp.sm.total <= 220 * 1024 ? 1 : 0;
 }

@@ -178,7 +178,7 @@ KERNELS = {"persistent": 0, "diagonal": 1, "queue": 2, "tiles": 3}
 TUNE = {"no_tiles": 1 << 0, "jobs": 1 << 1, "comm_off": 1 << 2, "comm_on": 1 << 3,
         "split_off": 1 << 4, "split_on": 1 << 5, "stream": 1 << 6, "batch_queue": 1 << 7,
         "profile": 1 << 8, "wide_search": 1 << 9, "uniform": 1 << 10,
-        "mixed": 1 << 11}
+        "mixed": 1 << 11, "no_prune": 1 << 12}
 _tuning: contextvars.ContextVar = contextvars.ContextVar("rkr_tuning", default=(0, 0))
 
 

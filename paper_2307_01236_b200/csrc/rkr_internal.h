@@ -239,6 +239,8 @@ int tile_plan(const Geometry& g, int width, int sms, int64_t nq, int ocap, const
 // K1t rows per warp for a table (or shard) of `slots` budget slots.
 int tile_rows_for(int64_t slots, int sms, const TileKnobs& kn);
 int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream);
+// One table as tile jobs (tp.jobs), descriptor and plan as kernel parameters.
+int launch_fill_tiles_jobs1(const InstDesc& d, const TilePlan& tp, unsigned int* counter, void* stream);
 // Batches: jobs (table, tile) in queue order; tps[i].sm is the batch-wide
 // layout (tile_batch_smem of a plan with every table's maxima).
 TileSmem tile_batch_smem(const TilePlan& proto);

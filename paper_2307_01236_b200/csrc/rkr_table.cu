@@ -489,9 +489,8 @@ rkr_status enqueue_fill(rkr_table* t, bool walk = false, int32_t s = 0, int32_t 
         tp.wout = t->wrec;
         tp.wstack = reinterpret_cast<int4*>(t->stack);
         if (tp.jobs) {  // more tiles than SMs: one-table tile jobs
-            if (launch_fill_tiles_batch(t->ddesc, t->dtp, t->djobs, tp.T,
-                                        reinterpret_cast<unsigned int*>(t->pdev.counter), tp,
-                                        t->stream, &tp))  // (a single table: its plan)
+            if (launch_fill_tiles_jobs1(t->hdesc, tp, reinterpret_cast<unsigned int*>(t->pdev.counter),
+                                        t->stream))
                 return cuda_fail(cudaGetLastError(), "tile job launch");
             return RKR_OK;
         }
@@ -562,7 +561,9 @@ rkr_status prepare_table(const rkr_menu* menu, int64_t unit, int32_t m_max, cons
     t->g.L = h.L;
     t->g.M = m_max;
     t->g.pad = (int32_t)std::min<int64_t>(maxshift, (int64_t)m_max + 1);
-    t->g.pad = (int32_t)round_up(t->g.pad, 8);
+    // a multiple of 32 slots: a 32-slot budget tile of a row is then one
+    // aligned 128-byte line (4 sectors per unshifted warp read, not 5)
+    t->g.pad = (int32_t)round_up(t->g.pad, 32);
     if (spec) {
         t->g.pad = spec->pad;
         t->g.m_base = spec->m_base;

@@ -56,6 +56,15 @@ constexpr uint32_t INF = kInf32;  // K1t runs the 32-bit cost path only
 #ifndef RKR_EXP_RELAXED
 #define RKR_EXP_RELAXED 0
 #endif
+#ifndef RKR_POLL_RELAXED
+#define RKR_POLL_RELAXED 1
+#endif
+// timing experiments: every compute warp waits for all tails of step k
+// before bulk(k+1); RKR_TRACE_UNIT2 stamps warp 0's first tail unit in
+// phases (scripts/trace_unit_phases.py)
+#ifndef RKR_EXP_SYNCDONE
+#define RKR_EXP_SYNCDONE 0
+#endif
 #ifndef RKR_EXP_DYNUNIT
 #define RKR_EXP_DYNUNIT 0
 #endif
@@ -231,6 +240,9 @@ __device__ __forceinline__ void stage_step(const TilePlan& tp, const ProgDev& pq
 // its line holds no other row, and the acquisition of the lower tiles'
 // diagonal k-1 before each tail (ld.acquire -> CCTL.IVALL) empties L1 of
 // anything older; the bulk's reads, which never repeat, stay L2-only.
+#ifndef RKR_PAIR_TAIL
+#define RKR_PAIR_TAIL 1
+#endif
 #ifndef RKR_TAIL_L1
 #define RKR_TAIL_L1 1
 #endif
@@ -574,8 +586,18 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         for (int k = 0; k < L; ++k) {
             if (k >= 1 && !RKR_EXP_NOWAIT) {  // diagonal k-1 of the lower tiles, acquired
                 const int* row = done + (int64_t)(k - 1) * tp.T;
-                for (int q = lane; q < d_eff; q += 32)
-                    while (t_ld_acquire(row + j - 1 - q) == 0) __nanosleep(20);
+                // relaxed polls, then one acquiring load of the flag seen set:
+                // an acquire (ld.acquire -> CCTL.IVALL) per poll would empty
+                // the SM's L1 -- the compute warps' cached tail windows,
+                // spills and plan reads -- every few tens of nanoseconds
+                for (int q = lane; q < d_eff; q += 32) {
+                    if (RKR_POLL_RELAXED) {
+                        while (t_ld_relaxed(row + j - 1 - q) == 0) __nanosleep(20);
+                        (void)t_ld_acquire(row + j - 1 - q);
+                    } else {
+                        while (t_ld_acquire(row + j - 1 - q) == 0) __nanosleep(20);
+                    }
+                }
                 // (tile 0 polls nothing: its own flag, for the L1 invalidation
                 // the tail's cached reads rely on)
                 if (d_eff == 0 && lane == 0) (void)t_ld_acquire(row + j);
@@ -584,7 +606,9 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
             }
             // trace: when the lower tiles' diagonal k-1 was acquired (the
             // compute warps pass READY at max(this, their last bulk))
+#ifndef RKR_TRACE_UNIT2
             if (tp.trace && lane == 0) tp.trace[6 * ((int64_t)k * tp.T + j) + 3] = clock64();
+#endif
             nb_arrive(kBarReady);
             nb_sync(kBarDone);  // the compute warps stored diagonal k
 #ifdef RKR_TRACE_EXPERIMENT
@@ -721,7 +745,88 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         // scan, so the cell's first minimum is h0 if h0.value <= h1.value.
         uint32_t* xbest = reinterpret_cast<uint32_t*>(smem_raw + sm.xch);
         uint16_t* xcode = reinterpret_cast<uint16_t*>(xbest + kNT);
+        // (OM) Two open units at once: when both rows of a warp's next two
+        // units are open and have at most 8 undominated options, all their
+        // reads (two tail cuts and 8 option windows each) go out together --
+        // one memory round trip for the pair instead of one per unit (the
+        // tail is a chain of dependent round trips per warp)
+        auto tail_pair = [&](int vA, int vB) -> bool {
+            const int sA = min(vA * RPW + rw, rows - 1), sB = min(vB * RPW + rw, rows - 1);
+            const int64_t thA = max(s_thx[sA] + s_thx[2 * L + sA + k], s_thx[L + sA]);
+            const int64_t thB = max(s_thx[sB] + s_thx[2 * L + sB + k], s_thx[L + sB]);
+            if (!__all_sync(0xffffffffu, thA <= m_lo && thB <= m_lo && s_pcnt[sA] <= 8 && s_pcnt[sB] <= 8))
+                return false;
+            const int m = m_lo + ml;
+            const int4 nil = make_int4(0, 0, 0, M + 2);
+            const int4 a0 = prog[sA * k], b0 = prog[sB * k];
+            const int4 a1 = k > 1 ? prog[sA * k + k - 1] : nil, b1 = k > 1 ? prog[sB * k + k - 1] : nil;
+            uint32_t ca[4], cb[4];
+            ca[0] = tail_ld(opt + (uint32_t)(a0.x + m));
+            ca[1] = tail_ld(opt + (uint32_t)(a0.y + m));
+            cb[0] = tail_ld(opt + (uint32_t)(b0.x + m));
+            cb[1] = tail_ld(opt + (uint32_t)(b0.y + m));
+            ca[2] = ca[3] = cb[2] = cb[3] = INF;
+            if (k > 1) {
+                ca[2] = tail_ld(opt + (uint32_t)(a1.x + m));
+                ca[3] = tail_ld(opt + (uint32_t)(a1.y + m));
+                cb[2] = tail_ld(opt + (uint32_t)(b1.x + m));
+                cb[3] = tail_ld(opt + (uint32_t)(b1.y + m));
+            }
+            // row (s+1, t) of each unit: id rid - (L - k)
+            const uint32_t* __restrict__ wA = lane_base(opt, (rbase + sA - (L - k)) * sr + g.pad + m);
+            const uint32_t* __restrict__ wB = lane_base(opt, (rbase + sB - (L - k)) * sr + g.pad + m);
+            const int4* pA = reinterpret_cast<const int4*>(s_pru + sA * kPcap);
+            const int4* pB = reinterpret_cast<const int4*>(s_pru + sB * kPcap);
+            uint32_t ta[8], tb[8];
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+                const int4 x = pA[q >> 1], y = pB[q >> 1];
+                ta[q] = (uint32_t)x.y + tail_ld(wA + x.x);
+                ta[q + 1] = (uint32_t)x.w + tail_ld(wA + x.z);
+                tb[q] = (uint32_t)y.y + tail_ld(wB + y.x);
+                tb[q + 1] = (uint32_t)y.w + tail_ld(wB + y.z);
+            }
+            auto finish = [&](const uint32_t (&t)[8], const uint32_t (&c)[4], const int4& e0, const int4& e1,
+                              int s, int u) {
+                uint32_t best = INF;
+                int code = 0;
+                merge8p(t, s_pcd + s * kPcap, best, code);
+                const int cbase = kCutBit | (s + 1);
+                uint32_t tot = (uint32_t)e0.z + c[0] + c[1];
+                if (e0.w <= m && tot < best) {
+                    best = tot;
+                    code = cbase;
+                }
+                for (int p = 0; nb > 0 && p < P; ++p) {
+                    const int idx = (p * units + u) * 32 + lane;
+                    const uint32_t vv = pbest[idx];
+                    if (vv < best) {
+                        best = vv;
+                        code = pcode[idx];
+                    }
+                }
+                tot = (uint32_t)e1.z + c[2] + c[3];
+                if (e1.w <= m && tot < best) {
+                    best = tot;
+                    code = cbase + k - 1;
+                }
+                if (m <= M && (RPW == 1 || u * RPW + rw < rows)) {  // store (chain_dp.hpp:176-177)
+                    const int rid = rbase + s;
+                    opt[(int64_t)rid * sr + g.pad + m] = best;
+                    arg[(int64_t)rid * g.sa + m] = (uint16_t)code;
+                }
+            };
+            finish(ta, ca, a0, a1, sA, vA);
+            finish(tb, cb, b0, b1, sB, vB);
+            return true;
+        };
         for (int v = warp; v < units * TS; v += kNC) {
+            if constexpr (OM && !STREAM && !SPLIT && !HALO) {
+                if (RKR_PAIR_TAIL && tp.prune && k > 0 && v + kNC < units && tail_pair(v, v + kNC)) {
+                    v += kNC;
+                    continue;
+                }
+            }
             const int h = TS == 1 ? -1 : (v >= units ? 1 : 0);  // -1: the whole tail
             const int u = TS == 1 ? v : v - h * units;
             const bool valid = RPW == 1 || u * RPW + rw < rows;  // stores only for real rows
@@ -873,10 +978,23 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                     }
                 }
             };
+#ifdef RKR_TRACE_UNIT2
+            unsigned long long xa = 0, xb = 0;
+            if (tp.trace && tid == 0 && v == warp) xa = clock64();
+#endif
             if (k > 0)
                 options(std::true_type{});
             else
                 options(std::false_type{});
+#ifdef RKR_TRACE_UNIT2
+            asm volatile("" ::"r"(best), "r"(code));
+            if (tp.trace && tid == 0 && v == warp) {
+                xb = clock64();
+                unsigned long long* tr = tp.trace + 6 * ((int64_t)k * tp.T + j);
+                tr[1] = xa;
+                tr[2] = xb;
+            }
+#endif
             if (cuts) {
                 // Case 2 (chain_dp.hpp:158-174): cut i = 0, bulk parts, cut i = k-1
                 const int cb = kCutBit | (s + 1);
@@ -905,6 +1023,10 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                     }
                 }
             }
+#ifdef RKR_TRACE_UNIT2
+            asm volatile("" ::"r"(best), "r"(code));
+            if (tp.trace && tid == 0 && v == warp) tp.trace[6 * ((int64_t)k * tp.T + j) + 3] = clock64();
+#endif
             if (h == 1) {  // hand the later half to the h = 0 warp
                 xbest[u * 32 + lane] = best;
                 xcode[u * 32 + lane] = (uint16_t)code;
@@ -947,17 +1069,23 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
         if (tp.trace && tid == 0) {
             t3 = clock64();
             unsigned long long* tr = tp.trace + 6 * ((int64_t)k * tp.T + j);
-#ifndef RKR_TRACE_EXPERIMENT
+#if !defined(RKR_TRACE_EXPERIMENT) && !defined(RKR_TRACE_UNIT2)
             tr[0] = t0;
 #endif
+#ifndef RKR_TRACE_UNIT2
             tr[1] = c0;
             tr[2] = t1;
             if (!COMM) tr[3] = t1;
+#endif
             tr[4] = t2;
             tr[5] = t3;
         }
         if constexpr (COMM) {
+#if RKR_EXP_SYNCDONE
+            nb_sync(kBarDone);  // timing experiment: bulk(k+1) only after every tail(k)
+#else
             nb_arrive(kBarDone);  // stores of diagonal k issued; go on to bulk(k+1)
+#endif
         } else {
             __syncthreads();
             if (tid == 0) {
@@ -1130,17 +1258,53 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
         const int q = s_job;
         if (q >= njobs) break;
         const int2 jb = jobs[q];
-        if (MIXED && jb.y >= tps[jb.x].j1)  // a half tile of the last wave
-            tile_job<2, COMM, SPLIT, STREAM, false, HALO, MIXED>(descs[jb.x], tps[jb.x], jb.y, smem_raw,
-                                                                 ph0, ph1);
+        const InstDesc& jd = descs[jb.x];
+        const TilePlan& jp = tps[jb.x];
+        if (MIXED && jb.y >= jp.j1)  // a half tile of the last wave
+            tile_job<2, COMM, SPLIT, STREAM, false, HALO, MIXED>(jd, jp, jb.y, smem_raw, ph0, ph1);
         else
-            tile_job<RPW, COMM, SPLIT, STREAM, false, HALO, MIXED>(descs[jb.x], tps[jb.x], jb.y, smem_raw,
-                                                                   ph0, ph1);
-        const int L = descs[jb.x].g.L;
+            tile_job<RPW, COMM, SPLIT, STREAM, false, HALO, MIXED>(jd, jp, jb.y, smem_raw, ph0, ph1);
+        const int L = jd.g.L;
         ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
         ph1 += (uint32_t)L / 2;
         // a single table run as tile jobs: the last job to finish walks
         if constexpr (WALK) last_walk(descs[0], walkp, njobs, smem_raw);
+        __syncthreads();  // shared memory and s_job are reused by the next job
+    }
+}
+
+// One table as tile jobs (config 3: more tiles than SMs), tiles in budget
+// order from a queue.  Like fill_tiles_batch on a one-table batch, but the
+// descriptor and plan are kernel parameters (constant bank): as global reads
+// they miss L1 after every acquisition of the lower tiles' flags (ld.acquire
+// empties L1) and put L2 round trips on the tail's critical path, and
+// constant-bank operands need no registers.
+template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool WALK, bool MIXED>
+__global__ void __launch_bounds__(kNT, 1) fill_tiles_jobs1(const __grid_constant__ InstDesc D,
+                                                          const __grid_constant__ TilePlan tp,
+                                                          unsigned int* __restrict__ counter) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ int s_job;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + tp.sm.bar);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bars + 0, 1);
+        mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    uint32_t ph0 = 0, ph1 = 0;
+    for (;;) {
+        if (tid == 0) s_job = (int)atomicAdd(counter, 1u);
+        __syncthreads();
+        const int j = s_job;
+        if (j >= tp.T) break;
+        if (MIXED && j >= tp.j1)  // a half tile of the last wave
+            tile_job<2, COMM, SPLIT, STREAM, false, false, MIXED>(D, tp, j, smem_raw, ph0, ph1);
+        else
+            tile_job<RPW, COMM, SPLIT, STREAM, false, false, MIXED>(D, tp, j, smem_raw, ph0, ph1);
+        ph0 += (uint32_t)(D.g.L + 1) / 2;
+        ph1 += (uint32_t)D.g.L / 2;
+        if constexpr (WALK) last_walk(D, tp, tp.T, smem_raw);
         __syncthreads();  // shared memory and s_job are reused by the next job
     }
 }
@@ -1337,6 +1501,48 @@ int launch_fill_tiles_batch_r(const InstDesc* descs, const TilePlan* tps, const 
 }
 
 }  // namespace
+
+namespace {
+template <int RPW>
+int launch_jobs1_r(const InstDesc& d, const TilePlan& tp, unsigned int* counter, cudaStream_t st) {
+    auto go = [&](auto kern) -> int {
+        const size_t smem = tp.sm.total;
+        if (set_dyn_smem((const void*)kern, smem) != cudaSuccess) return 3;
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int grid = tp.T < sms ? tp.T : sms;  // persistent: one CTA per SM
+        kern<<<grid, kNT, smem, st>>>(d, tp, counter);
+        return cudaPeekAtLastError() == cudaSuccess ? 0 : 3;
+    };
+    if (tp.halo) return 3;
+    if (RPW == 1 && tp.j1 != INT32_MAX) {  // mixed widths: staged programs, communication warp
+        if (tp.stream || tp.split || !tp.comm) return 3;
+        return tp.walk ? go(fill_tiles_jobs1<1, true, false, false, true, true>)
+                       : go(fill_tiles_jobs1<1, true, false, false, false, true>);
+    }
+    if (tp.stream)
+        return tp.comm ? (tp.walk ? go(fill_tiles_jobs1<RPW, true, false, true, true, false>)
+                                  : go(fill_tiles_jobs1<RPW, true, false, true, false, false>))
+                       : (tp.walk ? go(fill_tiles_jobs1<RPW, false, false, true, true, false>)
+                                  : go(fill_tiles_jobs1<RPW, false, false, true, false, false>));
+    if (tp.comm && tp.split)
+        return tp.walk ? go(fill_tiles_jobs1<RPW, true, true, false, true, false>)
+                       : go(fill_tiles_jobs1<RPW, true, true, false, false, false>);
+    if (tp.comm)
+        return tp.walk ? go(fill_tiles_jobs1<RPW, true, false, false, true, false>)
+                       : go(fill_tiles_jobs1<RPW, true, false, false, false, false>);
+    return tp.walk ? go(fill_tiles_jobs1<RPW, false, false, false, true, false>)
+                   : go(fill_tiles_jobs1<RPW, false, false, false, false, false>);
+}
+}  // namespace
+
+int launch_fill_tiles_jobs1(const InstDesc& d, const TilePlan& tp, unsigned int* counter, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (tp.rpw == 1) return launch_jobs1_r<1>(d, tp, counter, st);
+    if (tp.rpw == 2) return launch_jobs1_r<2>(d, tp, counter, st);
+    return 3;
+}
 
 int launch_fill_tiles(const InstDesc& d, const TilePlan& tp, int width, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);

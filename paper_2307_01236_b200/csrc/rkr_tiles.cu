@@ -56,6 +56,9 @@ constexpr uint32_t INF = kInf32;  // K1t runs the 32-bit cost path only
 #ifndef RKR_EXP_RELAXED
 #define RKR_EXP_RELAXED 0
 #endif
+#ifndef RKR_POLL_SLEEP
+#define RKR_POLL_SLEEP 20
+#endif
 #ifndef RKR_POLL_RELAXED
 #define RKR_POLL_RELAXED 1
 #endif
@@ -142,6 +145,10 @@ __device__ __forceinline__ void nb_arrive(int id) {
 
 
 constexpr int kU = 8;          // cuts per load batch (2 kU loads in flight per lane)
+#ifndef RKR_KUB
+#define RKR_KUB 16
+#endif
+constexpr int kUB = RKR_KUB;   // (tile jobs) cuts per load batch, sweeps re-read
 constexpr int kSlice = 64;          // STREAM: cut-program entries staged per warp at a time
 template <int RPW>
 constexpr int kOptBatch = RPW == 1 ? 16 : 8;  // options per load batch (ocap: a multiple)
@@ -314,30 +321,52 @@ __device__ __forceinline__ void merge8p(const uint32_t (&tot)[8], const uint16_t
 // last cut, every lane admits every cut of the batch.  RPW = 1 (one row per
 // warp, consecutive budgets): that is lane 0's test, warp-uniform, no vote.
 // RPW = 2 (two rows per warp, 16 budgets each): a warp vote.
-template <int RPW>
+// U = cuts per load batch.  RR (tile jobs: configs 3, 4): the
+// batch's addresses come from 8-byte program reads and the sweeps are read
+// again after the loads, so a cut in flight holds two registers instead of
+// four: batches of kUB cuts (2 kUB loads in flight per lane) at the cost of
+// one more shared-memory read per cut -- the bulk is a chain of dependent
+// round trips per warp.
+template <int RPW, int U = kU, bool RR = false>
 __device__ __forceinline__ bool scan_cuts(const uint32_t* __restrict__ opt, const int4* pe, int ib,
                                           int ie, int m, int cb, uint32_t& best, int& code) {
     const uint32_t* __restrict__ optm = lane_base(opt, m);
     const int m0 = m - (int)(threadIdx.x & 31);  // RPW = 1: warp-uniform, the smallest budget
     int i0 = ib;
-    for (; i0 + kU <= ie; i0 += kU) {
-        uint32_t lv[kU], rv[kU];
-        int4 e[kU];
+    for (; i0 + U <= ie; i0 += U) {
+        uint32_t lv[U], rv[U];
+        int4 e[RR ? 1 : U];
 #pragma unroll
-        for (int q = 0; q < kU; ++q) {
-            e[q] = pe[i0 + q];
+        for (int q = 0; q < U; ++q) {
+            int2 xy;
+            if constexpr (RR) {
+                xy = *reinterpret_cast<const int2*>(pe + i0 + q);
+            } else {
+                e[q] = pe[i0 + q];
+                xy = make_int2(e[q].x, e[q].y);
+            }
             // unconditional loads (every offset is inside the table); the
             // gate masks the candidate afterwards
-            lv[q] = __ldcg(optm + (uint32_t)e[q].x);
-            rv[q] = __ldcg(optm + (uint32_t)e[q].y);
+            lv[q] = __ldcg(optm + (uint32_t)xy.x);
+            rv[q] = __ldcg(optm + (uint32_t)xy.y);
         }
-        if (RPW == 1 ? e[kU - 1].w <= m0 : __all_sync(0xffffffffu, e[kU - 1].w <= m)) {
+        int wl;
+        if constexpr (RR)
+            wl = pe[i0 + U - 1].w;
+        else
+            wl = e[U - 1].w;
+        if (RPW == 1 ? wl <= m0 : __all_sync(0xffffffffu, wl <= m)) {
             // (warp-uniform) no lane gated in this batch
-            uint32_t tot[kU];
+            uint32_t tot[U];
 #pragma unroll
-            for (int q = 0; q < kU; ++q) tot[q] = (uint32_t)e[q].z + lv[q] + rv[q];
+            for (int q = 0; q < U; ++q) {
+                if constexpr (RR)
+                    tot[q] = (uint32_t)pe[i0 + q].z + lv[q] + rv[q];
+                else
+                    tot[q] = (uint32_t)e[q].z + lv[q] + rv[q];
+            }
 #pragma unroll
-            for (int q = 0; q < kU; ++q) {
+            for (int q = 0; q < U; ++q) {
                 bool keep;
                 best = __vibmin_u32(best, tot[q], &keep);
                 if (!keep) code = cb + i0 + q;  // strictly smaller: the scan's first minimum
@@ -345,16 +374,21 @@ __device__ __forceinline__ bool scan_cuts(const uint32_t* __restrict__ opt, cons
             continue;
         }
 #pragma unroll
-        for (int q = 0; q < kU; ++q) {
-            const uint32_t tot = (uint32_t)e[q].z + lv[q] + rv[q];
-            if (e[q].w <= m && tot < best) {
+        for (int q = 0; q < U; ++q) {
+            int2 zw;
+            if constexpr (RR)
+                zw = *reinterpret_cast<const int2*>(&pe[i0 + q].z);
+            else
+                zw = make_int2(e[q].z, e[q].w);
+            const uint32_t tot = (uint32_t)zw.x + lv[q] + rv[q];
+            if (zw.y <= m && tot < best) {
                 best = tot;
                 code = cb + i0 + q;
             }
         }
         // the gate only grows with i: stop once no lane admits the batch's
         // last cut (the `break` of :164)
-        if (!__any_sync(0xffffffffu, e[kU - 1].w <= m)) return true;
+        if (!__any_sync(0xffffffffu, wl <= m)) return true;
     }
     for (; i0 < ie; ++i0) {
         const int4 e = pe[i0];
@@ -592,7 +626,8 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                 // spills and plan reads -- every few tens of nanoseconds
                 for (int q = lane; q < d_eff; q += 32) {
                     if (RKR_POLL_RELAXED) {
-                        while (t_ld_relaxed(row + j - 1 - q) == 0) __nanosleep(20);
+                        while (t_ld_relaxed(row + j - 1 - q) == 0)
+                            if (RKR_POLL_SLEEP) __nanosleep(RKR_POLL_SLEEP);
                         (void)t_ld_acquire(row + j - 1 - q);
                     } else {
                         while (t_ld_acquire(row + j - 1 - q) == 0) __nanosleep(20);
@@ -706,7 +741,11 @@ __device__ __forceinline__ void tile_job(const InstDesc& D, const TilePlan& tp, 
                                             reinterpret_cast<int4*>(smem_raw + sm.prog) + warp * RPW * kSlice,
                                             ib, ie, m, kCutBit | (s + 1), best, code);
                 else
-                    scan_cuts<RPW>(opt, prog + s * k, ib, ie, m, kCutBit | (s + 1), best, code);
+                    // tile jobs: batches of kUB cuts with the sweeps re-read
+                    // (config 3 fill -4 %, config 4 -2.4 %); the co-resident
+                    // tables keep kU (config 1 +8 % with kUB)
+                    scan_cuts<RPW, TABLE ? kU : kUB, !TABLE>(opt, prog + s * k, ib, ie, m, kCutBit | (s + 1),
+                                                           best, code);
                 pbest[it * 32 + lane] = best;
                 pcode[it * 32 + lane] = (uint16_t)code;
             }
@@ -1235,7 +1274,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles(const __grid_constant__ Ins
 // tiles of its own table, which were dequeued earlier by CTAs that are
 // running or done, so the queue cannot deadlock and tables need not be
 // co-resident.
-template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool WALK, bool HALO, bool MIXED = false>
+template <int RPW, bool COMM, bool SPLIT, bool STREAM, bool WALK, bool HALO>
 __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __restrict__ descs,
                                                           const TilePlan* __restrict__ tps,
                                                           const int2* __restrict__ jobs, int njobs,
@@ -1260,10 +1299,7 @@ __global__ void __launch_bounds__(kNT, 1) fill_tiles_batch(const InstDesc* __res
         const int2 jb = jobs[q];
         const InstDesc& jd = descs[jb.x];
         const TilePlan& jp = tps[jb.x];
-        if (MIXED && jb.y >= jp.j1)  // a half tile of the last wave
-            tile_job<2, COMM, SPLIT, STREAM, false, HALO, MIXED>(jd, jp, jb.y, smem_raw, ph0, ph1);
-        else
-            tile_job<RPW, COMM, SPLIT, STREAM, false, HALO, MIXED>(jd, jp, jb.y, smem_raw, ph0, ph1);
+        tile_job<RPW, COMM, SPLIT, STREAM, false, HALO>(jd, jp, jb.y, smem_raw, ph0, ph1);
         const int L = jd.g.L;
         ph0 += (uint32_t)(L + 1) / 2;  // uses of mbarrier 0 (even steps) and 1
         ph1 += (uint32_t)L / 2;
@@ -1476,11 +1512,7 @@ int launch_fill_tiles_batch_r(const InstDesc* descs, const TilePlan* tps, const 
     // for it in the batch kernels)
     // (split tails only for a single table run as jobs, never for batches)
     const bool split = walk && proto.comm && proto.split;
-    if (RPW == 1 && proto.j1 != INT32_MAX) {  // mixed widths: single tables, staged programs
-        if (proto.stream || split || !proto.comm) return 3;
-        return walk && walk->walk ? go(fill_tiles_batch<1, true, false, false, true, false, true>)
-                                  : go(fill_tiles_batch<1, true, false, false, false, false, true>);
-    }
+    if (proto.j1 != INT32_MAX) return 3;  // mixed widths: single tables (fill_tiles_jobs1)
     if (walk && walk->walk) {
         if (proto.stream)
             return proto.comm ? go(fill_tiles_batch<RPW, true, false, true, true, false>)

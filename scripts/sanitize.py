@@ -62,3 +62,10 @@ try:
 except rotor.InfeasibleBudget:
     pass
 rotor.sweep_raw(synthetic_menu(9, 4, 300, 3, byte_scale=64), [50, 400, 3000, 20000], 300)
+# round 2 (late): dominance-pruned open rows and paired tail units of the
+# one-table tile-job kernel, on a tie-stress menu
+with rotor.tuning("jobs", "mixed"), rotor.DpTable(synthetic_menu(24, 8, 900, 11, tie_stress=True), 1, 900,
+                                                   kernel="tiles") as t:
+    t.refill_walk(0, 23, 900)
+    t.backtrack_fetch()
+print("sanitize workload (pruned rows) done")

@@ -112,8 +112,9 @@ def golden(cfg_idx):
 
 
 FILL_KERNELS = {
-    "tiles": "fill_tiles / fill_tiles_batch (K1t budget tiles: one 32-slot tile per CTA, co-resident "
-             "or as a tile-job queue when the tiles outnumber the SMs; the fused walk in the same launch)",
+    "tiles": "fill_tiles / fill_tiles_jobs1 (K1t budget tiles: one 32-slot tile per CTA, co-resident, "
+             "or as a queue of tile jobs when the tiles outnumber the SMs, dominance-pruned open rows; "
+             "the fused walk in the same launch)",
     "queue": "fill_persistent (K1p: one persistent launch, dataflow work queue)",
     "diagonal": "fill_diag (K1: one launch per anti-diagonal)",
 }

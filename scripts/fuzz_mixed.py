@@ -19,7 +19,11 @@ from paper_2307_01236_b200.menu import synthetic_menu  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--seconds", type=float, default=300)
 ap.add_argument("--seed", type=int, default=2024)
+ap.add_argument("--mode", default="mixed", choices=["mixed", "auto", "comm_off"],
+                help="mixed: one-table tile jobs with half tiles (pruned open rows); auto: the "
+                     "default plan (co-resident for small tables); comm_off: no communication warp")
 a = ap.parse_args()
+FLAGS = {"mixed": ("jobs", "mixed"), "auto": (), "comm_off": ("comm_off",)}[a.mode]
 orc = Orc()
 rng = np.random.default_rng(a.seed)
 t_end = time.time() + a.seconds
@@ -33,7 +37,7 @@ while time.time() < t_end:
     st, o, k, v, _, _ = orc.fill(menu, 1, M)
     assert st == 0
     rows = int(rng.integers(0, 3))  # 0 auto, 1, 2
-    with rotor.tuning("jobs", "mixed", tile_rows=rows), rotor.DpTable(menu, 1, M, kernel="tiles") as t:
+    with rotor.tuning(*FLAGS, tile_rows=rows), rotor.DpTable(menu, 1, M, kernel="tiles") as t:
         go, gk, gv = t.download()
         if not (np.array_equal(go, o) and np.array_equal(gk, k) and np.array_equal(gv, v)):
             raise SystemExit(f"MISMATCH L={L} B={B} M={M} tie={tie} rows={rows}")
@@ -48,4 +52,4 @@ while time.time() < t_end:
             raise SystemExit(f"WALK MISMATCH L={L} B={B} M={M} m={m}")
     n += 1
     cells += o.size
-print(f"fuzz_mixed: {n} tables ({cells / 1e6:.1f} M cells) bit-exact against the oracle, walks equal")
+print(f"fuzz_mixed ({a.mode}): {n} tables ({cells / 1e6:.1f} M cells) bit-exact against the oracle, walks equal")
